@@ -1,0 +1,201 @@
+/*
+ * coda.h — C-ABI of the B200-native CODA fused GEMM + epilogue engine.
+ *
+ * The reference (`tilefuse`, /root/reference/pkg/src/tilefuse) is a pure
+ * Python/numpy package with no FFI.  Its drop-in boundary is the Python op /
+ * epilogue-primitive API; the Python package `paper_2605_19269_b200` mirrors
+ * that API and calls these entry points through ctypes.  Each entry point
+ * below names the reference interface it replaces (file:line).
+ *
+ * Conventions
+ *   - Plain pointers, sizes and strides; no torch types.  The caller owns and
+ *     allocates every buffer (inputs, outputs, workspaces); the library never
+ *     allocates device memory and only borrows pointers for the duration of the
+ *     stream-ordered work it enqueues.
+ *   - All work is asynchronous on the caller's `stream` (a cudaStream_t).
+ *   - Return 0 on success, a negative CODA_E_* code on failure (validation
+ *     happens before anything is enqueued).  coda_last_error() returns the
+ *     thread-local message of the last failure.
+ *   - 2-D tensors are row-major with leading dimension `ld` (elements); `ld`
+ *     times the element size must be a multiple of 16 bytes and `ptr` must be
+ *     16-byte aligned (TMA / vector-access requirement).
+ */
+#ifndef CODA_H
+#define CODA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes: 1:1 with the reference taxonomy (errors.py:9-56) ---- */
+#define CODA_OK                 0
+#define CODA_E_DIMENSION       -1   /* DimensionError   errors.py:13 */
+#define CODA_E_BINDING         -2   /* BindingError     errors.py:17 */
+#define CODA_E_PROGRAM         -3   /* ProgramError     errors.py:21 */
+#define CODA_E_PAIRING         -4   /* PairingError     errors.py:26 */
+#define CODA_E_CONFIG          -5   /* ConfigError      errors.py:30 */
+#define CODA_E_LABEL           -6   /* LabelError       errors.py:34 */
+#define CODA_E_DEGENERATE      -7   /* DegenerateError  errors.py:42 */
+#define CODA_E_CUDA            -20  /* device / launch failure */
+
+/* ---- element types ---- */
+#define CODA_BF16  0
+#define CODA_F32   1
+#define CODA_I64   2
+#define CODA_I32   3
+
+/* ---- epilogue op codes: one per reference primitive (epilogue.py:198-593) ---- */
+#define CODA_OP_ROW_VEC_MUL      1   /* RowVecMul          epilogue.py:198 */
+#define CODA_OP_ROW_SCALE        2   /* RowScale           epilogue.py:214 */
+#define CODA_OP_RESIDUAL_ADD     3   /* ResidualAdd        epilogue.py:230 */
+#define CODA_OP_AUX_TILE_STORE   4   /* AuxTileStore       epilogue.py:246 */
+#define CODA_OP_PARTIAL_SUMSQ    5   /* PartialSumSq       epilogue.py:273 */
+#define CODA_OP_PARTIAL_ROWDOT   6   /* PartialRowDot      epilogue.py:294 */
+#define CODA_OP_PARTIAL_COLSUM   7   /* PartialColSum      epilogue.py:319 */
+#define CODA_OP_ONLINE_LSE       8   /* OnlineLse          epilogue.py:338 */
+#define CODA_OP_TARGET_GATHER    9   /* TargetGather       epilogue.py:373 */
+#define CODA_OP_ROPE            10   /* PairwiseRope       epilogue.py:409 */
+#define CODA_OP_SWIGLU          11   /* PairwiseSwiglu     epilogue.py:449 */
+#define CODA_OP_SWIGLU_BWD      12   /* PairwiseSwigluBackward epilogue.py:469 */
+#define CODA_OP_RMSNORM_BWD     13   /* RmsNormBackwardLocal   epilogue.py:522 */
+
+#define CODA_MAX_STEPS     8
+#define CODA_MAX_OPERANDS  8
+#define CODA_MAX_STORES    8
+
+/* A dense 1-D/2-D device tensor.  1-D tensors use rows = 1, cols = length. */
+typedef struct {
+    void*   ptr;
+    int64_t rows;
+    int64_t cols;
+    int64_t ld;      /* leading dimension in elements (2-D) */
+    int32_t dtype;   /* CODA_BF16 / CODA_F32 / CODA_I64 / CODA_I32 */
+    int32_t _pad;
+} coda_tensor_t;
+
+/* One GEMM launch: GemmProblem (engine.py:55-76) after lowering.
+ * storage: CODA_BF16 (SIMBF16) or CODA_F32 (SIM32; A/B are then the
+ * 6-term bf16 split operands produced by coda_split_operand, k = 6*kp). */
+typedef struct {
+    int64_t m, n, k;
+    int32_t trans_a, trans_b;
+    int32_t storage;       /* dtype of side TILE operands and aux TILE stores */
+    int32_t out_dtype;     /* dtype of the main output */
+    int32_t store_main;    /* engine.py:428-430 */
+    int32_t _pad;
+} coda_problem_t;
+
+/* One program step (EpilogueProgram.steps, epilogue.py:606-698).
+ * arg[] holds operand / store slot indices; meaning per op:
+ *   ROW_VEC_MUL    arg0 = operand (row vector)
+ *   ROW_SCALE      arg0 = operand (col vector)
+ *   RESIDUAL_ADD   arg0 = operand (tile)
+ *   AUX_TILE_STORE arg0 = store (tile)
+ *   PARTIAL_SUMSQ  arg0 = store (row-sum pieces)
+ *   PARTIAL_ROWDOT arg0 = operand (tile), arg1 = store (row-sum pieces)
+ *   PARTIAL_COLSUM arg0 = store (col-sum pieces)
+ *   ONLINE_LSE     arg0 = store (row-pair pieces)
+ *   TARGET_GATHER  arg0 = operand (labels, int64), arg1 = store (gather, f32)
+ *   ROPE           arg0 = cos operand, arg1 = sin operand, arg2 = backward flag
+ *   SWIGLU         —
+ *   SWIGLU_BWD     arg0 = preact operand (factor 2), arg1 = recompute store,
+ *                  arg2 = row-sum pieces store (factor 2)
+ *   RMSNORM_BWD    arg0 = pre, arg1 = inv_rms, arg2 = gamma, arg3 = stat,
+ *                  arg4 = accumulate operand or -1, arg5 = normed store,
+ *                  arg6 = gamma-grad col-sum pieces store
+ * width: running width factor at step entry, encoded x2 (1 = 1/2, 2 = 1, 4 = 2). */
+typedef struct {
+    int32_t op;
+    int32_t width2;
+    int32_t arg[7];
+    int32_t _pad;
+} coda_step_t;
+
+/* A partial/aux output.  For row-sum / row-pair / col-sum stores the tensor is
+ * the *piece* buffer and `piece_map` maps every scaled column (row-sum,
+ * row-pair; length n*factor) or every row (col-sum; length m) to its piece
+ * index.  Pieces are reference reduction blocks (epilogue.py:96-130) split at
+ * GPU tile boundaries; coda_combine_* folds them into blocks when they differ. */
+typedef struct {
+    coda_tensor_t  t;
+    const int32_t* piece_map;
+    int32_t        kind;      /* 0 tile, 1 row-sum, 2 row-pair, 3 col-sum, 4 gather */
+    int32_t        _pad;
+} coda_store_t;
+
+/* run_gemm (engine.py:376-464) / run_gemm_trans (engine.py:467-478):
+ * one persistent tcgen05 GEMM whose epilogue executes `steps`. */
+int coda_gemm_epilogue(const coda_problem_t* problem,
+                       const coda_tensor_t* a, const coda_tensor_t* b,
+                       const coda_step_t* steps, int nsteps,
+                       const coda_tensor_t* operands, int noperands,
+                       const coda_store_t* stores, int nstores,
+                       const coda_tensor_t* main_out,      /* NULL iff !store_main */
+                       void* stream);
+
+/* finalize_rms (reductions.py:64-80): r[i] = 1/sqrt(sum_b p[i,b] / d + eps). */
+int coda_finalize_rms(const float* partials, int64_t m, int64_t nb, int64_t ld,
+                      int64_t d, float eps, float* r, void* stream);
+
+/* finalize_rowdot (reductions.py:83-98): s[i] = sum_b p[i,b] / d. */
+int coda_finalize_rowdot(const float* partials, int64_t m, int64_t nb, int64_t ld,
+                         int64_t d, float* s, void* stream);
+
+/* reduce_row_partials (reductions.py:134-145): out[j] = sum_t p[t,j]. */
+int coda_reduce_row_partials(const float* partials, int64_t tm, int64_t n, int64_t ld,
+                             float* out, void* stream);
+
+/* combine_lse (reductions.py:101-131): lse[i] from (max, sum) pairs. */
+int coda_combine_lse(const float* pairs, int64_t m, int64_t nb, int64_t ld,
+                     float* lse, void* stream);
+
+/* cross_entropy_finalize (reductions.py:148-168): loss = lse - target. */
+int coda_cross_entropy_finalize(const float* target, const float* lse, int64_t m,
+                                float* losses, void* stream);
+
+/* rope_backward_stat (kernels.py:560-617): counter-rotated gradient (storage
+ * dtype) plus row-dot partials of grad*rotated over row_block_layout
+ * (`block_start`, nb+1 device offsets: block b covers [start[b], start[b+1])). */
+int coda_rope_backward_stat(const coda_tensor_t* grad, const coda_tensor_t* rotated,
+                            const coda_tensor_t* cos, const coda_tensor_t* sin,
+                            const int32_t* block_start, int64_t nb,
+                            coda_tensor_t* grad_z, float* rowdot, int64_t ld_rowdot,
+                            void* stream);
+
+/* Fold piece partials into reference blocks in ascending piece order.
+ * block_ptr (nb+1, host-built CSR) lists the piece range of each block. */
+int coda_combine_row_pieces(const float* pieces, int64_t m, int64_t np, int64_t ld_p,
+                            const int32_t* block_ptr, int64_t nb, int pairs,
+                            float* out, int64_t ld_o, void* stream);
+int coda_combine_col_pieces(const float* pieces, int64_t np, int64_t n, int64_t ld_p,
+                            const int32_t* block_ptr, int64_t nb,
+                            float* out, int64_t ld_o, void* stream);
+
+/* SIM32 operand preparation: splits an f32 operand into three bf16 terms
+ * x = x0 + x1 + x2 and lays out six K-blocks so that one bf16 GEMM with
+ * k' = 6*kp reproduces the f32 product to ~2^-24 (terms with i+j <= 2).
+ * k_axis: 1 if K runs along columns (A, or trans_b B), 0 if along rows.
+ * pattern: term index for each of the 6 K-blocks. */
+int coda_split_operand(const coda_tensor_t* src, int k_axis, int64_t kp,
+                       const int32_t pattern[6], coda_tensor_t* dst, void* stream);
+
+/* Elementwise storage conversion f32 -> bf16 (RNE), used after an f32
+ * allreduce of weight gradients so rounding happens once (engine.py:443-447). */
+int coda_convert_f32_bf16(const coda_tensor_t* src, coda_tensor_t* dst, void* stream);
+
+/* Number of SMs the persistent kernel sizes its grid for (0 if no device). */
+int coda_num_sms(void);
+
+/* Library build identifier, e.g. "coda sm_100a tcgen05". */
+const char* coda_version(void);
+
+/* Thread-local text of the last error. */
+const char* coda_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CODA_H */

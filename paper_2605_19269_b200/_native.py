@@ -1,0 +1,211 @@
+"""ctypes bridge to the C-ABI declared in include/coda.h.
+
+This is the only module that touches the shared library.  There is no
+fallback: if `libcoda.so` is missing or cannot be loaded, every GPU entry
+point raises `NativeUnavailable` (the product path must fail loudly).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+from . import errors
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libcoda.so"
+
+# ---- constants mirrored from include/coda.h ----
+BF16, F32, I64, I32 = 0, 1, 2, 3
+
+OP_ROW_VEC_MUL = 1
+OP_ROW_SCALE = 2
+OP_RESIDUAL_ADD = 3
+OP_AUX_TILE_STORE = 4
+OP_PARTIAL_SUMSQ = 5
+OP_PARTIAL_ROWDOT = 6
+OP_PARTIAL_COLSUM = 7
+OP_ONLINE_LSE = 8
+OP_TARGET_GATHER = 9
+OP_ROPE = 10
+OP_SWIGLU = 11
+OP_SWIGLU_BWD = 12
+OP_RMSNORM_BWD = 13
+
+STORE_TILE, STORE_ROW_SUM, STORE_ROW_PAIR, STORE_COL_SUM, STORE_GATHER = 0, 1, 2, 3, 4
+
+MAX_STEPS = 8
+MAX_OPERANDS = 8
+MAX_STORES = 8
+
+# GPU tile geometry of the persistent kernel (csrc/coda_gemm.cuh)
+GPU_TILE_M = 128
+GPU_TILE_N = 256
+
+EXPORTS = (
+    "coda_gemm_epilogue",
+    "coda_finalize_rms",
+    "coda_finalize_rowdot",
+    "coda_reduce_row_partials",
+    "coda_combine_lse",
+    "coda_cross_entropy_finalize",
+    "coda_rope_backward_stat",
+    "coda_combine_row_pieces",
+    "coda_combine_col_pieces",
+    "coda_split_operand",
+    "coda_convert_f32_bf16",
+    "coda_num_sms",
+    "coda_version",
+    "coda_last_error",
+)
+
+
+class Tensor(ctypes.Structure):
+    _fields_ = [
+        ("ptr", ctypes.c_void_p),
+        ("rows", ctypes.c_int64),
+        ("cols", ctypes.c_int64),
+        ("ld", ctypes.c_int64),
+        ("dtype", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
+    ]
+
+
+class Problem(ctypes.Structure):
+    _fields_ = [
+        ("m", ctypes.c_int64),
+        ("n", ctypes.c_int64),
+        ("k", ctypes.c_int64),
+        ("trans_a", ctypes.c_int32),
+        ("trans_b", ctypes.c_int32),
+        ("storage", ctypes.c_int32),
+        ("out_dtype", ctypes.c_int32),
+        ("store_main", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
+    ]
+
+
+class Step(ctypes.Structure):
+    _fields_ = [
+        ("op", ctypes.c_int32),
+        ("width2", ctypes.c_int32),
+        ("arg", ctypes.c_int32 * 7),
+        ("_pad", ctypes.c_int32),
+    ]
+
+
+class Store(ctypes.Structure):
+    _fields_ = [
+        ("t", Tensor),
+        ("piece_map", ctypes.c_void_p),
+        ("kind", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
+    ]
+
+
+class NativeUnavailable(errors.TileFuseError):
+    """The CUDA library could not be loaded (no silent CPU fallback exists)."""
+
+
+_lock = threading.Lock()
+_lib = None
+
+_ERRMAP = {
+    -1: errors.DimensionError,
+    -2: errors.BindingError,
+    -3: errors.ProgramError,
+    -4: errors.PairingError,
+    -5: errors.ConfigError,
+    -6: errors.LabelError,
+    -7: errors.DegenerateError,
+}
+
+
+def _declare(lib) -> None:
+    vp, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float
+    P = ctypes.POINTER
+    lib.coda_gemm_epilogue.argtypes = [P(Problem), P(Tensor), P(Tensor), P(Step), i32, P(Tensor), i32,
+                                       P(Store), i32, P(Tensor), vp]
+    lib.coda_finalize_rms.argtypes = [vp, i64, i64, i64, i64, f32, vp, vp]
+    lib.coda_finalize_rowdot.argtypes = [vp, i64, i64, i64, i64, vp, vp]
+    lib.coda_reduce_row_partials.argtypes = [vp, i64, i64, i64, vp, vp]
+    lib.coda_combine_lse.argtypes = [vp, i64, i64, i64, vp, vp]
+    lib.coda_cross_entropy_finalize.argtypes = [vp, vp, i64, vp, vp]
+    lib.coda_rope_backward_stat.argtypes = [P(Tensor), P(Tensor), P(Tensor), P(Tensor), vp, i64, P(Tensor),
+                                            vp, i64, vp]
+    lib.coda_combine_row_pieces.argtypes = [vp, i64, i64, i64, vp, i64, i32, vp, i64, vp]
+    lib.coda_combine_col_pieces.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, vp]
+    lib.coda_split_operand.argtypes = [P(Tensor), i32, i64, P(ctypes.c_int32), P(Tensor), vp]
+    lib.coda_convert_f32_bf16.argtypes = [P(Tensor), P(Tensor), vp]
+    lib.coda_num_sms.argtypes = []
+    lib.coda_version.argtypes = []
+    lib.coda_version.restype = ctypes.c_char_p
+    lib.coda_last_error.argtypes = []
+    lib.coda_last_error.restype = ctypes.c_char_p
+    for name in EXPORTS:
+        if name not in ("coda_version", "coda_last_error"):
+            getattr(lib, name).restype = ctypes.c_int
+
+
+def load(path: Path | None = None):
+    """Load (once) and return the ctypes handle of libcoda.so."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path) if path is not None else LIB_PATH
+        if not p.exists():
+            raise NativeUnavailable(
+                f"CUDA library {p} is missing; run __graft_entry__.build() "
+                f"(there is no CPU fallback)"
+            )
+        try:
+            lib = ctypes.CDLL(str(p))
+        except OSError as exc:  # pragma: no cover - depends on the box
+            raise NativeUnavailable(f"cannot load {p}: {exc}") from exc
+        _declare(lib)
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    """Raise the reference error class that a non-zero return code maps to."""
+    if rc == 0:
+        return
+    msg = (_lib.coda_last_error() or b"").decode(errors="replace") if _lib is not None else ""
+    cls = _ERRMAP.get(rc)
+    if cls is None:
+        raise RuntimeError(f"CUDA error in CODA library ({rc}): {msg}")
+    raise cls(msg)
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    check(getattr(lib, name)(*args))
+
+
+def tensor_desc(t, dtype_code: int | None = None) -> Tensor:
+    """Describe a 1-D or 2-D torch CUDA tensor (row-major, unit column stride)."""
+    import torch
+
+    code = dtype_code if dtype_code is not None else dtype_of(t)
+    if t.dim() == 1:
+        if t.stride(0) != 1:
+            raise errors.BindingError("vector operands must be contiguous")
+        return Tensor(t.data_ptr(), 1, t.shape[0], t.shape[0], code, 0)
+    if t.dim() != 2:
+        raise errors.DimensionError(f"expected a 1-D or 2-D tensor, got {t.dim()}-D")
+    if t.stride(1) != 1 and t.shape[1] > 1:
+        raise errors.BindingError("matrices must have unit column stride")
+    ld = t.stride(0) if t.shape[0] > 1 else max(t.stride(0), t.shape[1])
+    return Tensor(t.data_ptr(), t.shape[0], t.shape[1], ld, code, 0)
+
+
+def dtype_of(t) -> int:
+    import torch
+
+    m = {torch.bfloat16: BF16, torch.float32: F32, torch.int64: I64, torch.int32: I32}
+    if t.dtype not in m:
+        raise errors.BindingError(f"unsupported device dtype {t.dtype}")
+    return m[t.dtype]

@@ -1,0 +1,451 @@
+// coda_api.cu — extern "C" entry points declared in include/coda.h.
+//
+// Validation happens here, before anything is enqueued, and maps onto the
+// reference error taxonomy (errors.py:9-56).  The library never allocates
+// device memory; TMA descriptors are encoded on the host per launch (cached)
+// and passed as __grid_constant__ kernel parameters.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "../../include/coda.h"
+#include "coda_aux.cuh"
+#include "coda_gemm.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) return fail(CODA_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return CODA_OK;
+}
+
+int esize(int dtype) {
+    switch (dtype) {
+    case CODA_BF16: return 2;
+    case CODA_F32: return 4;
+    case CODA_I64: return 8;
+    case CODA_I32: return 4;
+    default: return 0;
+    }
+}
+
+// Make the runtime's current device the one owning `ptr` (torch may run on any device).
+int bind_device(const void* ptr) {
+    cudaPointerAttributes at{};
+    cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CODA_E_BINDING, "pointer %p is not a CUDA allocation", ptr);
+    }
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+        return fail(CODA_E_BINDING, "pointer %p is not device memory", ptr);
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != at.device) {
+        if (cudaSetDevice(at.device) != cudaSuccess) return fail(CODA_E_CUDA, "cudaSetDevice(%d) failed", at.device);
+    }
+    return CODA_OK;
+}
+
+int check_tensor2d(const coda_tensor_t* t, const char* name, int dtype) {
+    if (!t || !t->ptr) return fail(CODA_E_BINDING, "%s: null tensor", name);
+    if (t->dtype != dtype) return fail(CODA_E_BINDING, "%s: dtype %d, expected %d", name, t->dtype, dtype);
+    if (t->rows <= 0 || t->cols <= 0) return fail(CODA_E_DIMENSION, "%s: non-positive shape", name);
+    const int es = esize(dtype);
+    if ((reinterpret_cast<uintptr_t>(t->ptr) & 15) != 0)
+        return fail(CODA_E_BINDING, "%s: base pointer must be 16-byte aligned", name);
+    if (t->rows > 1 && ((t->ld * es) % 16 != 0 || t->ld < t->cols))
+        return fail(CODA_E_BINDING, "%s: leading dimension %lld invalid (needs >= cols and 16-byte rows)",
+                    name, (long long)t->ld);
+    return CODA_OK;
+}
+
+// ---------------------------------------------------------------- TMA descriptors
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+struct MapKey {
+    const void* ptr;
+    uint64_t d0, d1, stride;
+    uint32_t b0, b1;
+    bool operator==(const MapKey& o) const {
+        return ptr == o.ptr && d0 == o.d0 && d1 == o.d1 && stride == o.stride && b0 == o.b0 && b1 == o.b1;
+    }
+};
+struct MapKeyHash {
+    size_t operator()(const MapKey& k) const {
+        size_t h = std::hash<const void*>()(k.ptr);
+        h ^= std::hash<uint64_t>()(k.d0 * 1315423911ull + k.d1) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+        h ^= std::hash<uint64_t>()(k.stride * 2654435761ull + k.b0 * 131 + k.b1) + (h << 6) + (h >> 2);
+        return h;
+    }
+};
+
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+// 2-D bf16 tensor map, dim0 innermost (contiguous), SWIZZLE_128B, OOB -> zero.
+int make_map(CUtensorMap* out, const void* ptr, uint64_t d0, uint64_t d1, uint64_t row_bytes, uint32_t b0,
+             uint32_t b1) {
+    MapKey key{ptr, d0, d1, row_bytes, b0, b1};
+    {
+        std::lock_guard<std::mutex> lk(g_map_mu);
+        auto it = g_maps.find(key);
+        if (it != g_maps.end()) {
+            *out = it->second;
+            return CODA_OK;
+        }
+    }
+    auto enc = get_encode();
+    if (!enc) return fail(CODA_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {d0, d1};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {b0, b1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(CODA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    if (g_maps.size() > 4096) g_maps.clear();
+    g_maps.emplace(key, *out);
+    return CODA_OK;
+}
+
+int g_num_sms = -1;
+int num_sms() {
+    if (g_num_sms < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+        g_num_sms = n;
+    }
+    return g_num_sms;
+}
+
+template <typename TS>
+int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const coda::GemmParams& P, cudaStream_t st) {
+    static bool configured = false;
+    const size_t smem = coda::gemm_smem_bytes();
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(coda::coda_gemm_kernel<TS>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(gemm smem)");
+        configured = true;
+    }
+    const int nsm = num_sms();
+    const int grid = P.ntiles < nsm ? P.ntiles : nsm;
+    coda::coda_gemm_kernel<TS><<<grid, coda::NUM_THREADS, smem, st>>>(ma, mb, P);
+    return cuda_check(cudaGetLastError(), "coda_gemm_kernel launch");
+}
+
+inline unsigned grid1d(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+}  // namespace
+
+extern "C" {
+
+const char* coda_last_error(void) { return g_err.c_str(); }
+
+const char* coda_version(void) { return "coda sm_100a tcgen05 128x256x64 4-stage persistent"; }
+
+int coda_num_sms(void) { return num_sms(); }
+
+int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const coda_tensor_t* b,
+                       const coda_step_t* steps, int nsteps, const coda_tensor_t* operands, int noperands,
+                       const coda_store_t* stores, int nstores, const coda_tensor_t* main_out, void* stream) {
+    if (!pr) return fail(CODA_E_BINDING, "null problem");
+    const int64_t M = pr->m, N = pr->n, K = pr->k;
+    if (M <= 0 || N <= 0 || K <= 0) return fail(CODA_E_DIMENSION, "problem dims must be positive");
+    if (M > INT32_MAX / 2 || N > INT32_MAX / 4 || K > INT32_MAX / 2) return fail(CODA_E_DIMENSION, "problem too large");
+    if (pr->storage != CODA_BF16 && pr->storage != CODA_F32)
+        return fail(CODA_E_CONFIG, "storage dtype must be bf16 or f32");
+    int rc;
+    if ((rc = check_tensor2d(a, "a", CODA_BF16))) return rc;
+    if ((rc = check_tensor2d(b, "b", CODA_BF16))) return rc;
+    const int64_t ar = pr->trans_a ? K : M, ac = pr->trans_a ? M : K;
+    const int64_t br = pr->trans_b ? N : K, bc = pr->trans_b ? K : N;
+    if (a->rows != ar || a->cols != ac)
+        return fail(CODA_E_DIMENSION, "a has shape (%lld,%lld), problem wants (%lld,%lld)", (long long)a->rows,
+                    (long long)a->cols, (long long)ar, (long long)ac);
+    if (b->rows != br || b->cols != bc)
+        return fail(CODA_E_DIMENSION, "b has shape (%lld,%lld), problem wants (%lld,%lld)", (long long)b->rows,
+                    (long long)b->cols, (long long)br, (long long)bc);
+    if (nsteps < 0 || nsteps > CODA_MAX_STEPS) return fail(CODA_E_PROGRAM, "too many program steps (%d)", nsteps);
+    if (noperands < 0 || noperands > CODA_MAX_OPERANDS || nstores < 0 || nstores > CODA_MAX_STORES)
+        return fail(CODA_E_PROGRAM, "too many operands/stores");
+    if ((rc = bind_device(a->ptr))) return rc;
+
+    coda::GemmParams P;
+    memset(&P, 0, sizeof(P));
+    P.M = (int)M;
+    P.N = (int)N;
+    P.K = (int)K;
+    P.ntm = (int)((M + coda::BM - 1) / coda::BM);
+    P.ntn = (int)((N + coda::BN - 1) / coda::BN);
+    P.nk = (int)((K + coda::BK - 1) / coda::BK);
+    P.ntiles = P.ntm * P.ntn;
+    P.a_mn = pr->trans_a ? 1 : 0;
+    P.b_mn = pr->trans_b ? 0 : 1;
+    P.nsteps = nsteps;
+    P.store_main = pr->store_main ? 1 : 0;
+    P.out_f32 = pr->out_dtype == CODA_F32 ? 1 : 0;
+
+    const int sdt = pr->storage;
+    int w = 32;
+    for (int s = 0; s < nsteps; ++s) {
+        const coda_step_t& cs = steps[s];
+        coda::DevStep& d = P.steps[s];
+        d.op = cs.op;
+        d.w = cs.width2 * 16;
+        for (int i = 0; i < 7; ++i) d.a[i] = cs.arg[i];
+        if (d.w != w) return fail(CODA_E_PROGRAM, "step %d: width %d does not match running width %d", s, d.w, w);
+        auto opnd_ok = [&](int i) { return i >= 0 && i < noperands; };
+        auto store_ok = [&](int i) { return i >= 0 && i < nstores; };
+        bool ok = true;
+        switch (cs.op) {
+        case CODA_OP_ROW_VEC_MUL: case CODA_OP_ROW_SCALE: case CODA_OP_RESIDUAL_ADD: ok = opnd_ok(cs.arg[0]); break;
+        case CODA_OP_AUX_TILE_STORE: case CODA_OP_PARTIAL_COLSUM: ok = store_ok(cs.arg[0]); break;
+        case CODA_OP_PARTIAL_SUMSQ: case CODA_OP_ONLINE_LSE:
+            ok = store_ok(cs.arg[0]) && w == 32 && (cs.arg[6] == 0 || cs.arg[6] == 1); break;
+        case CODA_OP_PARTIAL_ROWDOT:
+            ok = opnd_ok(cs.arg[0]) && store_ok(cs.arg[1]) && w == 32 && (cs.arg[6] == 0 || cs.arg[6] == 1); break;
+        case CODA_OP_TARGET_GATHER: ok = opnd_ok(cs.arg[0]) && store_ok(cs.arg[1]) && w == 32; break;
+        case CODA_OP_ROPE: ok = opnd_ok(cs.arg[0]) && opnd_ok(cs.arg[1]); break;
+        case CODA_OP_SWIGLU:
+            if (w == 16) return fail(CODA_E_CONFIG, "GPU epilogue supports running width factors 1/2, 1, 2");
+            w /= 2; break;
+        case CODA_OP_SWIGLU_BWD:
+            ok = opnd_ok(cs.arg[0]) && store_ok(cs.arg[1]) && store_ok(cs.arg[2]) && w == 32 &&
+                 (cs.arg[6] == 0 || cs.arg[6] == 1);
+            w = 64; break;
+        case CODA_OP_RMSNORM_BWD:
+            ok = opnd_ok(cs.arg[0]) && opnd_ok(cs.arg[1]) && opnd_ok(cs.arg[2]) && opnd_ok(cs.arg[3]) &&
+                 (cs.arg[4] == -1 || opnd_ok(cs.arg[4])) && store_ok(cs.arg[5]) && store_ok(cs.arg[6]) && w == 32;
+            break;
+        default: return fail(CODA_E_PROGRAM, "step %d: unknown op %d", s, cs.op);
+        }
+        if (!ok) return fail(CODA_E_PROGRAM, "step %d (op %d): bad slot index or width", s, cs.op);
+    }
+    P.out_w = w;
+    for (int i = 0; i < noperands; ++i) {
+        const coda_tensor_t& t = operands[i];
+        if (!t.ptr) return fail(CODA_E_BINDING, "operand %d is null", i);
+        if (t.rows > 1 && t.dtype == sdt) {
+            char nm[32];
+            snprintf(nm, sizeof(nm), "operand %d", i);
+            if ((rc = check_tensor2d(&t, nm, sdt))) return rc;
+            if (t.rows != M) return fail(CODA_E_DIMENSION, "operand %d has %lld rows, expected %lld", i,
+                                         (long long)t.rows, (long long)M);
+        }
+        P.opnd[i].ptr = t.ptr;
+        P.opnd[i].ld = t.ld;
+        P.opnd[i].cols = t.cols;
+    }
+    for (int i = 0; i < nstores; ++i) {
+        const coda_store_t& s = stores[i];
+        if (!s.t.ptr) return fail(CODA_E_BINDING, "store %d is null", i);
+        if (s.kind == 0) {
+            char nm[32];
+            snprintf(nm, sizeof(nm), "store %d", i);
+            if ((rc = check_tensor2d(&s.t, nm, sdt))) return rc;
+        } else if (s.kind >= 1 && s.kind <= 3 && !s.piece_map) {
+            return fail(CODA_E_BINDING, "store %d needs a piece map", i);
+        }
+        P.store[i].ptr = s.t.ptr;
+        P.store[i].ld = s.t.ld;
+        P.store[i].cols = s.t.cols;
+        P.store[i].map = s.piece_map;
+    }
+    if (P.store_main) {
+        const int odt = P.out_f32 ? CODA_F32 : CODA_BF16;
+        if ((rc = check_tensor2d(main_out, "main", odt))) return rc;
+        const int64_t want = N * w / 32;
+        if (main_out->rows != M || main_out->cols != want)
+            return fail(CODA_E_DIMENSION, "main output has shape (%lld,%lld), expected (%lld,%lld)",
+                        (long long)main_out->rows, (long long)main_out->cols, (long long)M, (long long)want);
+        P.out = main_out->ptr;
+        P.ld_out = main_out->ld;
+    }
+
+    CUtensorMap ma, mb;
+    if (!pr->trans_a) rc = make_map(&ma, a->ptr, (uint64_t)K, (uint64_t)M, (uint64_t)a->ld * 2, coda::BK, coda::BM);
+    else rc = make_map(&ma, a->ptr, (uint64_t)M, (uint64_t)K, (uint64_t)a->ld * 2, 64, coda::BK);
+    if (rc) return rc;
+    if (pr->trans_b) rc = make_map(&mb, b->ptr, (uint64_t)K, (uint64_t)N, (uint64_t)b->ld * 2, coda::BK, coda::BN);
+    else rc = make_map(&mb, b->ptr, (uint64_t)N, (uint64_t)K, (uint64_t)b->ld * 2, 64, coda::BK);
+    if (rc) return rc;
+
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (sdt == CODA_BF16) return launch_gemm<__nv_bfloat16>(ma, mb, P, st);
+    return launch_gemm<float>(ma, mb, P, st);
+}
+
+int coda_finalize_rms(const float* p, int64_t m, int64_t nb, int64_t ld, int64_t d, float eps, float* r,
+                      void* stream) {
+    if (m <= 0 || nb <= 0) return fail(CODA_E_DIMENSION, "finalize_rms: empty partials");
+    if (d <= 0) return fail(CODA_E_DEGENERATE, "partial blocks cover no columns");
+    int rc;
+    if ((rc = bind_device(p))) return rc;
+    coda::finalize_rms_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(p, m, nb, ld, (float)d, eps, r);
+    return cuda_check(cudaGetLastError(), "finalize_rms");
+}
+
+int coda_finalize_rowdot(const float* p, int64_t m, int64_t nb, int64_t ld, int64_t d, float* s, void* stream) {
+    if (m <= 0 || nb <= 0) return fail(CODA_E_DIMENSION, "finalize_rowdot: empty partials");
+    if (d <= 0) return fail(CODA_E_CONFIG, "normalized width must be positive, got %lld", (long long)d);
+    int rc;
+    if ((rc = bind_device(p))) return rc;
+    coda::finalize_rowdot_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(p, m, nb, ld, (float)d, s);
+    return cuda_check(cudaGetLastError(), "finalize_rowdot");
+}
+
+int coda_reduce_row_partials(const float* p, int64_t tm, int64_t n, int64_t ld, float* out, void* stream) {
+    if (tm <= 0 || n <= 0) return fail(CODA_E_DIMENSION, "reduce_row_partials: empty partials");
+    int rc;
+    if ((rc = bind_device(p))) return rc;
+    coda::reduce_row_partials_kernel<<<grid1d(n, 256), 256, 0, (cudaStream_t)stream>>>(p, tm, n, ld, out);
+    return cuda_check(cudaGetLastError(), "reduce_row_partials");
+}
+
+int coda_combine_lse(const float* p, int64_t m, int64_t nb, int64_t ld, float* lse, void* stream) {
+    if (m <= 0 || nb <= 0) return fail(CODA_E_DIMENSION, "combine_lse: empty partials");
+    int rc;
+    if ((rc = bind_device(p))) return rc;
+    coda::combine_lse_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(p, m, nb, ld, lse);
+    return cuda_check(cudaGetLastError(), "combine_lse");
+}
+
+int coda_cross_entropy_finalize(const float* target, const float* lse, int64_t m, float* losses, void* stream) {
+    if (m <= 0) return fail(CODA_E_DIMENSION, "cross_entropy_finalize: empty");
+    int rc;
+    if ((rc = bind_device(lse))) return rc;
+    coda::ce_finalize_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(target, lse, m, losses);
+    return cuda_check(cudaGetLastError(), "cross_entropy_finalize");
+}
+
+int coda_rope_backward_stat(const coda_tensor_t* grad, const coda_tensor_t* rotated, const coda_tensor_t* cos,
+                            const coda_tensor_t* sin, const int32_t* block_start, int64_t nb, coda_tensor_t* grad_z,
+                            float* rowdot, int64_t ld_rowdot, void* stream) {
+    if (!grad) return fail(CODA_E_BINDING, "null grad");
+    const int dt = grad->dtype;
+    if (dt != CODA_BF16 && dt != CODA_F32) return fail(CODA_E_CONFIG, "rope_backward_stat: bad dtype");
+    int rc;
+    const coda_tensor_t* ts[5] = {grad, rotated, cos, sin, grad_z};
+    const char* nm[5] = {"grad", "rotated", "cos", "sin", "grad_z"};
+    for (int i = 0; i < 5; ++i) {
+        if ((rc = check_tensor2d(ts[i], nm[i], dt))) return rc;
+        if (ts[i]->rows != grad->rows || ts[i]->cols != grad->cols)
+            return fail(CODA_E_DIMENSION, "%s has shape (%lld,%lld), expected (%lld,%lld)", nm[i],
+                        (long long)ts[i]->rows, (long long)ts[i]->cols, (long long)grad->rows,
+                        (long long)grad->cols);
+    }
+    if (grad->cols % 2) return fail(CODA_E_DIMENSION, "rotary width must be even, got %lld", (long long)grad->cols);
+    const size_t smem = (size_t)grad->cols * 4;
+    if (smem > 200 * 1024) return fail(CODA_E_CONFIG, "rope_backward_stat: row too wide (%lld)", (long long)grad->cols);
+    if ((rc = bind_device(grad->ptr))) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dt == CODA_BF16) {
+        auto k = coda::rope_backward_stat_kernel<__nv_bfloat16>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        k<<<(unsigned)grad->rows, 256, smem, st>>>(
+            (const __nv_bfloat16*)grad->ptr, grad->ld, (const __nv_bfloat16*)rotated->ptr, rotated->ld,
+            (const __nv_bfloat16*)cos->ptr, cos->ld, (const __nv_bfloat16*)sin->ptr, sin->ld, grad->cols, block_start,
+            nb, (__nv_bfloat16*)grad_z->ptr, grad_z->ld, rowdot, ld_rowdot);
+    } else {
+        auto k = coda::rope_backward_stat_kernel<float>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        k<<<(unsigned)grad->rows, 256, smem, st>>>(
+            (const float*)grad->ptr, grad->ld, (const float*)rotated->ptr, rotated->ld, (const float*)cos->ptr, cos->ld,
+            (const float*)sin->ptr, sin->ld, grad->cols, block_start, nb, (float*)grad_z->ptr, grad_z->ld, rowdot,
+            ld_rowdot);
+    }
+    return cuda_check(cudaGetLastError(), "rope_backward_stat");
+}
+
+int coda_combine_row_pieces(const float* pieces, int64_t m, int64_t np, int64_t ldp, const int32_t* block_ptr,
+                            int64_t nb, int pairs, float* out, int64_t ldo, void* stream) {
+    if (m <= 0 || np <= 0 || nb <= 0) return fail(CODA_E_DIMENSION, "combine_row_pieces: empty");
+    int rc;
+    if ((rc = bind_device(pieces))) return rc;
+    coda::combine_row_pieces_kernel<<<grid1d(m * nb, 256), 256, 0, (cudaStream_t)stream>>>(
+        pieces, m, np, ldp, block_ptr, nb, pairs, out, ldo);
+    return cuda_check(cudaGetLastError(), "combine_row_pieces");
+}
+
+int coda_combine_col_pieces(const float* pieces, int64_t np, int64_t n, int64_t ldp, const int32_t* block_ptr,
+                            int64_t nb, float* out, int64_t ldo, void* stream) {
+    if (n <= 0 || np <= 0 || nb <= 0) return fail(CODA_E_DIMENSION, "combine_col_pieces: empty");
+    if (nb > 65535) return fail(CODA_E_CONFIG, "combine_col_pieces: too many blocks");
+    int rc;
+    if ((rc = bind_device(pieces))) return rc;
+    dim3 grid(grid1d(n, 256), (unsigned)nb);
+    coda::combine_col_pieces_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(pieces, np, n, ldp, block_ptr, nb, out, ldo);
+    return cuda_check(cudaGetLastError(), "combine_col_pieces");
+}
+
+int coda_split_operand(const coda_tensor_t* src, int k_axis, int64_t kp, const int32_t pattern[6],
+                       coda_tensor_t* dst, void* stream) {
+    int rc;
+    if ((rc = check_tensor2d(src, "split src", CODA_F32))) return rc;
+    if ((rc = check_tensor2d(dst, "split dst", CODA_BF16))) return rc;
+    const int64_t kk = k_axis ? src->cols : src->rows;
+    if (kp < kk) return fail(CODA_E_DIMENSION, "split: kp < K");
+    const int64_t drows = k_axis ? src->rows : 6 * kp, dcols = k_axis ? 6 * kp : src->cols;
+    if (dst->rows != drows || dst->cols != dcols) return fail(CODA_E_DIMENSION, "split: dst shape mismatch");
+    coda::SplitPattern pat;
+    for (int i = 0; i < 6; ++i) {
+        if (pattern[i] < 0 || pattern[i] > 2) return fail(CODA_E_CONFIG, "split: bad pattern");
+        pat.t[i] = pattern[i];
+    }
+    if ((rc = bind_device(src->ptr))) return rc;
+    coda::split_operand_kernel<<<grid1d(drows * dcols, 256), 256, 0, (cudaStream_t)stream>>>(
+        (const float*)src->ptr, src->rows, src->cols, src->ld, k_axis, kp, pat, (__nv_bfloat16*)dst->ptr, drows,
+        dcols, dst->ld);
+    return cuda_check(cudaGetLastError(), "split_operand");
+}
+
+int coda_convert_f32_bf16(const coda_tensor_t* src, coda_tensor_t* dst, void* stream) {
+    if (!src || !dst || !src->ptr || !dst->ptr) return fail(CODA_E_BINDING, "convert: null tensor");
+    if (src->dtype != CODA_F32 || dst->dtype != CODA_BF16) return fail(CODA_E_BINDING, "convert: dtypes");
+    if (src->rows != dst->rows || src->cols != dst->cols) return fail(CODA_E_DIMENSION, "convert: shapes differ");
+    int rc;
+    if ((rc = bind_device(src->ptr))) return rc;
+    coda::convert_f32_bf16_kernel<<<grid1d(src->rows * src->cols, 256), 256, 0, (cudaStream_t)stream>>>(
+        (const float*)src->ptr, src->rows, src->cols, src->ld, (__nv_bfloat16*)dst->ptr, dst->ld);
+    return cuda_check(cudaGetLastError(), "convert_f32_bf16");
+}
+
+}  // extern "C"

@@ -1,0 +1,197 @@
+// coda_aux.cuh — the HBM-bound kernels around the fused GEMMs:
+//   second-level reductions (reductions.py:64-168), the boundary RoPE
+//   backward pass (kernels.py:560-617), piece->block folds, the SIM32
+//   operand split and f32->bf16 storage conversion.
+// All reductions run in a fixed ascending order with no atomics, so every
+// launch is bit-reproducible (reductions.py:1-12).
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+#include "coda_gemm.cuh"
+
+namespace coda {
+
+// r = 1 / sqrt(total / d + eps), total summed over blocks in ascending order.
+// IEEE-rounded intrinsics keep the float32 op sequence of reductions.py:74-78.
+__global__ void finalize_rms_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
+                                    float d, float eps, float* __restrict__ r) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const float* row = p + i * ld;
+    float t = 0.0f;
+    for (int64_t b = 0; b < nb; ++b) t = __fadd_rn(t, row[b]);
+    r[i] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(t, d), eps)));
+}
+
+__global__ void finalize_rowdot_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
+                                       float d, float* __restrict__ s) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const float* row = p + i * ld;
+    float t = 0.0f;
+    for (int64_t b = 0; b < nb; ++b) t = __fadd_rn(t, row[b]);
+    s[i] = __fdiv_rn(t, d);
+}
+
+// Column totals over tile rows (coalesced: one thread per column).
+__global__ void reduce_row_partials_kernel(const float* __restrict__ p, int64_t tm, int64_t n, int64_t ld,
+                                           float* __restrict__ out) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    float t = 0.0f;
+    for (int64_t b = 0; b < tm; ++b) t = __fadd_rn(t, p[b * ld + j]);
+    out[j] = t;
+}
+
+__device__ __forceinline__ void lse_merge(float& m, float& s, float mb, float sb) {
+    const float mn = fmaxf(m, mb);
+    const float so = (m == -INFINITY) ? 0.0f : expf(m - mn);
+    const float sn = (mb == -INFINITY) ? 0.0f : expf(mb - mn);
+    s = s * so + sb * sn;
+    m = mn;
+}
+
+__global__ void combine_lse_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
+                                   float* __restrict__ lse) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    float mx = -INFINITY, s = 0.0f;
+    for (int64_t b = 0; b < nb; ++b) lse_merge(mx, s, p[i * ld + 2 * b], p[i * ld + 2 * b + 1]);
+    lse[i] = (mx == -INFINITY) ? NAN : mx + logf(s);
+}
+
+__global__ void ce_finalize_kernel(const float* __restrict__ target, const float* __restrict__ lse, int64_t m,
+                                   float* __restrict__ loss) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) loss[i] = lse[i] - target[i];
+}
+
+// pieces (m, np) -> blocks (m, nb): block b sums pieces [ptr[b], ptr[b+1]).
+__global__ void combine_row_pieces_kernel(const float* __restrict__ pc, int64_t m, int64_t np, int64_t ldp,
+                                          const int32_t* __restrict__ ptr, int64_t nb, int pairs,
+                                          float* __restrict__ out, int64_t ldo) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= m * nb) return;
+    const int64_t i = idx / nb, b = idx % nb;
+    const float* row = pc + i * ldp;
+    if (!pairs) {
+        float t = 0.0f;
+        for (int p = ptr[b]; p < ptr[b + 1]; ++p) t += row[p];
+        out[i * ldo + b] = t;
+    } else {
+        float mx = -INFINITY, s = 0.0f;
+        for (int p = ptr[b]; p < ptr[b + 1]; ++p) lse_merge(mx, s, row[2 * p], row[2 * p + 1]);
+        out[i * ldo + 2 * b] = mx;
+        out[i * ldo + 2 * b + 1] = s;
+    }
+}
+
+// pieces (np, n) -> blocks (nb, n)
+__global__ void combine_col_pieces_kernel(const float* __restrict__ pc, int64_t np, int64_t n, int64_t ldp,
+                                          const int32_t* __restrict__ ptr, int64_t nb,
+                                          float* __restrict__ out, int64_t ldo) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t b = blockIdx.y;
+    if (j >= n || b >= nb) return;
+    float t = 0.0f;
+    for (int p = ptr[b]; p < ptr[b + 1]; ++p) t += pc[(int64_t)p * ldp + j];
+    out[b * ldo + j] = t;
+}
+
+// Boundary RoPE backward (kernels.py:589-606).  One CTA per row:
+//   grad_z[2k]   =  g0*cos[2k]   + g1*sin[2k]
+//   grad_z[2k+1] = -g0*sin[2k+1] + g1*cos[2k+1]
+//   rowdot[b]    = sum_{c in block b} grad[c] * rotated[c]   (ascending c)
+// The products are staged in shared memory so each block is reduced by one
+// thread in column order (deterministic, no atomics).
+template <typename TS>
+__global__ void __launch_bounds__(256)
+rope_backward_stat_kernel(const TS* __restrict__ g, int64_t ldg, const TS* __restrict__ rot, int64_t ldr,
+                          const TS* __restrict__ cs, int64_t ldc, const TS* __restrict__ sn, int64_t lds,
+                          int64_t n, const int32_t* __restrict__ bstart, int64_t nb,
+                          TS* __restrict__ gz, int64_t ldz, float* __restrict__ rowdot, int64_t ldd) {
+    extern __shared__ float prod[];
+    const int64_t i = blockIdx.x;
+    constexpr int V = Io<TS>::V;
+    const TS* gr = g + i * ldg;
+    const TS* rr = rot + i * ldr;
+    const TS* cr = cs + i * ldc;
+    const TS* sr = sn + i * lds;
+    TS* zr = gz + i * ldz;
+    for (int64_t c0 = (int64_t)threadIdx.x * V; c0 < n; c0 += (int64_t)blockDim.x * V) {
+        float gv[V], rv[V], cv[V], sv[V], zv[V];
+        if (c0 + V <= n) {
+            Io<TS>::load(gr + c0, gv);
+            Io<TS>::load(rr + c0, rv);
+            Io<TS>::load(cr + c0, cv);
+            Io<TS>::load(sr + c0, sv);
+        } else {
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                const bool ok = c0 + e < n;
+                gv[e] = ok ? Io<TS>::load1(gr + c0 + e) : 0.f;
+                rv[e] = ok ? Io<TS>::load1(rr + c0 + e) : 0.f;
+                cv[e] = ok ? Io<TS>::load1(cr + c0 + e) : 0.f;
+                sv[e] = ok ? Io<TS>::load1(sr + c0 + e) : 0.f;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < V / 2; ++k) {
+            const float g0 = gv[2 * k], g1 = gv[2 * k + 1];
+            zv[2 * k] = g0 * cv[2 * k] + g1 * sv[2 * k];
+            zv[2 * k + 1] = -g0 * sv[2 * k + 1] + g1 * cv[2 * k + 1];
+        }
+#pragma unroll
+        for (int e = 0; e < V; ++e)
+            if (c0 + e < n) prod[c0 + e] = gv[e] * rv[e];
+        store_seg<TS, V>(zr, c0, n, zv);
+    }
+    __syncthreads();
+    for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) {
+        float t = 0.0f;
+        for (int c = bstart[b]; c < bstart[b + 1]; ++c) t += prod[c];
+        rowdot[i * ldd + b] = t;
+    }
+}
+
+// SIM32 split: x = x0 + x1 + x2 with x0 = bf16(x), x1 = bf16(x - x0), x2 = bf16(x - x0 - x1)
+// (each difference is exact in f32).  dst holds 6 K-blocks of kp, block j = term pattern[j].
+struct SplitPattern { int t[6]; };
+
+__device__ __forceinline__ float split_term(float x, int term) {
+    const float x0 = __bfloat162float(__float2bfloat16_rn(x));
+    if (term == 0) return x0;
+    const float r1 = x - x0;
+    const float x1 = __bfloat162float(__float2bfloat16_rn(r1));
+    if (term == 1) return x1;
+    return r1 - x1;   // rounded to bf16 on store
+}
+
+__global__ void split_operand_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
+                                     int k_axis, int64_t kp, SplitPattern pat,
+                                     __nv_bfloat16* __restrict__ dst, int64_t drows, int64_t dcols, int64_t ldd) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= drows * dcols) return;
+    const int64_t r = idx / dcols, c = idx % dcols;
+    float val = 0.0f;
+    if (k_axis == 1) {          // K along columns: dst (rows, 6kp)
+        const int j = (int)(c / kp);
+        const int64_t k = c % kp;
+        if (k < cols) val = split_term(src[r * lds + k], pat.t[j]);
+    } else {                    // K along rows: dst (6kp, cols)
+        const int j = (int)(r / kp);
+        const int64_t k = r % kp;
+        if (k < rows) val = split_term(src[k * lds + c], pat.t[j]);
+    }
+    dst[r * ldd + c] = __float2bfloat16_rn(val);
+}
+
+__global__ void convert_f32_bf16_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
+                                        __nv_bfloat16* __restrict__ dst, int64_t ldd) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= rows * cols) return;
+    const int64_t r = idx / cols, c = idx % cols;
+    dst[r * ldd + c] = __float2bfloat16_rn(src[r * lds + c]);
+}
+
+}  // namespace coda

@@ -1,0 +1,696 @@
+// coda_gemm.cuh — the fixed GEMM mainloop with a composable epilogue.
+//
+// One persistent, warp-specialised sm_100a kernel replaces the reference's
+// simulated launch `run_gemm` (pkg/src/tilefuse/engine.py:376-464):
+//
+//   warp 0      TMA producer: 4-stage SWIZZLE_128B smem ring of A/B k-blocks
+//   warp 1      MMA issuer:   tcgen05.mma.cta_group::1.kind::f16, 128x256 tile,
+//                             f32 accumulator in TMEM, double-buffered (2 x 256 cols)
+//   warps 2..5  epilogue:     tcgen05.ld.32x32b -> registers (thread == tile row),
+//                             runs the program steps (epilogue.py:606-698) on
+//                             32-column chunks, stores with 16-byte vectors,
+//                             while the MMA warp runs the next tile's mainloop.
+//
+// Operand majorness follows the reference's layouts (engine.py:402-403, 436-437):
+//   A (m,k) -> K-major,  A (k,m) [trans_a] -> MN-major
+//   B (k,n) -> MN-major, B (n,k) [trans_b] -> K-major
+// Both are expressed purely through the TMA boxes and UMMA smem descriptors,
+// so the same binary serves forward (NN), dgrad (NT) and wgrad (TN).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include "coda_ptx.cuh"
+
+namespace coda {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;                 // one 128-byte swizzle atom of bf16 along K
+constexpr int STAGES = 4;
+constexpr int A_STAGE_BYTES = BM * BK * 2;   // 16 KiB
+constexpr int B_STAGE_BYTES = BN * BK * 2;   // 32 KiB
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int EPI_WARPS = 4;
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;   // producer, mma, 4 epilogue warps
+constexpr int CHUNK = 32;                    // accumulator columns per tcgen05.ld
+constexpr int RED_LD = 33;                   // padded row stride of the col-sum scratch
+constexpr int TMEM_COLS = 512;               // 2 accumulator buffers x 256 columns
+constexpr int RASTER_GROUP = 16;             // m-tiles per raster group (L2 reuse)
+
+constexpr int MAX_STEPS = 8;
+constexpr int MAX_SLOTS = 8;
+
+enum OpCode : int {
+    OP_ROW_VEC_MUL = 1, OP_ROW_SCALE = 2, OP_RESIDUAL_ADD = 3, OP_AUX_TILE_STORE = 4,
+    OP_PARTIAL_SUMSQ = 5, OP_PARTIAL_ROWDOT = 6, OP_PARTIAL_COLSUM = 7, OP_ONLINE_LSE = 8,
+    OP_TARGET_GATHER = 9, OP_ROPE = 10, OP_SWIGLU = 11, OP_SWIGLU_BWD = 12, OP_RMSNORM_BWD = 13,
+};
+
+struct DevStep {
+    int op;
+    int w;          // running width in values per chunk at step entry (16, 32, 64)
+    int a[7];
+};
+struct DevOperand {
+    const void* ptr;
+    int64_t ld;
+    int64_t cols;   // logical width (for masking)
+};
+struct DevStore {
+    void* ptr;
+    int64_t ld;
+    int64_t cols;            // logical width (tile) / piece columns
+    const int32_t* map;      // piece map (row-sum: per scaled column, col-sum: per row)
+};
+
+struct GemmParams {
+    int M, N, K;
+    int ntm, ntn, nk, ntiles;
+    int a_mn, b_mn;
+    int nsteps;
+    int store_main, out_f32, out_w;   // out_w: values per chunk at program end
+    void* out;
+    int64_t ld_out;
+    DevStep steps[MAX_STEPS];
+    DevOperand opnd[MAX_SLOTS];
+    DevStore store[MAX_SLOTS];
+};
+
+// ----------------------------------------------------------------- storage I/O
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+template <typename TS> struct Io;
+
+template <> struct Io<__nv_bfloat16> {
+    static constexpr int V = 8;
+    __device__ static __forceinline__ void load(const __nv_bfloat16* p, float* d) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            d[2 * i] = __uint_as_float(w[i] << 16);
+            d[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+        }
+    }
+    __device__ static __forceinline__ void store(__nv_bfloat16* p, const float* s) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(s[2 * i], s[2 * i + 1]);
+            w[i] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    __device__ static __forceinline__ float load1(const __nv_bfloat16* p) { return __bfloat162float(p[0]); }
+    __device__ static __forceinline__ void store1(__nv_bfloat16* p, float x) { p[0] = __float2bfloat16_rn(x); }
+};
+
+template <> struct Io<float> {
+    static constexpr int V = 4;
+    __device__ static __forceinline__ void load(const float* p, float* d) {
+        const float4 u = __ldg(reinterpret_cast<const float4*>(p));
+        d[0] = u.x; d[1] = u.y; d[2] = u.z; d[3] = u.w;
+    }
+    __device__ static __forceinline__ void store(float* p, const float* s) {
+        *reinterpret_cast<float4*>(p) = make_float4(s[0], s[1], s[2], s[3]);
+    }
+    __device__ static __forceinline__ float load1(const float* p) { return p[0]; }
+    __device__ static __forceinline__ void store1(float* p, float x) { p[0] = x; }
+};
+
+// Load W values of one row segment [c0, c0+W) (columns >= ncols read as 0).
+template <typename TS, int W>
+__device__ __forceinline__ void load_seg(const TS* rowp, int64_t c0, int64_t ncols, float* d) {
+    constexpr int V = Io<TS>::V;
+#pragma unroll
+    for (int i = 0; i < W; i += V) {
+        if (c0 + i + V <= ncols) {
+            Io<TS>::load(rowp + c0 + i, d + i);
+        } else {
+#pragma unroll
+            for (int e = 0; e < V; ++e)
+                d[i + e] = (c0 + i + e < ncols) ? Io<TS>::load1(rowp + c0 + i + e) : 0.0f;
+        }
+    }
+}
+// Store W values (rounded to TS) of one row segment, masking columns >= ncols.
+template <typename TS, int W>
+__device__ __forceinline__ void store_seg(TS* rowp, int64_t c0, int64_t ncols, const float* s) {
+    constexpr int V = Io<TS>::V;
+#pragma unroll
+    for (int i = 0; i < W; i += V) {
+        if (c0 + i + V <= ncols) {
+            Io<TS>::store(rowp + c0 + i, s + i);
+        } else {
+#pragma unroll
+            for (int e = 0; e < V; ++e)
+                if (c0 + i + e < ncols) Io<TS>::store1(rowp + c0 + i + e, s[i + e]);
+        }
+    }
+}
+// Broadcast f32 vector segment (row vector operand, same for all rows).
+template <int W>
+__device__ __forceinline__ void load_vec_seg(const float* vp, int64_t c0, int64_t n, float* d) {
+#pragma unroll
+    for (int i = 0; i < W; i += 4) {
+        if (c0 + i + 4 <= n) {
+            const float4 u = __ldg(reinterpret_cast<const float4*>(vp + c0 + i));
+            d[i] = u.x; d[i + 1] = u.y; d[i + 2] = u.z; d[i + 3] = u.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) d[i + e] = (c0 + i + e < n) ? __ldg(vp + c0 + i + e) : 0.0f;
+        }
+    }
+}
+
+// Running row-directed partial (row-sum or (max, sum) pair) of one thread.
+struct RowPart {
+    float acc;
+    float mx;
+    int pid;
+};
+
+__device__ __forceinline__ void rowpart_flush(const DevStore& st, RowPart& p, int64_t row, bool row_ok,
+                                              bool pair) {
+    if (row_ok && p.pid >= 0) {
+        float* o = static_cast<float*>(st.ptr) + row * st.ld;
+        if (pair) {
+            o[2 * p.pid] = p.mx;
+            o[2 * p.pid + 1] = p.acc;
+        } else {
+            o[p.pid] = p.acc;
+        }
+    }
+}
+
+// Accumulate W row-sum contributions x[i] at scaled columns c0+i into the
+// piece-blocked partial.  Pieces never straddle GPU tiles, so a chunk whose
+// first and last valid column share a piece takes the fast path.
+template <int W>
+__device__ __forceinline__ void rowsum_accum(const DevStore& st, RowPart& p, int64_t row, bool row_ok,
+                                             int64_t c0, int64_t ncols, const float* x) {
+    const int64_t last = (c0 + W <= ncols ? c0 + W : ncols) - 1;
+    if (last < c0) return;
+    const int p0 = __ldg(st.map + c0);
+    const int p1 = __ldg(st.map + last);
+    if (p0 == p1) {
+        if (p0 != p.pid) {
+            rowpart_flush(st, p, row, row_ok, false);
+            p.pid = p0;
+            p.acc = 0.0f;
+        }
+        float s = p.acc;
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            if (c0 + i <= last) s += x[i];
+        p.acc = s;
+    } else {
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            if (c0 + i <= last) {
+                const int q = __ldg(st.map + c0 + i);
+                if (q != p.pid) {
+                    rowpart_flush(st, p, row, row_ok, false);
+                    p.pid = q;
+                    p.acc = 0.0f;
+                }
+                p.acc += x[i];
+            }
+        }
+    }
+}
+
+// Online (max, scaled-sum) update in ascending column order (epilogue.py:355-366).
+template <int W>
+__device__ __forceinline__ void rowlse_accum(const DevStore& st, RowPart& p, int64_t row, bool row_ok,
+                                             int64_t c0, int64_t ncols, const float* x) {
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        if (c0 + i < ncols) {
+            const int q = __ldg(st.map + c0 + i);
+            if (q != p.pid) {
+                rowpart_flush(st, p, row, row_ok, true);
+                p.pid = q;
+                p.acc = 0.0f;
+                p.mx = -INFINITY;
+            }
+            const float mn = fmaxf(p.mx, x[i]);
+            const float sc = (p.mx == -INFINITY) ? 0.0f : __expf(p.mx - mn);
+            p.acc = p.acc * sc + __expf(x[i] - mn);
+            p.mx = mn;
+        }
+    }
+}
+
+// Column sums of a 128-row x 32-column chunk, segmented by the row-piece map.
+// Every epilogue thread deposits its row; warp quadrant 0 walks the columns.
+__device__ __forceinline__ void colsum_chunk(const DevStore& st, float* red, int lrow, int64_t m0, int M,
+                                             int64_t gcol0, int N, const float* x, bool row_ok) {
+#pragma unroll
+    for (int i = 0; i < CHUNK; ++i) red[lrow * RED_LD + i] = row_ok ? x[i] : 0.0f;
+    named_bar_sync(1, 32 * EPI_WARPS);
+    if (lrow < 32) {
+        const int c = lrow;
+        const int64_t gc = gcol0 + c;
+        if (gc < N) {
+            const int rows = (int)((M - m0) < BM ? (M - m0) : BM);
+            const int pfirst = __ldg(st.map + m0);
+            const int plast = __ldg(st.map + m0 + rows - 1);
+            float* out = static_cast<float*>(st.ptr);
+            if (pfirst == plast) {
+                float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+                int r = 0;
+                for (; r + 4 <= rows; r += 4) {
+                    s0 += red[(r + 0) * RED_LD + c];
+                    s1 += red[(r + 1) * RED_LD + c];
+                    s2 += red[(r + 2) * RED_LD + c];
+                    s3 += red[(r + 3) * RED_LD + c];
+                }
+                for (; r < rows; ++r) s0 += red[r * RED_LD + c];
+                out[(int64_t)pfirst * st.ld + gc] = (s0 + s1) + (s2 + s3);
+            } else {
+                int pid = pfirst;
+                float s = 0.f;
+                for (int r = 0; r < rows; ++r) {
+                    const int q = __ldg(st.map + m0 + r);
+                    if (q != pid) {
+                        out[(int64_t)pid * st.ld + gc] = s;
+                        pid = q;
+                        s = 0.f;
+                    }
+                    s += red[r * RED_LD + c];
+                }
+                out[(int64_t)pid * st.ld + gc] = s;
+            }
+        }
+    }
+    named_bar_sync(1, 32 * EPI_WARPS);
+}
+
+// --------------------------------------------------------------- kernel
+template <typename TS>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                 const __grid_constant__ GemmParams P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
+    float* red = reinterpret_cast<float*>(sB + STAGES * B_STAGE_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(red + BM * RED_LD);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 32 * EPI_WARPS);
+        }
+        fence_mbar_init();
+        tma_prefetch_desc(&tma_a);
+        tma_prefetch_desc(&tma_b);
+    }
+    if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int ntn = P.ntn;
+    auto tile_mn = [&](int t, int& tm, int& tn) {
+        const int per_group = RASTER_GROUP * ntn;
+        const int g = t / per_group;
+        const int first = g * RASTER_GROUP;
+        const int gs = min(P.ntm - first, RASTER_GROUP);
+        const int r = t - g * per_group;
+        tm = first + r % gs;
+        tn = r / gs;
+    };
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+                int tm, tn;
+                tile_mn(t, tm, tn);
+                const int m0 = tm * BM, n0 = tn * BN;
+                for (int kb = 0; kb < P.nk; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+                    const uint32_t sa = smem_u32(sA + stage * A_STAGE_BYTES);
+                    const uint32_t sb = smem_u32(sB + stage * B_STAGE_BYTES);
+                    const int k0 = kb * BK;
+                    if (!P.a_mn) {
+                        tma_load_2d(sa, &tma_a, k0, m0, &full[stage]);
+                    } else {
+#pragma unroll
+                        for (int b = 0; b < BM / 64; ++b)
+                            tma_load_2d(sa + b * (BK * 128), &tma_a, m0 + 64 * b, k0, &full[stage]);
+                    }
+                    if (!P.b_mn) {
+                        tma_load_2d(sb, &tma_b, k0, n0, &full[stage]);
+                    } else {
+#pragma unroll
+                        for (int b = 0; b < BN / 64; ++b)
+                            tma_load_2d(sb + b * (BK * 128), &tma_b, n0 + 64 * b, k0, &full[stage]);
+                    }
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            // kind::f16 instruction descriptor: D f32, A/B bf16, majorness, N>>3, M>>4.
+            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
+                                   ((uint32_t)P.a_mn << 15) | ((uint32_t)P.b_mn << 16) |
+                                   ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+            // K-major: LBO unused (16), SBO = 8 rows * 128 B; advance 32 B per UMMA_K=16.
+            // MN-major: LBO = next 64-wide MN atom column (BK*128 B), SBO = 8 K-rows * 128 B;
+            //           advance 2 x 1024 B per UMMA_K=16.
+            const uint32_t a_lbo = P.a_mn ? BK * 128 : 16, b_lbo = P.b_mn ? BK * 128 : 16;
+            const uint32_t a_step = P.a_mn ? 2048 : 32, b_step = P.b_mn ? 2048 : 32;
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+                for (int kb = 0; kb < P.nk; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(sA + stage * A_STAGE_BYTES);
+                    const uint32_t sb = smem_u32(sB + stage * B_STAGE_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t ad = umma_desc_sw128(sa + k * a_step, a_lbo, 1024);
+                        const uint64_t bd = umma_desc_sw128(sb + k * b_step, b_lbo, 1024);
+                        umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    umma_commit(&empty[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                umma_commit(&tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue
+        const int q = warp & 3;                 // TMEM lane quadrant this warp may read
+        const int lrow = q * 32 + lane;         // tile row owned by this thread
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+            int tm, tn;
+            tile_mn(t, tm, tn);
+            const int64_t m0 = (int64_t)tm * BM, n0 = (int64_t)tn * BN;
+            const int64_t row = m0 + lrow;
+            const bool row_ok = row < P.M;
+            const int64_t rem_chunks = ((int64_t)P.N - n0 + CHUNK - 1) / CHUNK;
+            const int nchunks = rem_chunks < BN / CHUNK ? (int)rem_chunks : BN / CHUNK;
+            RowPart rp0{0.f, -INFINITY, -1}, rp1{0.f, -INFINITY, -1};
+
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+
+            for (int j = 0; j < nchunks; ++j) {
+                float v[64];
+                {
+                    float c[32];
+                    tmem_ld32(tbase + j * CHUNK, c);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = c[i];
+                }
+                if (j == nchunks - 1) {
+                    // accumulator fully drained: hand the TMEM buffer back to the MMA warp
+                    tc_fence_before();
+                    mbar_arrive(&tempty[acc]);
+                }
+                const int64_t gcol0 = n0 + (int64_t)j * CHUNK;
+                int w = CHUNK;
+                for (int s = 0; s < P.nsteps; ++s) {
+                    const DevStep& st = P.steps[s];
+                    switch (st.op) {
+                    case OP_ROW_VEC_MUL: {
+                        const DevOperand& o = P.opnd[st.a[0]];
+                        const float* vp = static_cast<const float*>(o.ptr);
+#define CODA_ROWVEC(WW)                                                              \
+    {                                                                                \
+        float g[WW];                                                                 \
+        load_vec_seg<WW>(vp, gcol0 * WW / CHUNK, o.cols, g);                         \
+        _Pragma("unroll") for (int i = 0; i < WW; ++i) v[i] *= g[i];                 \
+    }
+                        if (w == 16) CODA_ROWVEC(16) else if (w == 32) CODA_ROWVEC(32) else CODA_ROWVEC(64)
+#undef CODA_ROWVEC
+                        break;
+                    }
+                    case OP_ROW_SCALE: {
+                        const float* vp = static_cast<const float*>(P.opnd[st.a[0]].ptr);
+                        const float r = row_ok ? __ldg(vp + row) : 0.0f;
+#pragma unroll
+                        for (int i = 0; i < 64; ++i) v[i] *= r;
+                        break;
+                    }
+                    case OP_RESIDUAL_ADD: {
+                        const DevOperand& o = P.opnd[st.a[0]];
+                        if (row_ok) {
+                            const TS* rp = static_cast<const TS*>(o.ptr) + row * o.ld;
+#define CODA_RES(WW)                                                                 \
+    {                                                                                \
+        float x[WW];                                                                 \
+        load_seg<TS, WW>(rp, gcol0 * WW / CHUNK, o.cols, x);                         \
+        _Pragma("unroll") for (int i = 0; i < WW; ++i) v[i] += x[i];                 \
+    }
+                            if (w == 16) CODA_RES(16) else if (w == 32) CODA_RES(32) else CODA_RES(64)
+#undef CODA_RES
+                        }
+                        break;
+                    }
+                    case OP_AUX_TILE_STORE: {
+                        const DevStore& o = P.store[st.a[0]];
+                        if (row_ok) {
+                            TS* rp = static_cast<TS*>(o.ptr) + row * o.ld;
+                            if (w == 16) store_seg<TS, 16>(rp, gcol0 / 2, o.cols, v);
+                            else if (w == 32) store_seg<TS, 32>(rp, gcol0, o.cols, v);
+                            else store_seg<TS, 64>(rp, gcol0 * 2, o.cols, v);
+                        }
+                        break;
+                    }
+                    case OP_PARTIAL_SUMSQ: {
+                        float x[32];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) x[i] = v[i] * v[i];
+                        const DevStore& o = P.store[st.a[0]];
+                        if (st.a[6] == 0) rowsum_accum<32>(o, rp0, row, row_ok, gcol0, P.N, x);
+                        else rowsum_accum<32>(o, rp1, row, row_ok, gcol0, P.N, x);
+                        break;
+                    }
+                    case OP_PARTIAL_ROWDOT: {
+                        const DevOperand& oi = P.opnd[st.a[0]];
+                        float x[32];
+                        if (row_ok) load_seg<TS, 32>(static_cast<const TS*>(oi.ptr) + row * oi.ld, gcol0, oi.cols, x);
+                        else {
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) x[i] = 0.f;
+                        }
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) x[i] *= v[i];
+                        const DevStore& o = P.store[st.a[1]];
+                        if (st.a[6] == 0) rowsum_accum<32>(o, rp0, row, row_ok, gcol0, P.N, x);
+                        else rowsum_accum<32>(o, rp1, row, row_ok, gcol0, P.N, x);
+                        break;
+                    }
+                    case OP_PARTIAL_COLSUM: {
+                        colsum_chunk(P.store[st.a[0]], red, lrow, m0, P.M, gcol0, P.N, v, row_ok);
+                        break;
+                    }
+                    case OP_ONLINE_LSE: {
+                        const DevStore& o = P.store[st.a[0]];
+                        if (st.a[6] == 0) rowlse_accum<32>(o, rp0, row, row_ok, gcol0, P.N, v);
+                        else rowlse_accum<32>(o, rp1, row, row_ok, gcol0, P.N, v);
+                        break;
+                    }
+                    case OP_TARGET_GATHER: {
+                        if (row_ok) {
+                            const int64_t lab = static_cast<const int64_t*>(P.opnd[st.a[0]].ptr)[row];
+                            const int64_t local = lab - gcol0;
+                            if (local >= 0 && local < 32 && lab < P.N) {
+                                float val = 0.f;
+#pragma unroll
+                                for (int i = 0; i < 32; ++i)
+                                    if (i == (int)local) val = v[i];
+                                static_cast<float*>(P.store[st.a[1]].ptr)[row] = val;
+                            }
+                        }
+                        break;
+                    }
+                    case OP_ROPE: {
+                        const DevOperand& oc = P.opnd[st.a[0]];
+                        const DevOperand& os = P.opnd[st.a[1]];
+                        const float sgn = st.a[2] ? -1.0f : 1.0f;
+                        if (row_ok) {
+                            const TS* cp = static_cast<const TS*>(oc.ptr) + row * oc.ld;
+                            const TS* sp = static_cast<const TS*>(os.ptr) + row * os.ld;
+#define CODA_ROPE(WW)                                                                \
+    {                                                                                \
+        float cs[WW], sn[WW];                                                        \
+        load_seg<TS, WW>(cp, gcol0 * WW / CHUNK, oc.cols, cs);                       \
+        load_seg<TS, WW>(sp, gcol0 * WW / CHUNK, os.cols, sn);                       \
+        _Pragma("unroll") for (int k = 0; k < WW / 2; ++k) {                         \
+            const float x0 = v[2 * k], x1 = v[2 * k + 1];                            \
+            const float se = sgn * sn[2 * k], so = sgn * sn[2 * k + 1];              \
+            v[2 * k] = x0 * cs[2 * k] - x1 * se;                                     \
+            v[2 * k + 1] = x0 * so + x1 * cs[2 * k + 1];                             \
+        }                                                                            \
+    }
+                            if (w == 16) CODA_ROPE(16) else if (w == 32) CODA_ROPE(32) else CODA_ROPE(64)
+#undef CODA_ROPE
+                        }
+                        break;
+                    }
+                    case OP_SWIGLU: {
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) {
+                            if (2 * k < w) {
+                                const float g = v[2 * k], u = v[2 * k + 1];
+                                v[k] = g * sigmoid_stable(g) * u;
+                            }
+                        }
+                        w >>= 1;
+                        break;
+                    }
+                    case OP_SWIGLU_BWD: {
+                        // entry width 32 (factor 1); preact read at 64 (factor 2)
+                        const DevOperand& oz = P.opnd[st.a[0]];
+                        float z[64];
+                        if (row_ok) load_seg<TS, 64>(static_cast<const TS*>(oz.ptr) + row * oz.ld, gcol0 * 2, oz.cols, z);
+                        else {
+#pragma unroll
+                            for (int i = 0; i < 64; ++i) z[i] = 0.f;
+                        }
+                        float rec[32];
+                        // descending k: v[2k], v[2k+1] overwrite only entries >= k
+#pragma unroll
+                        for (int k = 31; k >= 0; --k) {
+                            const float g = z[2 * k], u = z[2 * k + 1], d = v[k];
+                            const float sg = sigmoid_stable(g);
+                            const float sl = g * sg;
+                            rec[k] = sl * u;
+                            const float gu = d * sl;
+                            const float gg = d * u * (sg + sl * (1.0f - sg));
+                            v[2 * k] = gg;
+                            v[2 * k + 1] = gu;
+                            z[2 * k] = g * gg;        // <preact, grad_preact> terms
+                            z[2 * k + 1] = u * gu;
+                        }
+                        const DevStore& orc = P.store[st.a[1]];
+                        if (row_ok) store_seg<TS, 32>(static_cast<TS*>(orc.ptr) + row * orc.ld, gcol0, orc.cols, rec);
+                        const DevStore& opd = P.store[st.a[2]];
+                        if (st.a[6] == 0) rowsum_accum<64>(opd, rp0, row, row_ok, gcol0 * 2, (int64_t)P.N * 2, z);
+                        else rowsum_accum<64>(opd, rp1, row, row_ok, gcol0 * 2, (int64_t)P.N * 2, z);
+                        w = 64;
+                        break;
+                    }
+                    case OP_RMSNORM_BWD: {
+                        const DevOperand& op_pre = P.opnd[st.a[0]];
+                        float cpre[32], gam[32];
+                        float r = 0.f, sstat = 0.f;
+                        if (row_ok) {
+                            load_seg<TS, 32>(static_cast<const TS*>(op_pre.ptr) + row * op_pre.ld, gcol0, op_pre.cols, cpre);
+                            r = __ldg(static_cast<const float*>(P.opnd[st.a[1]].ptr) + row);
+                            sstat = __ldg(static_cast<const float*>(P.opnd[st.a[3]].ptr) + row);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) cpre[i] = 0.f;
+                        }
+                        load_vec_seg<32>(static_cast<const float*>(P.opnd[st.a[2]].ptr), gcol0, P.opnd[st.a[2]].cols, gam);
+                        float tmp[32];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            cpre[i] *= r;                 // c_n = c * r
+                            tmp[i] = cpre[i] * gam[i];    // normed = c_n * gamma
+                        }
+                        const DevStore& on = P.store[st.a[5]];
+                        if (row_ok) store_seg<TS, 32>(static_cast<TS*>(on.ptr) + row * on.ld, gcol0, on.cols, tmp);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) tmp[i] = v[i] * cpre[i];   // D * c_n
+                        colsum_chunk(P.store[st.a[6]], red, lrow, m0, P.M, gcol0, P.N, tmp, row_ok);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = (v[i] * gam[i] - cpre[i] * sstat) * r;
+                        if (st.a[4] >= 0 && row_ok) {
+                            const DevOperand& oa = P.opnd[st.a[4]];
+                            float x[32];
+                            load_seg<TS, 32>(static_cast<const TS*>(oa.ptr) + row * oa.ld, gcol0, oa.cols, x);
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) v[i] += x[i];
+                        }
+                        break;
+                    }
+                    default:
+                        break;
+                    }
+                }
+                if (P.store_main && row_ok) {
+                    const int64_t ncols = (int64_t)P.N * w / CHUNK;
+                    const int64_t c0 = gcol0 * w / CHUNK;
+                    if (P.out_f32) {
+                        float* rp = static_cast<float*>(P.out) + row * P.ld_out;
+                        if (w == 16) store_seg<float, 16>(rp, c0, ncols, v);
+                        else if (w == 32) store_seg<float, 32>(rp, c0, ncols, v);
+                        else store_seg<float, 64>(rp, c0, ncols, v);
+                    } else {
+                        __nv_bfloat16* rp = static_cast<__nv_bfloat16*>(P.out) + row * P.ld_out;
+                        if (w == 16) store_seg<__nv_bfloat16, 16>(rp, c0, ncols, v);
+                        else if (w == 32) store_seg<__nv_bfloat16, 32>(rp, c0, ncols, v);
+                        else store_seg<__nv_bfloat16, 64>(rp, c0, ncols, v);
+                    }
+                }
+            }
+            // flush the row-directed partials of this tile (pieces end at tile edges)
+            for (int s = 0; s < P.nsteps; ++s) {
+                const DevStep& st = P.steps[s];
+                int si = -1, slot = -1;
+                bool pair = false;
+                if (st.op == OP_PARTIAL_SUMSQ) { si = st.a[6]; slot = st.a[0]; }
+                else if (st.op == OP_PARTIAL_ROWDOT) { si = st.a[6]; slot = st.a[1]; }
+                else if (st.op == OP_ONLINE_LSE) { si = st.a[6]; slot = st.a[0]; pair = true; }
+                else if (st.op == OP_SWIGLU_BWD) { si = st.a[6]; slot = st.a[2]; }
+                if (si == 0) rowpart_flush(P.store[slot], rp0, row, row_ok, pair);
+                else if (si == 1) rowpart_flush(P.store[slot], rp1, row, row_ok, pair);
+            }
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<TMEM_COLS>(tmem_base);
+    }
+}
+
+constexpr size_t gemm_smem_bytes() {
+    return 1024 + (size_t)STAGES * STAGE_BYTES + (size_t)BM * RED_LD * 4 + (2 * STAGES + 4) * 8 + 16;
+}
+
+}  // namespace coda

@@ -1,0 +1,127 @@
+"""GPU parity of the fused layer forward + backward (§8 rows a29-a31).
+
+  * golden: reference engine outputs (tilefuse, SIM32 / SIMBF16) on stored inputs;
+  * C1 tiny fp32 config (M=128, d=256, I=1024): every gradient vs the float64
+    canonical oracle at <= 1e-5 relative, and vs the fused-order oracle;
+  * bf16 at a mid size vs the fused-order oracle at <= 2e-2.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import coda_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+WKEYS = ("w_out", "gamma_ffn", "w_gate_up", "w_down", "gamma_qkv", "w_qkv")
+
+
+def _cd():
+    import paper_2605_19269_b200 as cd
+
+    return cd
+
+
+def _run_layer(cd, P, cfg, x, z, w, cos, sin, gq, gr):
+    M = lambda a: cd.DenseMatrix.from_array(a, P)  # noqa: E731
+    weights = cd.LayerWeights(w_out=M(w["w_out"]), gamma_ffn=cd.Vector.from_array(w["gamma_ffn"], P),
+                              w_gate_up=M(w["w_gate_up"]), w_down=M(w["w_down"]),
+                              gamma_qkv=cd.Vector.from_array(w["gamma_qkv"], P), w_qkv=M(w["w_qkv"]))
+    fwd = cd.layer_forward(M(x), M(z), weights, M(cos), M(sin), config=cfg)
+    bwd = cd.layer_backward(M(gq), fwd.tape, weights, grad_residual=M(gr), config=cfg)
+    return fwd, bwd
+
+
+@pytest.mark.parametrize("tag", ["tiny", "ragged"])
+@pytest.mark.parametrize("mode", ["sim32", "simbf16"])
+def test_layer_vs_reference_golden(cuda_ready, tag, mode):
+    cd = _cd()
+    g = load_golden(f"layer_{tag}_{mode}")
+    m, d, ffn, tm, tn, rtn = (int(v) for v in g["meta"])
+    P = {"sim32": cd.PrecisionMode.SIM32, "simbf16": cd.PrecisionMode.SIMBF16}[mode]
+    cfg = cd.PipelineConfig(hidden=d, ffn=ffn, tile_m=tm, tile_n=tn, reduction_tile_n=rtn, precision=P)
+    w = {k: g[k] for k in WKEYS}
+    fwd, bwd = _run_layer(cd, P, cfg, g["x"], g["z"], w, g["cos"], g["sin"], g["grad_qkv"], g["grad_residual"])
+    tol = 1e-5 if mode == "sim32" else 2e-2
+    errs = {"qkv": O.rel_error(fwd.qkv.data, g["qkv"]), "residual": O.rel_error(fwd.residual.data, g["residual"])}
+    for key in O.GRAD_KEYS:
+        errs[key] = O.rel_error(getattr(bwd, key).data, g[f"g_{key}"])
+    print(f"\n[{tag}/{mode}] vs reference engine: " + ", ".join(f"{k}={v:.2e}" for k, v in errs.items()))
+    assert max(errs.values()) <= tol, errs
+    # and vs the float64 canonical chain
+    ref = {"qkv": O.rel_error(fwd.qkv.data, g["ref_qkv"])}
+    for key in O.GRAD_KEYS:
+        ref[key] = O.rel_error(getattr(bwd, key).data, g[f"ref_g_{key}"])
+    assert max(ref.values()) <= tol, ref
+
+
+def test_c1_tiny_fp32_vs_float64_oracle(cuda_ready):
+    """BASELINE config 0: d=256, ffn(I)=1024 (F=2048), 128 tokens, fp32 path <= 1e-5."""
+    cd = _cd()
+    m, d, ffn = 128, 256, 2048
+    rng = np.random.default_rng(0)
+    w = O.random_layer(rng, d, ffn, O.SIM32)
+    x = O.q(rng.standard_normal((m, d)), O.SIM32)
+    z = O.q(rng.standard_normal((m, d)), O.SIM32)
+    cos, sin = O.qkv_rope_tables(m, d, O.SIM32)
+    gq = O.q(rng.standard_normal((m, 3 * d)), O.SIM32)
+    gr = O.q(rng.standard_normal((m, d)), O.SIM32)
+    P = cd.PrecisionMode.SIM32
+    cfg = cd.PipelineConfig(hidden=d, ffn=ffn, precision=P)
+    fwd, bwd = _run_layer(cd, P, cfg, x, z, w, cos, sin, gq, gr)
+    ref = O.layer_ref_forward(x, z, w, cos, sin)
+    refb = O.layer_ref_backward(gq, gr, ref, x, w, cos, sin)
+    errs = {"qkv": O.rel_error(fwd.qkv.data, ref["qkv"]), "residual": O.rel_error(fwd.residual.data, ref["h1b"])}
+    mx = {"qkv": float(np.max(np.abs(fwd.qkv.data - ref["qkv"])))}
+    for key in O.GRAD_KEYS:
+        got = getattr(bwd, key).data
+        errs[key] = O.rel_error(got, refb[key])
+        mx[key] = float(np.max(np.abs(got - refb[key])))
+    print("\n[C1 fp32] rel vs f64: " + ", ".join(f"{k}={v:.2e}" for k, v in errs.items()))
+    print("[C1 fp32] max abs:    " + ", ".join(f"{k}={v:.2e}" for k, v in mx.items()))
+    assert max(errs.values()) <= 1e-5, errs
+    # fused-order oracle (same precision model) agrees too
+    of = O.layer_forward(x, z, w, cos, sin, O.SIM32)
+    ob = O.layer_backward(gq, of, w, O.SIM32, grad_residual=gr)
+    for key in O.GRAD_KEYS:
+        assert O.rel_error(getattr(bwd, key).data, ob[key]) <= 1e-5, key
+
+
+def test_bf16_mid_layer_vs_fused_oracle(cuda_ready):
+    """bf16 path at a shape with several GPU tiles in every dimension."""
+    cd = _cd()
+    m, d, ffn = 512, 512, 2816
+    rng = np.random.default_rng(1)
+    mode = O.SIMBF16
+    w = O.random_layer(rng, d, ffn, mode, scale=0.05)
+    x = O.q(rng.standard_normal((m, d)), mode)
+    z = O.q(rng.standard_normal((m, d)), mode)
+    cos, sin = O.qkv_rope_tables(m, d, mode)
+    gq = O.q(rng.standard_normal((m, 3 * d)), mode)
+    gr = O.q(rng.standard_normal((m, d)), mode)
+    P = cd.PrecisionMode.SIMBF16
+    cfg = cd.PipelineConfig(hidden=d, ffn=ffn, precision=P)
+    fwd, bwd = _run_layer(cd, P, cfg, x, z, w, cos, sin, gq, gr)
+    of = O.layer_forward(x, z, w, cos, sin, mode)
+    ob = O.layer_backward(gq, of, w, mode, grad_residual=gr)
+    errs = {"qkv": O.rel_error(fwd.qkv.data, of["qkv"])}
+    for key in O.GRAD_KEYS:
+        errs[key] = O.rel_error(getattr(bwd, key).data, ob[key])
+    print("\n[bf16 512x512x2816] rel vs fused oracle: " + ", ".join(f"{k}={v:.2e}" for k, v in errs.items()))
+    assert max(errs.values()) <= 2e-2, errs
+
+
+def test_eps_path_all_zero_input(cuda_ready):
+    """reference tests/test_kernels.py:385-393: zero x, z -> r = 1/sqrt(eps), qkv = 0."""
+    cd = _cd()
+    P = cd.PrecisionMode.SIM32
+    d, ffn, m = 16, 32, 8
+    cfg = cd.PipelineConfig(hidden=d, ffn=ffn, precision=P)
+    rng = np.random.default_rng(0)
+    w = cd.LayerWeights.random(rng, cfg)
+    zero = cd.DenseMatrix.from_array(np.zeros((m, d)), P)
+    cos, sin = cd.qkv_rope_tables(m, d, precision=P)
+    fwd = cd.layer_forward(zero, zero, w, cos, sin, config=cfg)
+    assert np.all(fwd.qkv.data == 0.0)
+    np.testing.assert_allclose(fwd.tape.inv_rms_a.data, np.float32(1.0 / np.sqrt(np.float32(1e-6))), rtol=1e-6)
