@@ -1,0 +1,391 @@
+"""Benchmark: fused LLaMA-style block forward + backward, tokens/s (BASELINE.json).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c4|c3|c1] [--impl coda|reference]
+
+One step = `layer_forward` + `layer_backward` of the reference's
+reparameterized block (6 + 13 fused launches) over this rank's tokens, plus
+the NCCL all-reduce of weight gradients when N > 1 (token-sharded data
+parallelism).  Prints ONE JSON line on rank 0.
+
+  value  — whole-job tokens/s with inputs resident in HBM (device-timed, max over ranks)
+  e2e    — same metric through the public API from pinned HOST buffers: the H2D copy of
+           each step's inputs and the D2H read of its results are inside the timed region
+  roofline — the dominant GEMM launch's achieved TFLOP/s vs the measured bf16 peak
+  cpu_baseline — the CPU oracle (reference algorithm, oracle/) on a bounded token sample
+
+`--impl reference` times the reference's CPU algorithm (oracle port; the
+Python reference cannot travel to the GPU box) on all host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (hidden d, LLaMA intermediate I, tokens per job, label)
+    "c1": (256, 1024, 128, "tiny LLaMA-style block fp32 (d=256, ffn=1024, 128 tokens)"),
+    "c3": (2048, 8192, 8192, "LLaMA-3-1B block shapes (d=2048, ffn=8192, 8192 tokens) bf16 fwd+bwd"),
+    "c4": (4096, 14336, 16384, "LLaMA-3-8B block shapes (d=4096, ffn=14336, 16384 tokens) bf16 fwd+bwd"),
+}
+
+
+def flops_per_token(d: int, inter: int) -> float:
+    """fwd+bwd = 3 x 2(d^2 + d*F + I*d + d*Q), F = 2I, Q = 3d."""
+    f, q = 2 * inter, 3 * d
+    return 3 * 2.0 * (d * d + d * f + inter * d + d * q)
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join(timeout=6)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and
+                          s[2 + i].lower() in ("active", "1")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- workload
+
+
+def make_workload(cd, d, inter, m, rank, device, seed=0):
+    """Synthetic bf16 inputs and random-init weights (N(0, 0.02^2), gains 1 + 0.1 N)."""
+    import torch
+
+    P = cd.PrecisionMode.SIMBF16
+    g = torch.Generator(device=device).manual_seed(seed)
+    gr = torch.Generator(device=device).manual_seed(seed * 1000 + 17 + rank)
+
+    def w(*shape, scale=0.02, gen=g):
+        t = cd.tensors.alloc_matrix(shape[0], shape[1], torch.bfloat16, device)
+        t.copy_(torch.randn(shape, generator=gen, device=device) * scale)
+        return cd.DenseMatrix.from_tensor(t, P)
+
+    def gain(n):
+        return cd.Vector.from_tensor(1.0 + 0.1 * torch.randn(n, generator=g, device=device), P)
+
+    f = 2 * inter
+    weights = cd.LayerWeights(w_out=w(d, d), gamma_ffn=gain(d), w_gate_up=w(d, f), w_down=w(inter, d),
+                              gamma_qkv=gain(d), w_qkv=w(d, 3 * d))
+    acts = {name: w(m, width, scale=1.0, gen=gr) for name, width in
+            (("x", d), ("z", d), ("grad_qkv", 3 * d), ("grad_residual", d))}
+    cos, sin = cd.qkv_rope_tables(m, d, start=rank * m, precision=P)
+    return weights, acts, cos, sin
+
+
+def run_step(cd, cfg, weights, acts, cos, sin, hook=None):
+    fwd = cd.layer_forward(acts["x"], acts["z"], weights, cos, sin, config=cfg)
+    bwd = cd.layer_backward(acts["grad_qkv"], fwd.tape, weights, grad_residual=acts["grad_residual"], config=cfg,
+                            wgrad_hook=hook)
+    return fwd, bwd
+
+
+class WgradAllReduce:
+    """Token-sharded DP: all-reduce(sum) of each f32 weight gradient on a side stream,
+    overlapped with the remaining backward launches; waited before the step ends."""
+
+    def __init__(self, dist, device):
+        import torch
+
+        self.dist = dist
+        self.side = torch.cuda.Stream(device)
+        self.pending = []
+
+    def __call__(self, name, tensor):
+        import torch
+
+        main = torch.cuda.current_stream(tensor.device)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        with torch.cuda.stream(self.side):
+            self.side.wait_event(ev)
+            self.dist.all_reduce(tensor)
+        tensor.record_stream(self.side)
+        self.pending.append(tensor)
+
+    def wait(self):
+        import torch
+
+        torch.cuda.current_stream().wait_stream(self.side)
+        self.pending.clear()
+
+
+def cpu_oracle_tokens_per_s(d, inter, sample_tokens, seconds_budget=20.0):
+    """Time the CPU oracle (fused-order SIMBF16 restatement of the reference) on a token sample."""
+    import numpy as np
+
+    from oracle import coda_oracle as O
+
+    rng = np.random.default_rng(0)
+    mode = O.SIMBF16
+    wts = O.random_layer(rng, d, 2 * inter, mode, scale=0.02)
+    m = sample_tokens
+    x, z = (O.q(rng.standard_normal((m, d)), mode) for _ in range(2))
+    cos, sin = O.qkv_rope_tables(m, d, mode)
+    gq = O.q(rng.standard_normal((m, 3 * d)), mode)
+    gres = O.q(rng.standard_normal((m, d)), mode)
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        f = O.layer_forward(x, z, wts, cos, sin, mode)
+        O.layer_backward(gq, f, wts, mode, grad_residual=gres)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > seconds_budget or len(times) >= 5:
+            break
+    best = min(times)
+    return m / best, best, len(times)
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------- arms
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the reference algorithm on the host cores (oracle port)."""
+    d, inter, tokens, label = CONFIGS[args.config]
+    if rank != 0:
+        return
+    sample = args.cpu_sample
+    per_step = []
+    for _ in range(max(1, args.warmup)):
+        cpu_oracle_tokens_per_s(d, inter, sample, seconds_budget=0.0)
+    for _ in range(args.steps):
+        tps, secs, _ = cpu_oracle_tokens_per_s(d, inter, sample, seconds_budget=0.0)
+        per_step.append(secs)
+    t = statistics.median(per_step)
+    value = sample / t
+    cores = host_cores()
+    line = {
+        "impl": "reference", "metric": "block fwd+bwd tokens/s", "value": value, "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (bf16 storage grid)",
+        "data": "synthetic", "config": {"workload": label, "tokens_sampled_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
+                         "sample": f"{sample} tokens of the {args.config} block per step, numpy/OpenBLAS all cores"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def coda_arm(args, rank, world, local_rank):
+    import torch
+
+    import paper_2605_19269_b200 as cd
+    from paper_2605_19269_b200 import _native
+
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # noqa: F811
+
+        dist.init_process_group("nccl", device_id=device)
+    d, inter, tokens, label = CONFIGS[args.config]
+    m = tokens // world if args.scaling == "strong" else tokens
+    P = cd.PrecisionMode.SIMBF16
+    cfg = cd.PipelineConfig(hidden=d, ffn=2 * inter, precision=P)
+    weights, acts, cos, sin = make_workload(cd, d, inter, m, rank, device)
+    hook = WgradAllReduce(dist, device) if dist is not None else None
+
+    def step():
+        out = run_step(cd, cfg, weights, acts, cos, sin, hook)
+        if hook is not None:
+            hook.wait()
+        return out
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _native.launch_count()
+    with ClockSampler(local_rank) as clocks:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    launches = _native.launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * m / (ms_step / 1e3)
+
+    # ---- e2e through the public API from pinned host buffers
+    host = {k: v.tensor.cpu().pin_memory() for k, v in acts.items()}
+    dev_in = {k: torch.empty_like(v.tensor) for k, v in acts.items()}
+    h2d = sum(t.numel() * t.element_size() for t in host.values())
+    out_host = torch.empty((m, d), dtype=torch.bfloat16).pin_memory()
+    gam_host = torch.empty((2, d), dtype=torch.float32).pin_memory()
+    d2h = out_host.numel() * 2 + gam_host.numel() * 4
+
+    def e2e_step():
+        for k in host:
+            dev_in[k].copy_(host[k], non_blocking=True)
+        a = {k: cd.DenseMatrix.from_tensor(dev_in[k], P) for k in dev_in}
+        _, bwd = run_step(cd, cfg, weights, a, cos, sin, hook)
+        if hook is not None:
+            hook.wait()
+        out_host.copy_(bwd.x.tensor, non_blocking=True)
+        gam_host[0].copy_(bwd.gamma_ffn.tensor, non_blocking=True)
+        gam_host[1].copy_(bwd.gamma_qkv.tensor, non_blocking=True)
+
+    for _ in range(max(1, args.warmup // 2)):
+        e2e_step()
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    barrier()
+    ms_e2e = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms_e2e], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    e2e_value = world * m / (ms_e2e / args.steps / 1e3)
+
+    # ---- roofline of the dominant launch: per-launch CUDA events over 2 profiled steps
+    prof = _native.profile_launches(lambda: step(), reps=2)
+    pk = peaks()
+    roofline = None
+    if prof:
+        top = max(prof.values(), key=lambda r: r["total_ms"])
+        achieved = top["flops"] / (top["avg_ms"] / 1e3) / 1e12
+        peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+        traffic = None
+        tp = ROOT / "profiles" / "traffic.json"
+        if tp.exists():
+            traffic = json.loads(tp.read_text()).get(f"{args.config}:{top['name']}")
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": traffic, "kernel": top["name"],
+                    "peak_kind": "measured sustained bf16 (MEASURED_PEAKS.json)",
+                    "share_of_step": top["total_ms"] / sum(r["total_ms"] for r in prof.values())}
+    total_flops = flops_per_token(d, inter) * m
+    block_tflops = total_flops / (ms_step / 1e3) / 1e12
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        tps, secs, reps = cpu_oracle_tokens_per_s(d, inter, args.cpu_sample)
+        cpu = {"value": tps, "unit": "tokens/s", "cores": host_cores(), "kind": "port",
+               "sample": f"{args.cpu_sample} tokens of the {args.config} block, fused-order SIMBF16 oracle, "
+                         f"best of {reps} ({secs:.2f} s each)"}
+
+    if rank == 0:
+        line = {
+            "metric": "block fwd+bwd tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if args.scaling == "strong" and world > 1 else "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, N(0,1) activations)",
+            "config": {"workload": label, "tokens_per_gpu": m, "global_tokens": world * m, "hidden": d,
+                       "intermediate": inter, "ffn_interleaved": 2 * inter, "qkv": 3 * d,
+                       "parallelism": f"token-sharded dp{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (>=100 MB activations per launch)"},
+            "block_tflops": block_tflops,
+            "frac_of_bf16_peak": block_tflops / pk["bf16_tflops"],
+            "clocks": clocks.summary(),
+            "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "launch_breakdown_ms": {k: round(v["avg_ms"], 4) for k, v in (prof or {}).items()},
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("coda", "reference"), default="coda")
+    ap.add_argument("--config", choices=tuple(CONFIGS), default="c4")
+    ap.add_argument("--scaling", choices=("strong", "weak"), default="weak")
+    ap.add_argument("--cpu-sample", type=int, default=256)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.gpus == 1 else 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+    else:
+        coda_arm(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

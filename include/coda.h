@@ -122,7 +122,9 @@ typedef struct {
     coda_tensor_t  t;
     const int32_t* piece_map;
     int32_t        kind;      /* 0 tile, 1 row-sum, 2 row-pair, 3 col-sum, 4 gather */
-    int32_t        _pad;
+    int32_t        aligned;   /* row-sum/row-pair: every piece starts on a 32*factor column
+                                 boundary; col-sum: every piece starts on a 32-row boundary.
+                                 Enables the specialised epilogue kernels. */
 } coda_store_t;
 
 /* run_gemm (engine.py:376-464) / run_gemm_trans (engine.py:467-478):
@@ -133,6 +135,8 @@ int coda_gemm_epilogue(const coda_problem_t* problem,
                        const coda_tensor_t* operands, int noperands,
                        const coda_store_t* stores, int nstores,
                        const coda_tensor_t* main_out,      /* NULL iff !store_main */
+                       const coda_tensor_t* acc_in,        /* NULL, or f32 (m, n) added to the
+                                                              accumulator before step 0 (C += A*B) */
                        void* stream);
 
 /* finalize_rms (reductions.py:64-80): r[i] = 1/sqrt(sum_b p[i,b] / d + eps). */

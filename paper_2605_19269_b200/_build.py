@@ -20,7 +20,7 @@ LIB = LIBDIR / "libcoda.so"
 INCLUDE = PKG.parent / "include"
 
 SOURCES = ["coda_api.cu"]
-DEPS = ["coda_api.cu", "coda_gemm.cuh", "coda_aux.cuh", "coda_ptx.cuh"]
+DEPS = ["coda_api.cu", "coda_gemm.cuh", "coda_aux.cuh", "coda_ptx.cuh", "coda_mainloop.cuh", "coda_fast.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

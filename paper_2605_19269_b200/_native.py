@@ -99,7 +99,7 @@ class Store(ctypes.Structure):
         ("t", Tensor),
         ("piece_map", ctypes.c_void_p),
         ("kind", ctypes.c_int32),
-        ("_pad", ctypes.c_int32),
+        ("aligned", ctypes.c_int32),
     ]
 
 
@@ -125,7 +125,7 @@ def _declare(lib) -> None:
     vp, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float
     P = ctypes.POINTER
     lib.coda_gemm_epilogue.argtypes = [P(Problem), P(Tensor), P(Tensor), P(Step), i32, P(Tensor), i32,
-                                       P(Store), i32, P(Tensor), vp]
+                                       P(Store), i32, P(Tensor), P(Tensor), vp]
     lib.coda_finalize_rms.argtypes = [vp, i64, i64, i64, i64, f32, vp, vp]
     lib.coda_finalize_rowdot.argtypes = [vp, i64, i64, i64, i64, vp, vp]
     lib.coda_reduce_row_partials.argtypes = [vp, i64, i64, i64, vp, vp]
@@ -180,9 +180,59 @@ def check(rc: int) -> None:
     raise cls(msg)
 
 
-def call(name: str, *args) -> None:
+_launches = 0
+_profile = None   # list of (tag, flops, start_event, end_event) while profiling
+
+
+def call(name: str, *args, tag: str | None = None, flops: float = 0.0) -> None:
+    """Invoke one C-ABI entry point; every call enqueues exactly one kernel."""
+    global _launches
     lib = load()
-    check(getattr(lib, name)(*args))
+    if _profile is not None:
+        import torch
+
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        check(getattr(lib, name)(*args))
+        e1.record()
+        _profile.append((tag or name, flops, e0, e1))
+    else:
+        check(getattr(lib, name)(*args))
+    _launches += 1
+
+
+def launch_count() -> int:
+    """Number of CODA kernels enqueued by this process so far."""
+    return _launches
+
+
+def profile_launches(fn, reps: int = 2) -> dict:
+    """Run fn() `reps` times recording CUDA events around every launch.
+
+    Returns {tag: {name, count, avg_ms, total_ms, flops}} (flops per launch).
+    Events are recorded on the launching (current) stream.
+    """
+    import torch
+
+    global _profile
+    _profile = []
+    try:
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        rows = _profile
+    finally:
+        _profile = None
+    out: dict = {}
+    for tag, flops, e0, e1 in rows:
+        r = out.setdefault(tag, {"name": tag, "count": 0, "total_ms": 0.0, "flops": flops})
+        r["count"] += 1
+        r["total_ms"] += e0.elapsed_time(e1)
+    for r in out.values():
+        r["avg_ms"] = r["total_ms"] / r["count"]
+        r["total_ms"] /= reps
+        r["count"] //= reps
+    return out
 
 
 def tensor_desc(t, dtype_code: int | None = None) -> Tensor:

@@ -9,6 +9,7 @@
 #include <cudaTypedefs.h>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -17,6 +18,7 @@
 #include "../../include/coda.h"
 #include "coda_aux.cuh"
 #include "coda_gemm.cuh"
+#include "coda_fast.cuh"
 
 namespace {
 
@@ -96,15 +98,18 @@ struct MapKey {
     const void* ptr;
     uint64_t d0, d1, stride;
     uint32_t b0, b1;
+    int dtype, swz;
     bool operator==(const MapKey& o) const {
-        return ptr == o.ptr && d0 == o.d0 && d1 == o.d1 && stride == o.stride && b0 == o.b0 && b1 == o.b1;
+        return ptr == o.ptr && d0 == o.d0 && d1 == o.d1 && stride == o.stride && b0 == o.b0 && b1 == o.b1 &&
+               dtype == o.dtype && swz == o.swz;
     }
 };
 struct MapKeyHash {
     size_t operator()(const MapKey& k) const {
         size_t h = std::hash<const void*>()(k.ptr);
         h ^= std::hash<uint64_t>()(k.d0 * 1315423911ull + k.d1) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
-        h ^= std::hash<uint64_t>()(k.stride * 2654435761ull + k.b0 * 131 + k.b1) + (h << 6) + (h >> 2);
+        h ^= std::hash<uint64_t>()(k.stride * 2654435761ull + k.b0 * 131 + k.b1 * 7 + k.dtype * 3 + k.swz) +
+             (h << 6) + (h >> 2);
         return h;
     }
 };
@@ -112,10 +117,10 @@ struct MapKeyHash {
 std::mutex g_map_mu;
 std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 
-// 2-D bf16 tensor map, dim0 innermost (contiguous), SWIZZLE_128B, OOB -> zero.
+// 2-D tensor map, dim0 innermost (contiguous); swz = swizzle span in bytes (0/32/64/128).
 int make_map(CUtensorMap* out, const void* ptr, uint64_t d0, uint64_t d1, uint64_t row_bytes, uint32_t b0,
-             uint32_t b1) {
-    MapKey key{ptr, d0, d1, row_bytes, b0, b1};
+             uint32_t b1, int dtype = CODA_BF16, int swz = 128) {
+    MapKey key{ptr, d0, d1, row_bytes, b0, b1, dtype, swz};
     {
         std::lock_guard<std::mutex> lk(g_map_mu);
         auto it = g_maps.find(key);
@@ -130,8 +135,12 @@ int make_map(CUtensorMap* out, const void* ptr, uint64_t d0, uint64_t d1, uint64
     cuuint64_t strides[1] = {row_bytes};
     cuuint32_t box[2] = {b0, b1};
     cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+    const CUtensorMapSwizzle sw = swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swz == 64  ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : swz == 32  ? CU_TENSOR_MAP_SWIZZLE_32B
+                                             : CU_TENSOR_MAP_SWIZZLE_NONE;
+    const CUtensorMapDataType dt = dtype == CODA_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    CUresult r = enc(out, dt, 2, const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(CODA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     std::lock_guard<std::mutex> lk(g_map_mu);
@@ -173,6 +182,112 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const coda::GemmPa
 
 inline unsigned grid1d(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 
+// ---------------------------------------------------------------- specialised epilogues
+using coda::F_AUX;
+using coda::F_OUT_F32;
+using coda::F_RESIDUAL;
+using coda::F_RMSBWD;
+using coda::F_RMSBWD_ACC;
+using coda::F_ROPE;
+using coda::F_ROWSCALE;
+using coda::F_ROWVEC;
+using coda::F_STORE_MAIN;
+using coda::F_SUMSQ;
+using coda::F_SWIGLU;
+using coda::F_SWIGLU_BWD;
+
+#define CODA_FAST_SETS(X)                                             \
+    X(F_STORE_MAIN)                                                   \
+    X(F_STORE_MAIN | F_OUT_F32)                                       \
+    X(F_ROPE | F_STORE_MAIN)                                          \
+    X(F_SWIGLU | F_STORE_MAIN)                                        \
+    X(F_AUX | F_SWIGLU | F_STORE_MAIN)                                \
+    X(F_RESIDUAL | F_AUX | F_SUMSQ | F_ROWVEC | F_STORE_MAIN)         \
+    X(F_RESIDUAL | F_AUX | F_SUMSQ)                                   \
+    X(F_ROWSCALE | F_STORE_MAIN)                                      \
+    X(F_ROWSCALE | F_AUX | F_SWIGLU | F_STORE_MAIN)                   \
+    X(F_ROWSCALE | F_ROPE | F_STORE_MAIN)                             \
+    X(F_RMSBWD | F_STORE_MAIN)                                        \
+    X(F_RMSBWD | F_RMSBWD_ACC | F_STORE_MAIN)                         \
+    X(F_SWIGLU_BWD | F_STORE_MAIN)
+
+template <int FL>
+int launch_fast_fl(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mm, const CUtensorMap& mx,
+                   const coda::FastParams& P, cudaStream_t st) {
+    static bool configured = false;
+    const size_t smem = coda::fast_smem_bytes();
+    auto kern = coda::coda_gemm_fast<__nv_bfloat16, FL>;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(fast smem)");
+        configured = true;
+    }
+    const int nsm = num_sms();
+    const int grid = P.mp.ntiles < nsm ? P.mp.ntiles : nsm;
+    kern<<<grid, coda::FAST_THREADS, smem, st>>>(ma, mb, mm, mx, P);
+    return cuda_check(cudaGetLastError(), "coda_gemm_fast launch");
+}
+
+bool fast_supported(int fl) {
+#define CODA_FAST_CASE(F) if (fl == (F)) return true;
+    CODA_FAST_SETS(CODA_FAST_CASE)
+#undef CODA_FAST_CASE
+    return false;
+}
+
+int launch_fast(int fl, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mm, const CUtensorMap& mx,
+                const coda::FastParams& P, cudaStream_t st) {
+#define CODA_FAST_CASE(F) if (fl == (F)) return launch_fast_fl<(F)>(ma, mb, mm, mx, P, st);
+    CODA_FAST_SETS(CODA_FAST_CASE)
+#undef CODA_FAST_CASE
+    return fail(CODA_E_CONFIG, "no specialised kernel for flags 0x%x", fl);
+}
+
+// Map a validated program onto the flag set of a specialised kernel (or -1).
+int match_fast(const coda_problem_t* pr, const coda_step_t* steps, int nsteps, const coda_store_t* stores) {
+    static const bool force_generic = [] {
+        const char* e = getenv("CODA_FORCE_GENERIC");
+        return e && e[0] && e[0] != '0';
+    }();
+    if (force_generic || pr->storage != CODA_BF16) return -1;
+    int fl = 0, last_rank = 0;
+    auto rank_ok = [&](int rk) {
+        if (rk <= last_rank) return false;
+        last_rank = rk;
+        return true;
+    };
+    for (int s = 0; s < nsteps; ++s) {
+        const coda_step_t& st = steps[s];
+        if (st.width2 != 2) return -1;   // every fast op runs at factor 1
+        switch (st.op) {
+        case CODA_OP_ROW_SCALE: if (!rank_ok(1)) return -1; fl |= F_ROWSCALE; break;
+        case CODA_OP_RESIDUAL_ADD: if (!rank_ok(2)) return -1; fl |= F_RESIDUAL; break;
+        case CODA_OP_AUX_TILE_STORE: if (!rank_ok(3)) return -1; fl |= F_AUX; break;
+        case CODA_OP_PARTIAL_SUMSQ:
+            if (!rank_ok(4) || !stores[st.arg[0]].aligned) return -1;
+            fl |= F_SUMSQ; break;
+        case CODA_OP_ROW_VEC_MUL: if (!rank_ok(5)) return -1; fl |= F_ROWVEC; break;
+        case CODA_OP_ROPE: if (!rank_ok(6)) return -1; fl |= F_ROPE; break;
+        case CODA_OP_SWIGLU: if (!rank_ok(7)) return -1; fl |= F_SWIGLU; break;
+        case CODA_OP_SWIGLU_BWD:
+            if (!rank_ok(7) || !stores[st.arg[2]].aligned) return -1;
+            fl |= F_SWIGLU_BWD; break;
+        case CODA_OP_RMSNORM_BWD:
+            if (!rank_ok(7) || !stores[st.arg[6]].aligned) return -1;
+            fl |= F_RMSBWD | (st.arg[4] >= 0 ? F_RMSBWD_ACC : 0); break;
+        default: return -1;
+        }
+    }
+    if (pr->store_main) fl |= F_STORE_MAIN;
+    if (pr->out_dtype == CODA_F32) {
+        if (fl != F_STORE_MAIN) return -1;
+        fl |= F_OUT_F32;
+    }
+    return fast_supported(fl) ? fl : -1;
+}
+
+int store_swizzle(int row_bytes) { return row_bytes >= 128 ? 128 : row_bytes; }
+
 }  // namespace
 
 extern "C" {
@@ -185,7 +300,8 @@ int coda_num_sms(void) { return num_sms(); }
 
 int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const coda_tensor_t* b,
                        const coda_step_t* steps, int nsteps, const coda_tensor_t* operands, int noperands,
-                       const coda_store_t* stores, int nstores, const coda_tensor_t* main_out, void* stream) {
+                       const coda_store_t* stores, int nstores, const coda_tensor_t* main_out,
+                       const coda_tensor_t* acc_in, void* stream) {
     if (!pr) return fail(CODA_E_BINDING, "null problem");
     const int64_t M = pr->m, N = pr->n, K = pr->k;
     if (M <= 0 || N <= 0 || K <= 0) return fail(CODA_E_DIMENSION, "problem dims must be positive");
@@ -300,6 +416,15 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         P.ld_out = main_out->ld;
     }
 
+    if (acc_in) {
+        if ((rc = check_tensor2d(acc_in, "acc_in", CODA_F32))) return rc;
+        if (acc_in->rows != M || acc_in->cols != N)
+            return fail(CODA_E_DIMENSION, "acc_in has shape (%lld,%lld), expected (%lld,%lld)",
+                        (long long)acc_in->rows, (long long)acc_in->cols, (long long)M, (long long)N);
+        P.acc_in = static_cast<const float*>(acc_in->ptr);
+        P.ld_acc = acc_in->ld;
+    }
+
     CUtensorMap ma, mb;
     if (!pr->trans_a) rc = make_map(&ma, a->ptr, (uint64_t)K, (uint64_t)M, (uint64_t)a->ld * 2, coda::BK, coda::BM);
     else rc = make_map(&ma, a->ptr, (uint64_t)M, (uint64_t)K, (uint64_t)a->ld * 2, 64, coda::BK);
@@ -309,6 +434,68 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
     if (rc) return rc;
 
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+
+    const int fl = match_fast(pr, steps, nsteps, stores);
+    if (fl >= 0) {
+        coda::FastParams F;
+        memset(&F, 0, sizeof(F));
+        F.mp = coda::MainParams{P.M, P.N, P.K, P.ntm, P.ntn, P.nk, P.ntiles, P.a_mn, P.b_mn};
+        F.acc_in = P.acc_in;
+        F.ld_acc = P.ld_acc;
+        F.rope_sign = 1.0f;
+        int aux_slot = -1;
+        for (int s = 0; s < nsteps; ++s) {
+            const coda_step_t& cs = steps[s];
+            const coda::DevOperand* o = P.opnd;
+            switch (cs.op) {
+            case CODA_OP_ROW_SCALE: F.rowscale = (const float*)o[cs.arg[0]].ptr; break;
+            case CODA_OP_RESIDUAL_ADD: F.residual = o[cs.arg[0]].ptr; F.ld_res = o[cs.arg[0]].ld; break;
+            case CODA_OP_AUX_TILE_STORE: aux_slot = cs.arg[0]; break;
+            case CODA_OP_PARTIAL_SUMSQ:
+                F.rowpart = (float*)P.store[cs.arg[0]].ptr; F.ld_rowpart = P.store[cs.arg[0]].ld;
+                F.rowpart_map = P.store[cs.arg[0]].map; break;
+            case CODA_OP_ROW_VEC_MUL: F.rowvec = (const float*)o[cs.arg[0]].ptr; break;
+            case CODA_OP_ROPE:
+                F.cosp = o[cs.arg[0]].ptr; F.ld_cos = o[cs.arg[0]].ld;
+                F.sinp = o[cs.arg[1]].ptr; F.ld_sin = o[cs.arg[1]].ld;
+                F.rope_sign = cs.arg[2] ? -1.0f : 1.0f; break;
+            case CODA_OP_SWIGLU_BWD:
+                F.preact2 = o[cs.arg[0]].ptr; F.ld_pre2 = o[cs.arg[0]].ld;
+                aux_slot = cs.arg[1];
+                F.rowpart = (float*)P.store[cs.arg[2]].ptr; F.ld_rowpart = P.store[cs.arg[2]].ld;
+                F.rowpart_map = P.store[cs.arg[2]].map; break;
+            case CODA_OP_RMSNORM_BWD:
+                F.pre = o[cs.arg[0]].ptr; F.ld_pre = o[cs.arg[0]].ld;
+                F.inv_rms = (const float*)o[cs.arg[1]].ptr;
+                F.gamma = (const float*)o[cs.arg[2]].ptr;
+                F.stat = (const float*)o[cs.arg[3]].ptr;
+                if (cs.arg[4] >= 0) { F.grad_in = o[cs.arg[4]].ptr; F.ld_gin = o[cs.arg[4]].ld; }
+                aux_slot = cs.arg[5];
+                F.colpart = (float*)P.store[cs.arg[6]].ptr; F.ld_colpart = P.store[cs.arg[6]].ld;
+                F.colpart_map = P.store[cs.arg[6]].map; break;
+            default: break;
+            }
+        }
+        CUtensorMap mm, mx;
+        memset(&mm, 0, sizeof(mm));
+        memset(&mx, 0, sizeof(mx));
+        if (P.store_main) {
+            const int odt = P.out_f32 ? CODA_F32 : CODA_BF16;
+            const int es = P.out_f32 ? 4 : 2;
+            const int wv = w;                  // values per 32-column chunk after the program
+            const int rb = wv * es;
+            rc = make_map(&mm, main_out->ptr, (uint64_t)main_out->cols, (uint64_t)M, (uint64_t)main_out->ld * es,
+                          (uint32_t)wv, rb >= 128 ? 16u : 32u, odt, store_swizzle(rb));
+            if (rc) return rc;
+        }
+        if (aux_slot >= 0) {
+            const coda_store_t& xs = stores[aux_slot];
+            rc = make_map(&mx, xs.t.ptr, (uint64_t)xs.t.cols, (uint64_t)M, (uint64_t)xs.t.ld * 2, 32u, 32u, CODA_BF16,
+                          64);
+            if (rc) return rc;
+        }
+        return launch_fast(fl, ma, mb, mm, mx, F, st);
+    }
     if (sdt == CODA_BF16) return launch_gemm<__nv_bfloat16>(ma, mb, P, st);
     return launch_gemm<float>(ma, mb, P, st);
 }

@@ -1,0 +1,450 @@
+// coda_fast.cuh — compile-time specialised epilogues for the fused CODA launches.
+//
+// The generic interpreter (coda_gemm.cuh) executes any valid EpilogueProgram.
+// The reference's hot programs (tilefuse/kernels.py:243-557: K1, K2, K4-K7,
+// K9, K10 and the plain dgrad/wgrad GEMMs) are additionally compiled as
+// flag-specialised kernels with:
+//
+//   * 8 epilogue warps: warp w reads TMEM lane quadrant w%4 (32 rows, thread ==
+//     row) and one 128-column half of the 128x256 accumulator, in 32-column
+//     chunks (tcgen05.ld.32x32b.x32);
+//   * stores staged through a per-warp 4 KiB swizzled smem buffer and written
+//     by TMA (cp.async.bulk.tensor ... bulk_group) — fully coalesced, and the
+//     tensor maps clip ragged edges;
+//   * thread-local row reductions (sum of squares, <preact, grad>) and a
+//     warp-butterfly column reduction (31 shuffles for 32 columns) combined
+//     across the four row quadrants through 2 KiB of smem, in fixed order.
+//
+// Op order is the canonical order of the reference programs:
+//   acc_in -> RowScale -> ResidualAdd -> AuxTileStore -> PartialSumSq ->
+//   RowVecMul -> PairwiseRope -> PairwiseSwiglu | PairwiseSwigluBackward |
+//   RmsNormBackwardLocal -> main store.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include "coda_gemm.cuh"
+#include "coda_mainloop.cuh"
+#include "coda_ptx.cuh"
+
+namespace coda {
+
+enum FastFlags : int {
+    F_ROWSCALE = 1 << 0,
+    F_RESIDUAL = 1 << 1,
+    F_AUX = 1 << 2,         // AuxTileStore of the running tile (factor 1)
+    F_SUMSQ = 1 << 3,
+    F_ROWVEC = 1 << 4,
+    F_ROPE = 1 << 5,
+    F_SWIGLU = 1 << 6,
+    F_SWIGLU_BWD = 1 << 7,  // aux = recompute, rowpart = <preact, grad> at factor 2
+    F_RMSBWD = 1 << 8,      // aux = normed, colpart = gamma-grad pieces
+    F_RMSBWD_ACC = 1 << 9,
+    F_STORE_MAIN = 1 << 10,
+    F_OUT_F32 = 1 << 11,
+};
+
+constexpr int FAST_EPI_WARPS = 8;
+constexpr int FAST_THREADS = 64 + 32 * FAST_EPI_WARPS;
+constexpr int STG_BYTES = 4096;                   // per epilogue warp: two 2 KiB regions
+constexpr int COLRED_BYTES = 2 * 2 * 4 * 32 * 4;  // [half][buf][quadrant][32] f32
+
+struct FastParams {
+    MainParams mp;
+    const float* acc_in;
+    int64_t ld_acc;
+    const float* rowscale;
+    const void* residual;
+    int64_t ld_res;
+    const float* rowvec;
+    const void* cosp;
+    int64_t ld_cos;
+    const void* sinp;
+    int64_t ld_sin;
+    float rope_sign;
+    const void* preact2;
+    int64_t ld_pre2;
+    const void* pre;
+    int64_t ld_pre;
+    const float* inv_rms;
+    const float* gamma;
+    const float* stat;
+    const void* grad_in;
+    int64_t ld_gin;
+    float* rowpart;
+    int64_t ld_rowpart;
+    const int32_t* rowpart_map;
+    float* colpart;
+    int64_t ld_colpart;
+    const int32_t* colpart_map;
+};
+
+constexpr size_t fast_smem_bytes() {
+    return (size_t)STAGES * STAGE_BYTES + (size_t)FAST_EPI_WARPS * STG_BYTES + COLRED_BYTES + (2 * STAGES + 4) * 8 + 16;
+}
+
+// -------------------------------------------------------------- row-segment loads
+// W values of a row starting at column c0 into d[]; zero for !ok rows and for
+// columns >= ncols (tensor rows are padded to 16 B so a vector that starts
+// inside the row never leaves the allocation).
+template <typename TS, int W>
+__device__ __forceinline__ void fload(const TS* rowp, int64_t c0, int64_t ncols, bool ok, float* d) {
+    constexpr int V = Io<TS>::V;
+#pragma unroll
+    for (int i = 0; i < W; i += V) {
+        if (ok && c0 + i < ncols) {
+            Io<TS>::load(rowp + c0 + i, d + i);
+        } else {
+#pragma unroll
+            for (int e = 0; e < V; ++e) d[i + e] = 0.0f;
+        }
+    }
+    if (c0 + W > ncols) {
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            if (c0 + i >= ncols) d[i] = 0.0f;
+    }
+}
+
+template <int W>
+__device__ __forceinline__ void fload_vec(const float* vp, int64_t c0, int64_t n, float* d) {
+#pragma unroll
+    for (int i = 0; i < W; i += 4) {
+        if (c0 + i + 4 <= n) {
+            const float4 u = __ldg(reinterpret_cast<const float4*>(vp + c0 + i));
+            d[i] = u.x; d[i + 1] = u.y; d[i + 2] = u.z; d[i + 3] = u.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) d[i + e] = (c0 + i + e < n) ? __ldg(vp + c0 + i + e) : 0.0f;
+        }
+    }
+}
+
+// -------------------------------------------------------------- staged TMA stores
+// Per-warp staging: region r (0/1) = 2 KiB at stg + 2048 r.  A store of W
+// elements of TO per row (RB = row bytes <= 64) uses one region; RB == 128
+// uses both (rows 0-15 / 16-31, two 16-row TMA boxes).  `wide_pending`
+// remembers that the last committed group occupied both regions.
+struct Stager {
+    uint32_t base;      // smem address of this warp's 4 KiB buffer (1024-aligned)
+    int region;
+    bool wide_pending;
+};
+
+template <typename TO, int W>
+__device__ __forceinline__ void staged_store(Stager& sg, const CUtensorMap* tm, int x, int y, const float* v,
+                                             int lane) {
+    constexpr int RB = W * (int)sizeof(TO);
+    static_assert(RB == 32 || RB == 64 || RB == 128, "row bytes per staged store");
+    constexpr uint32_t MASK = RB == 128 ? 0x70u : (RB == 64 ? 0x30u : 0x10u);
+    // 1. make sure the bytes we are about to overwrite were read by earlier stores
+    if (lane == 0) {
+        if (RB == 128 || sg.wide_pending) bulk_wait_read<0>();
+        else bulk_wait_read<1>();
+    }
+    __syncwarp();
+    uint32_t rbase;
+    int r;
+    if (RB == 128) {
+        rbase = sg.base + (uint32_t)((lane >> 4) * 2048);
+        r = lane & 15;
+    } else {
+        rbase = sg.base + (uint32_t)(sg.region * 2048);
+        r = lane;
+    }
+    // 2. write this thread's row, 16 B at a time, in the TMA swizzle pattern
+#pragma unroll
+    for (int c = 0; c < RB / 16; ++c) {
+        const uint32_t off = (uint32_t)(r * RB + c * 16);
+        const uint32_t phys = off ^ ((off >> 3) & MASK);
+        uint32_t w0, w1, w2, w3;
+        if constexpr (sizeof(TO) == 2) {
+            w0 = pack_bf16x2(v[c * 8 + 0], v[c * 8 + 1]);
+            w1 = pack_bf16x2(v[c * 8 + 2], v[c * 8 + 3]);
+            w2 = pack_bf16x2(v[c * 8 + 4], v[c * 8 + 5]);
+            w3 = pack_bf16x2(v[c * 8 + 6], v[c * 8 + 7]);
+        } else {
+            w0 = __float_as_uint(v[c * 4 + 0]);
+            w1 = __float_as_uint(v[c * 4 + 1]);
+            w2 = __float_as_uint(v[c * 4 + 2]);
+            w3 = __float_as_uint(v[c * 4 + 3]);
+        }
+        st_shared_v4(rbase + phys, w0, w1, w2, w3);
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    // 3. one lane hands the box to the TMA engine
+    if (lane == 0) {
+        if (RB == 128) {
+            tma_store_2d(tm, sg.base, x, y);
+            tma_store_2d(tm, sg.base + 2048, x, y + 16);
+        } else {
+            tma_store_2d(tm, rbase, x, y);
+        }
+        bulk_commit();
+    }
+    if (RB == 128) {
+        sg.wide_pending = true;
+    } else {
+        sg.wide_pending = false;
+        sg.region ^= 1;
+    }
+}
+
+// Column sums over the warp's 32 rows: lane l ends with column l (fixed tree).
+__device__ __forceinline__ float warp_colsum32(float (&x)[32], int lane) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < off; ++i) {
+            const float send = up ? x[i] : x[i + off];
+            const float keep = up ? x[i + off] : x[i];
+            x[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    return x[0];
+}
+
+// -------------------------------------------------------------- kernel
+template <typename TS, int FL>
+__global__ void __launch_bounds__(FAST_THREADS, 1)
+coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+               const __grid_constant__ CUtensorMap tma_main, const __grid_constant__ CUtensorMap tma_aux,
+               const __grid_constant__ FastParams P) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
+    uint8_t* stg = sB + STAGES * B_STAGE_BYTES;
+    float* colred = reinterpret_cast<float*>(stg + FAST_EPI_WARPS * STG_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(colred) + COLRED_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const MainParams& mp = P.mp;
+
+    if (threadIdx.x == 0) {
+        if (smem_u32(smem) & 1023u) __trap();   // swizzled TMA buffers need 1 KiB alignment
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 32 * FAST_EPI_WARPS);
+        }
+        fence_mbar_init();
+        tma_prefetch_desc(&tma_a);
+        tma_prefetch_desc(&tma_b);
+        if (FL & F_STORE_MAIN) tma_prefetch_desc(&tma_main);
+        if (FL & (F_AUX | F_SWIGLU_BWD | F_RMSBWD)) tma_prefetch_desc(&tma_aux);
+    }
+    if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) producer_loop(mp, &tma_a, &tma_b, sA, sB, full, empty);
+    } else if (warp == 1) {
+        if (lane == 0) mma_loop(mp, tmem_base, sA, sB, full, empty, tfull, tempty);
+    } else {
+        const int ew = warp - 2;            // 0..7
+        const int q = warp & 3;             // TMEM lane quadrant
+        const int h = ew >> 2;              // column half of the 256-wide tile
+        const int lrow = q * 32 + lane;
+        const int M = mp.M, N = mp.N;
+        Stager sg{smem_u32(stg + ew * STG_BYTES), 0, false};
+        int cbuf = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < mp.ntiles; t += gridDim.x) {
+            int tm, tn;
+            tile_coord(mp, t, tm, tn);
+            const int m0 = tm * BM;
+            const int n0 = tn * BN;
+            const int64_t row = (int64_t)m0 + lrow;
+            const bool row_ok = row < M;
+            float rsc = 1.0f, rr = 0.0f, ss = 0.0f;
+            if ((FL & F_ROWSCALE) && row_ok) rsc = __ldg(P.rowscale + row);
+            if ((FL & F_RMSBWD) && row_ok) {
+                rr = __ldg(P.inv_rms + row);
+                ss = __ldg(P.stat + row);
+            }
+            float pacc = 0.0f;
+            int ppid = -1;
+
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + h * 128);
+
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                float v[32];
+                tmem_ld32(tbase + c * 32, v);
+                if (c == 3) {
+                    tc_fence_before();
+                    mbar_arrive(&tempty[acc]);
+                }
+                const int gcol0 = n0 + h * 128 + c * 32;
+                if (gcol0 >= N) continue;   // uniform for the 4 warps of this half
+                const bool edge = gcol0 + 32 > N;
+                if (P.acc_in != nullptr) {
+                    float x[32];
+                    fload<float, 32>(P.acc_in + row * P.ld_acc, gcol0, N, row_ok, x);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] += x[i];
+                }
+                if (FL & F_ROWSCALE) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] *= rsc;
+                }
+                if (FL & F_RESIDUAL) {
+                    float x[32];
+                    fload<TS, 32>(static_cast<const TS*>(P.residual) + row * P.ld_res, gcol0, N, row_ok, x);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] += x[i];
+                }
+                if (FL & F_AUX) staged_store<TS, 32>(sg, &tma_aux, gcol0, m0 + q * 32, v, lane);
+                if (FL & F_SUMSQ) {
+                    float s = 0.0f;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) s += v[i] * v[i];
+                    const int pid = __ldg(P.rowpart_map + gcol0);
+                    if (pid != ppid) {
+                        if (ppid >= 0 && row_ok) P.rowpart[row * P.ld_rowpart + ppid] = pacc;
+                        ppid = pid;
+                        pacc = 0.0f;
+                    }
+                    pacc += s;
+                }
+                if (FL & F_ROWVEC) {
+                    float g[32];
+                    fload_vec<32>(P.rowvec, gcol0, N, g);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] *= g[i];
+                }
+                if (FL & F_ROPE) {
+                    float cs[32], sn[32];
+                    fload<TS, 32>(static_cast<const TS*>(P.cosp) + row * P.ld_cos, gcol0, N, row_ok, cs);
+                    fload<TS, 32>(static_cast<const TS*>(P.sinp) + row * P.ld_sin, gcol0, N, row_ok, sn);
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float x0 = v[2 * k], x1 = v[2 * k + 1];
+                        const float se = P.rope_sign * sn[2 * k], so = P.rope_sign * sn[2 * k + 1];
+                        v[2 * k] = x0 * cs[2 * k] - x1 * se;
+                        v[2 * k + 1] = x0 * so + x1 * cs[2 * k + 1];
+                    }
+                }
+                if (FL & F_SWIGLU) {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float g = v[2 * k], u = v[2 * k + 1];
+                        v[k] = g * sigmoid_stable(g) * u;
+                    }
+                    if (FL & F_STORE_MAIN) staged_store<TS, 16>(sg, &tma_main, gcol0 / 2, m0 + q * 32, v, lane);
+                } else if (FL & F_SWIGLU_BWD) {
+                    float z[64];
+                    fload<TS, 64>(static_cast<const TS*>(P.preact2) + row * P.ld_pre2, 2 * (int64_t)gcol0,
+                                  2 * (int64_t)N, row_ok, z);
+                    float rec[32];
+                    float s = 0.0f;
+                    float o[64];
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) {
+                        const float g = z[2 * k], u = z[2 * k + 1], dd = v[k];
+                        const float sg_ = sigmoid_stable(g);
+                        const float sl = g * sg_;
+                        rec[k] = sl * u;
+                        const float gu = dd * sl;
+                        const float gg = dd * u * (sg_ + sl * (1.0f - sg_));
+                        o[2 * k] = gg;
+                        o[2 * k + 1] = gu;
+                        s += g * gg;
+                        s += u * gu;
+                    }
+                    staged_store<TS, 32>(sg, &tma_aux, gcol0, m0 + q * 32, rec, lane);
+                    const int pid = __ldg(P.rowpart_map + 2 * gcol0);
+                    if (pid != ppid) {
+                        if (ppid >= 0 && row_ok) P.rowpart[row * P.ld_rowpart + ppid] = pacc;
+                        ppid = pid;
+                        pacc = 0.0f;
+                    }
+                    pacc += s;
+                    if (FL & F_STORE_MAIN) staged_store<TS, 64>(sg, &tma_main, 2 * gcol0, m0 + q * 32, o, lane);
+                } else if (FL & F_RMSBWD) {
+                    float cp[32], g[32], tmp[32];
+                    fload<TS, 32>(static_cast<const TS*>(P.pre) + row * P.ld_pre, gcol0, N, row_ok, cp);
+                    fload_vec<32>(P.gamma, gcol0, N, g);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        cp[i] *= rr;             // c_n
+                        tmp[i] = cp[i] * g[i];   // normed
+                    }
+                    staged_store<TS, 32>(sg, &tma_aux, gcol0, m0 + q * 32, tmp, lane);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) tmp[i] = v[i] * cp[i];
+                    const float csum = warp_colsum32(tmp, lane);
+                    float* red = colred + ((h * 2 + cbuf) * 4) * 32;
+                    red[q * 32 + lane] = csum;
+                    named_bar_sync(2 + h, 128);
+                    if (q == 0) {
+                        const int gc = gcol0 + lane;
+                        if (gc < N) {
+                            int pid = -1;
+                            float a = 0.0f;
+#pragma unroll
+                            for (int qq = 0; qq < 4; ++qq) {
+                                const int r0 = m0 + 32 * qq;
+                                if (r0 < M) {
+                                    const int p = __ldg(P.colpart_map + r0);
+                                    if (p != pid) {
+                                        if (pid >= 0) P.colpart[(int64_t)pid * P.ld_colpart + gc] = a;
+                                        pid = p;
+                                        a = 0.0f;
+                                    }
+                                    a += red[qq * 32 + lane];
+                                }
+                            }
+                            if (pid >= 0) P.colpart[(int64_t)pid * P.ld_colpart + gc] = a;
+                        }
+                    }
+                    cbuf ^= 1;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = (v[i] * g[i] - cp[i] * ss) * rr;
+                    if (FL & F_RMSBWD_ACC) {
+                        float x[32];
+                        fload<TS, 32>(static_cast<const TS*>(P.grad_in) + row * P.ld_gin, gcol0, N, row_ok, x);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] += x[i];
+                    }
+                    if (FL & F_STORE_MAIN) staged_store<TS, 32>(sg, &tma_main, gcol0, m0 + q * 32, v, lane);
+                } else if (FL & F_STORE_MAIN) {
+                    if (FL & F_OUT_F32) staged_store<float, 32>(sg, &tma_main, gcol0, m0 + q * 32, v, lane);
+                    else staged_store<TS, 32>(sg, &tma_main, gcol0, m0 + q * 32, v, lane);
+                }
+                (void)edge;
+            }
+            if ((FL & (F_SUMSQ | F_SWIGLU_BWD)) && ppid >= 0 && row_ok) P.rowpart[row * P.ld_rowpart + ppid] = pacc;
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+        if (lane == 0) bulk_wait<0>();
+        __syncwarp();
+    }
+
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<TMEM_COLS>(tmem_base);
+    }
+}
+
+}  // namespace coda

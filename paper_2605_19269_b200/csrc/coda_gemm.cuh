@@ -21,22 +21,14 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include "coda_ptx.cuh"
+#include "coda_mainloop.cuh"
 
 namespace coda {
 
-constexpr int BM = 128;
-constexpr int BN = 256;
-constexpr int BK = 64;                 // one 128-byte swizzle atom of bf16 along K
-constexpr int STAGES = 4;
-constexpr int A_STAGE_BYTES = BM * BK * 2;   // 16 KiB
-constexpr int B_STAGE_BYTES = BN * BK * 2;   // 32 KiB
-constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int EPI_WARPS = 4;
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;   // producer, mma, 4 epilogue warps
 constexpr int CHUNK = 32;                    // accumulator columns per tcgen05.ld
 constexpr int RED_LD = 33;                   // padded row stride of the col-sum scratch
-constexpr int TMEM_COLS = 512;               // 2 accumulator buffers x 256 columns
-constexpr int RASTER_GROUP = 16;             // m-tiles per raster group (L2 reuse)
 
 constexpr int MAX_STEPS = 8;
 constexpr int MAX_SLOTS = 8;
@@ -72,6 +64,8 @@ struct GemmParams {
     int store_main, out_f32, out_w;   // out_w: values per chunk at program end
     void* out;
     int64_t ld_out;
+    const float* acc_in;     // optional f32 (M, N) added before the program (K-chunked SIM32 GEMMs)
+    int64_t ld_acc;
     DevStep steps[MAX_STEPS];
     DevOperand opnd[MAX_SLOTS];
     DevStore store[MAX_SLOTS];
@@ -327,89 +321,13 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int ntn = P.ntn;
-    auto tile_mn = [&](int t, int& tm, int& tn) {
-        const int per_group = RASTER_GROUP * ntn;
-        const int g = t / per_group;
-        const int first = g * RASTER_GROUP;
-        const int gs = min(P.ntm - first, RASTER_GROUP);
-        const int r = t - g * per_group;
-        tm = first + r % gs;
-        tn = r / gs;
-    };
+    const MainParams mp{P.M, P.N, P.K, P.ntm, P.ntn, P.nk, P.ntiles, P.a_mn, P.b_mn};
+    auto tile_mn = [&](int t, int& tm, int& tn) { tile_coord(mp, t, tm, tn); };
 
     if (warp == 0) {
-        // ------------------------------------------------ TMA producer
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
-                int tm, tn;
-                tile_mn(t, tm, tn);
-                const int m0 = tm * BM, n0 = tn * BN;
-                for (int kb = 0; kb < P.nk; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-                    const uint32_t sa = smem_u32(sA + stage * A_STAGE_BYTES);
-                    const uint32_t sb = smem_u32(sB + stage * B_STAGE_BYTES);
-                    const int k0 = kb * BK;
-                    if (!P.a_mn) {
-                        tma_load_2d(sa, &tma_a, k0, m0, &full[stage]);
-                    } else {
-#pragma unroll
-                        for (int b = 0; b < BM / 64; ++b)
-                            tma_load_2d(sa + b * (BK * 128), &tma_a, m0 + 64 * b, k0, &full[stage]);
-                    }
-                    if (!P.b_mn) {
-                        tma_load_2d(sb, &tma_b, k0, n0, &full[stage]);
-                    } else {
-#pragma unroll
-                        for (int b = 0; b < BN / 64; ++b)
-                            tma_load_2d(sb + b * (BK * 128), &tma_b, n0 + 64 * b, k0, &full[stage]);
-                    }
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                }
-            }
-        }
+        if (lane == 0) producer_loop(mp, &tma_a, &tma_b, sA, sB, full, empty);
     } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            // kind::f16 instruction descriptor: D f32, A/B bf16, majorness, N>>3, M>>4.
-            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
-                                   ((uint32_t)P.a_mn << 15) | ((uint32_t)P.b_mn << 16) |
-                                   ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-            // K-major: LBO unused (16), SBO = 8 rows * 128 B; advance 32 B per UMMA_K=16.
-            // MN-major: LBO = next 64-wide MN atom column (BK*128 B), SBO = 8 K-rows * 128 B;
-            //           advance 2 x 1024 B per UMMA_K=16.
-            const uint32_t a_lbo = P.a_mn ? BK * 128 : 16, b_lbo = P.b_mn ? BK * 128 : 16;
-            const uint32_t a_step = P.a_mn ? 2048 : 32, b_step = P.b_mn ? 2048 : 32;
-            int stage = 0;
-            uint32_t phase = 0;
-            int acc = 0;
-            uint32_t acc_phase = 0;
-            for (int t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
-                tc_fence_after();
-                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-                for (int kb = 0; kb < P.nk; ++kb) {
-                    mbar_wait(&full[stage], phase);
-                    tc_fence_after();
-                    const uint32_t sa = smem_u32(sA + stage * A_STAGE_BYTES);
-                    const uint32_t sb = smem_u32(sB + stage * B_STAGE_BYTES);
-#pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {
-                        const uint64_t ad = umma_desc_sw128(sa + k * a_step, a_lbo, 1024);
-                        const uint64_t bd = umma_desc_sw128(sb + k * b_step, b_lbo, 1024);
-                        umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
-                    }
-                    umma_commit(&empty[stage]);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                }
-                umma_commit(&tfull[acc]);
-                acc ^= 1;
-                if (acc == 0) acc_phase ^= 1;
-            }
-        }
+        if (lane == 0) mma_loop(mp, tmem_base, sA, sB, full, empty, tfull, tempty);
     } else {
         // ------------------------------------------------ epilogue
         const int q = warp & 3;                 // TMEM lane quadrant this warp may read
@@ -445,6 +363,12 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
                 }
                 const int64_t gcol0 = n0 + (int64_t)j * CHUNK;
                 int w = CHUNK;
+                if (P.acc_in != nullptr && row_ok) {
+                    float x[32];
+                    load_seg<float, 32>(P.acc_in + row * P.ld_acc, gcol0, P.N, x);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] += x[i];
+                }
                 for (int s = 0; s < P.nsteps; ++s) {
                     const DevStep& st = P.steps[s];
                     switch (st.op) {

@@ -106,11 +106,13 @@ def row_pieces(n: int, tile_n: int, rtn: int, scale: int, device):
     if hit is not None:
         return hit
     blocks = scaled_row_blocks(n, tile_n, rtn, scale)
-    starts, ptr = split_at([(b.start, b.stop) for b in blocks], nat.GPU_TILE_N * scale)
+    # split at every 128-column half tile (each half belongs to one epilogue warp group)
+    starts, ptr = split_at([(b.start, b.stop) for b in blocks], nat.GPU_TILE_N // 2 * scale)
     npieces = len(starts) - 1
     pmap = np.repeat(np.arange(npieces, dtype=np.int32), np.diff(starts))
     counts = np.array([b.width for b in blocks], dtype=np.int64)
-    val = (_device_i32(pmap, device), _device_i32(ptr, device), npieces, len(blocks), counts)
+    aligned = bool(np.all(starts[:-1] % (32 * scale) == 0))
+    val = (_device_i32(pmap, device), _device_i32(ptr, device), npieces, len(blocks), counts, aligned)
     _map_cache[key] = val
     return val
 
@@ -126,7 +128,8 @@ def col_pieces(m: int, tile_m: int, device):
     npieces = len(starts) - 1
     pmap = np.repeat(np.arange(npieces, dtype=np.int32), np.diff(starts))
     counts = np.array([b - a for a, b in bounds], dtype=np.int64)
-    val = (_device_i32(pmap, device), _device_i32(ptr, device), npieces, len(bounds), counts)
+    aligned = bool(np.all(starts[:-1] % 32 == 0))
+    val = (_device_i32(pmap, device), _device_i32(ptr, device), npieces, len(bounds), counts, aligned)
     _map_cache[key] = val
     return val
 
@@ -147,6 +150,16 @@ def block_starts(n: int, tile_n: int, rtn: int, device):
 # ----------------------------------------------------------------------------- helpers
 
 
+def _tile_cols(n: int, tile_n: int) -> list[tuple[int, int]]:
+    """(col0, width) of every reference tile column; only these matter for pairing."""
+    key = ("cols", n, tile_n)
+    hit = _map_cache.get(key)
+    if hit is None:
+        hit = [(c0, min(tile_n, n - c0)) for c0 in range(0, n, tile_n)]
+        _map_cache[key] = hit
+    return hit
+
+
 def storage_tensor(mat: DenseMatrix, precision: PrecisionMode):
     """Device payload of `mat` in the storage dtype of `precision`."""
     t = mat.tensor
@@ -158,8 +171,15 @@ def storage_tensor(mat: DenseMatrix, precision: PrecisionMode):
     return as_tma_ready(t)
 
 
-_A_PATTERN = (0, 0, 1, 0, 1, 2)   # a-terms of the 6 products with i+j <= 2
-_B_PATTERN = (0, 1, 0, 2, 1, 0)   # matching b-terms
+# The six products a_i*b_j with i+j <= 2, smallest first: the tensor-core f32
+# accumulator truncates each MMA's sum relative to the running magnitude, so
+# the tiny terms are accumulated while it is still small and the dominant
+# a0*b0 term comes last.
+_A_PATTERN = (2, 1, 0, 1, 0, 0)
+_B_PATTERN = (0, 1, 2, 0, 1, 0)
+# SIM32 K-chunk: each chunk's product is summed into an f32 accumulator input
+# (software RNE adds), bounding the number of MMA accumulations per sum.
+SIM32_K_CHUNK = 256
 
 
 def split_f32(t, k_axis: int, kp: int, pattern):
@@ -226,15 +246,20 @@ def run_gemm(
     if b.shape != want_b:
         raise DimensionError(f"b has shape {b.shape}, problem wants {want_b}")
 
-    tiles = tile_coords(p.m, p.n, p.tile_shape)
-    program.check_pairing([(c.col0, c.cols) for c in tiles if c.i == 0])
+    tm_ref, tn_ref = int(p.tile_shape[0]), int(p.tile_shape[1])
+    pair_factors = tuple(s.entry_factor for s in program.steps if s.primitive.needs_pair_alignment)
+    if pair_factors:
+        key = ("pairing", pair_factors, p.n, tn_ref)
+        if key not in _map_cache:
+            program.check_pairing(_tile_cols(p.n, tn_ref))
+            _map_cache[key] = True
     n_out = program.scaled_width(p.n) if store_main else None
 
     unknown = set(bindings) - set(program.operands)
     if unknown:
         raise BindingError(f"bindings not used by the program: {sorted(unknown)}")
     if tile_order is not None:
-        grid = sorted((c.i, c.j) for c in tiles)
+        grid = sorted((c.i, c.j) for c in tile_coords(p.m, p.n, p.tile_shape))
         if sorted(tuple(x) for x in tile_order) != grid:
             raise ConfigError("tile_order must be a permutation of the launch's (i, j) grid")
 
@@ -317,19 +342,19 @@ def run_gemm(
         elif st.kind in (StoreKind.ROW_SUM, StoreKind.ROW_PAIR):
             if st.factor.denominator != 1:
                 raise ProgramError(f"partial stores need an integer width scale, got {st.factor}")
-            pmap, ptr, npc, nb, counts = row_pieces(p.n, p.tile_shape[1], p.reduction_tile_n,
-                                                    st.factor.numerator, dev)
+            pmap, ptr, npc, nb, counts, aligned = row_pieces(p.n, p.tile_shape[1], p.reduction_tile_n,
+                                                             st.factor.numerator, dev)
             pair = st.kind is StoreKind.ROW_PAIR
             t = torch.empty((p.m, npc * (2 if pair else 1)), dtype=torch.float32, device=dev)
             st_descs[i] = nat.Store(nat.tensor_desc(t), pmap.data_ptr(),
-                                    nat.STORE_ROW_PAIR if pair else nat.STORE_ROW_SUM, 0)
+                                    nat.STORE_ROW_PAIR if pair else nat.STORE_ROW_SUM, int(aligned))
             keep.append(pmap)
             folds.append((name, st.kind, t, ptr, nb, counts, npc))
             write_bytes += (2 if pair else 1) * p.m * nb * pw
         elif st.kind is StoreKind.COL_SUM:
-            pmap, ptr, npc, nb, counts = col_pieces(p.m, p.tile_shape[0], dev)
+            pmap, ptr, npc, nb, counts, aligned = col_pieces(p.m, p.tile_shape[0], dev)
             t = torch.empty((npc, width), dtype=torch.float32, device=dev)
-            st_descs[i] = nat.Store(nat.tensor_desc(t), pmap.data_ptr(), nat.STORE_COL_SUM, 0)
+            st_descs[i] = nat.Store(nat.tensor_desc(t), pmap.data_ptr(), nat.STORE_COL_SUM, int(aligned))
             keep.append(pmap)
             folds.append((name, st.kind, t, ptr, nb, counts, npc))
             write_bytes += nb * width * pw
@@ -339,17 +364,6 @@ def run_gemm(
             st_descs[i] = nat.Store(nat.tensor_desc(t), None, nat.STORE_GATHER, 0)
             write_bytes += p.m * pw
 
-    # ---- A / B in the kernel's operand format
-    if prec is PrecisionMode.SIMBF16:
-        ta, tb = storage_tensor(a, prec), storage_tensor(b, prec)
-        kk = p.k
-    else:
-        kp = -(-p.k // 8) * 8
-        fa, fb = storage_tensor(a, prec), storage_tensor(b, prec)
-        ta = split_f32(fa, 0 if p.trans_a else 1, kp, _A_PATTERN)
-        tb = split_f32(fb, 1 if p.trans_b else 0, kp, _B_PATTERN)
-        kk = 6 * kp
-
     main_t = None
     main_desc = None
     if store_main:
@@ -357,16 +371,43 @@ def run_gemm(
         main_t = alloc_matrix(p.m, n_out, odt, dev)
         main_desc = nat.tensor_desc(main_t)
         write_bytes += p.m * n_out * prec.storage_bytes
-
-    prob = nat.Problem(p.m, p.n, kk, int(p.trans_a), int(p.trans_b), scode,
-                       nat.F32 if (out_f32 or scode == nat.F32) else nat.BF16, int(store_main), 0)
     step_arr = (nat.Step * max(1, len(steps)))()
     for i, (op, w2, args) in enumerate(steps):
         step_arr[i] = nat.Step(op, w2, (ctypes.c_int32 * 7)(*args), 0)
-    nat.call("coda_gemm_epilogue", ctypes.byref(prob), ctypes.byref(nat.tensor_desc(ta)),
-             ctypes.byref(nat.tensor_desc(tb)), step_arr, len(steps), op_descs, len(onames),
-             st_descs, len(snames), ctypes.byref(main_desc) if main_desc is not None else None,
-             _stream(dev))
+
+    def enqueue(ta, tb, kk, program_on, mdesc, acc_t, odtype):
+        prob = nat.Problem(p.m, p.n, kk, int(p.trans_a), int(p.trans_b), scode, odtype,
+                           int(mdesc is not None), 0)
+        acc_desc = nat.tensor_desc(acc_t) if acc_t is not None else None
+        nat.call("coda_gemm_epilogue", ctypes.byref(prob), ctypes.byref(nat.tensor_desc(ta)),
+                 ctypes.byref(nat.tensor_desc(tb)), step_arr, len(steps) if program_on else 0, op_descs,
+                 len(onames), st_descs, len(snames) if program_on else 0,
+                 ctypes.byref(mdesc) if mdesc is not None else None,
+                 ctypes.byref(acc_desc) if acc_desc is not None else None, _stream(dev),
+                 tag=f"{kernel_name} {p.m}x{p.n}x{p.k}{' TN' if p.trans_a else ''}{' NT' if p.trans_b else ''}",
+                 flops=2.0 * p.m * p.n * (kk if scode == nat.BF16 else kk // 6))
+
+    out_code = nat.F32 if (out_f32 or scode == nat.F32) else nat.BF16
+    if prec is PrecisionMode.SIMBF16:
+        enqueue(storage_tensor(a, prec), storage_tensor(b, prec), p.k, True, main_desc, None, out_code)
+    else:
+        # SIM32: f32 operands as 6-term bf16 splits, K chunked with an f32 running sum
+        fa, fb = storage_tensor(a, prec), storage_tensor(b, prec)
+        acc = None
+        for k0 in range(0, p.k, SIM32_K_CHUNK):
+            k1 = min(p.k, k0 + SIM32_K_CHUNK)
+            kp = -(-(k1 - k0) // 8) * 8
+            sa = fa[k0:k1, :] if p.trans_a else fa[:, k0:k1]
+            sb = fb[:, k0:k1] if p.trans_b else fb[k0:k1, :]
+            ta = split_f32(sa, 0 if p.trans_a else 1, kp, _A_PATTERN)
+            tb = split_f32(sb, 1 if p.trans_b else 0, kp, _B_PATTERN)
+            if k1 < p.k:
+                part = alloc_matrix(p.m, p.n, torch.float32, dev)
+                enqueue(ta, tb, 6 * kp, False, nat.tensor_desc(part), acc, nat.F32)
+                keep.append(part)
+                acc = part
+            else:
+                enqueue(ta, tb, 6 * kp, True, main_desc, acc, out_code)
 
     # ---- fold pieces into the reference block layout
     aux: dict = {}

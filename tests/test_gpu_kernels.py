@@ -166,3 +166,43 @@ def test_tile_shape_invariance(cuda_ready):
         rs.append(cd.finalize_rms(k4.aux["sumsq"]).data)
     for r in rs[1:]:
         assert O.rel_error(r, rs[0]) < 1e-6
+
+
+def test_specialised_and_generic_epilogues_agree(cuda_ready):
+    """The flag-specialised kernels and the generic interpreter compute the same launch."""
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests"); sys.path.insert(0, ".")
+from conftest import load_golden
+import paper_2605_19269_b200 as cd
+g = load_golden("kernels_default_simbf16")
+P = cd.PrecisionMode.SIMBF16
+M = lambda k: cd.DenseMatrix.from_array(g[k], P)
+a, b, bt, z, cos, sin, pre, gin, pre2 = (M(x) for x in ("a","b","bt","z","cos","sin","pre","gin","preact2"))
+r = cd.Vector.from_array(g["r"], cd.PrecisionMode.SIM32); s = cd.Vector.from_array(g["s"], cd.PrecisionMode.SIM32)
+gamma = cd.Vector.from_array(g["gamma"], P)
+kw = dict(precision=P)
+outs = []
+k4 = cd.gemm_residual_partial_rms(a, b, z, gamma, **kw); outs += [k4.main.data, k4.aux["pre_norm"].data, k4.aux["sumsq"].data]
+k6 = cd.gemm_rms_swiglu(a, b, r, **kw); outs += [k6.main.data, k6.aux["preact"].data]
+outs.append(cd.gemm_rms_rope(a, b, r, cos, sin, **kw).main.data)
+k9 = cd.gemm_rmsnorm_backward(a, bt, pre, r, gamma, s, grad_in=gin, trans_b=True, **kw)
+outs += [k9.main.data, k9.aux["normed"].data, k9.aux["gamma_grad"].data]
+k10 = cd.gemm_swiglu_backward(a, bt, pre2, trans_b=True, **kw)
+outs += [k10.main.data, k10.aux["recompute"].data, k10.aux["rowdot"].data]
+np.savez(sys.argv[1], *outs)
+'''
+    res = {}
+    for mode in ("0", "1"):
+        out = f"/tmp/coda_epi_{mode}.npz"
+        env = dict(os.environ, CODA_FORCE_GENERIC=mode)
+        subprocess.run([sys.executable, "-c", code, out], check=True, env=env, cwd=str(__import__("conftest").ROOT))
+        with np.load(out) as z:
+            res[mode] = [z[k] for k in z.files]
+    for x, y in zip(res["0"], res["1"]):
+        assert x.shape == y.shape
+        assert O.rel_error(x, y) < 1e-5 if np.linalg.norm(y) else np.all(x == y)
