@@ -102,13 +102,17 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- workload
 
 
-def make_workload(cd, d, inter, m, rank, device, seed=0):
-    """Synthetic bf16 inputs and random-init weights (N(0, 0.02^2), gains 1 + 0.1 N)."""
+def make_workload(cd, d, inter, m, start, device, seed=0):
+    """Synthetic bf16 inputs and random-init weights (N(0, 0.02^2), gains 1 + 0.1 N).
+
+    Weights are identical on every rank (same seed); activations differ per
+    shard; RoPE tables start at the shard's first token position.
+    """
     import torch
 
     P = cd.PrecisionMode.SIMBF16
     g = torch.Generator(device=device).manual_seed(seed)
-    gr = torch.Generator(device=device).manual_seed(seed * 1000 + 17 + rank)
+    gr = torch.Generator(device=device).manual_seed(seed * 1000 + 17 + start)
 
     def w(*shape, scale=0.02, gen=g):
         t = cd.tensors.alloc_matrix(shape[0], shape[1], torch.bfloat16, device)
@@ -123,7 +127,7 @@ def make_workload(cd, d, inter, m, rank, device, seed=0):
                               gamma_qkv=gain(d), w_qkv=w(d, 3 * d))
     acts = {name: w(m, width, scale=1.0, gen=gr) for name, width in
             (("x", d), ("z", d), ("grad_qkv", 3 * d), ("grad_residual", d))}
-    cos, sin = cd.qkv_rope_tables(m, d, start=rank * m, precision=P)
+    cos, sin = cd.qkv_rope_tables(m, d, start=start, precision=P)
     return weights, acts, cos, sin
 
 
@@ -134,61 +138,43 @@ def run_step(cd, cfg, weights, acts, cos, sin, hook=None):
     return fwd, bwd
 
 
-class WgradAllReduce:
-    """Token-sharded DP: all-reduce(sum) of each f32 weight gradient on a side stream,
-    overlapped with the remaining backward launches; waited before the step ends."""
+class CpuOracle:
+    """The reference algorithm on the host cores: the fused-order SIMBF16 oracle
+    (oracle/coda_oracle.py, numpy/OpenBLAS using every core) on a token sample."""
 
-    def __init__(self, dist, device):
-        import torch
+    def __init__(self, d, inter, sample_tokens, seed=0):
+        import numpy as np
 
-        self.dist = dist
-        self.side = torch.cuda.Stream(device)
-        self.pending = []
+        from oracle import coda_oracle as O
 
-    def __call__(self, name, tensor):
-        import torch
+        self.O = O
+        rng = np.random.default_rng(seed)
+        self.mode = O.SIMBF16
+        self.w = O.random_layer(rng, d, 2 * inter, self.mode, scale=0.02)
+        self.m = sample_tokens
+        self.x, self.z = (O.q(rng.standard_normal((self.m, d)), self.mode) for _ in range(2))
+        self.cos, self.sin = O.qkv_rope_tables(self.m, d, self.mode)
+        self.gq = O.q(rng.standard_normal((self.m, 3 * d)), self.mode)
+        self.gres = O.q(rng.standard_normal((self.m, d)), self.mode)
 
-        main = torch.cuda.current_stream(tensor.device)
-        ev = torch.cuda.Event()
-        ev.record(main)
-        with torch.cuda.stream(self.side):
-            self.side.wait_event(ev)
-            self.dist.all_reduce(tensor)
-        tensor.record_stream(self.side)
-        self.pending.append(tensor)
-
-    def wait(self):
-        import torch
-
-        torch.cuda.current_stream().wait_stream(self.side)
-        self.pending.clear()
+    def step(self) -> float:
+        O = self.O
+        t0 = time.perf_counter()
+        f = O.layer_forward(self.x, self.z, self.w, self.cos, self.sin, self.mode)
+        O.layer_backward(self.gq, f, self.w, self.mode, grad_residual=self.gres)
+        return time.perf_counter() - t0
 
 
-def cpu_oracle_tokens_per_s(d, inter, sample_tokens, seconds_budget=20.0):
-    """Time the CPU oracle (fused-order SIMBF16 restatement of the reference) on a token sample."""
-    import numpy as np
-
-    from oracle import coda_oracle as O
-
-    rng = np.random.default_rng(0)
-    mode = O.SIMBF16
-    wts = O.random_layer(rng, d, 2 * inter, mode, scale=0.02)
-    m = sample_tokens
-    x, z = (O.q(rng.standard_normal((m, d)), mode) for _ in range(2))
-    cos, sin = O.qkv_rope_tables(m, d, mode)
-    gq = O.q(rng.standard_normal((m, 3 * d)), mode)
-    gres = O.q(rng.standard_normal((m, d)), mode)
+def cpu_oracle_tokens_per_s(d, inter, sample_tokens, seconds_budget=20.0, max_reps=5):
+    runner = CpuOracle(d, inter, sample_tokens)
     times = []
     t_start = time.perf_counter()
     while True:
-        t0 = time.perf_counter()
-        f = O.layer_forward(x, z, wts, cos, sin, mode)
-        O.layer_backward(gq, f, wts, mode, grad_residual=gres)
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_start > seconds_budget or len(times) >= 5:
+        times.append(runner.step())
+        if time.perf_counter() - t_start > seconds_budget or len(times) >= max_reps:
             break
     best = min(times)
-    return m / best, best, len(times)
+    return sample_tokens / best, best, len(times)
 
 
 def host_cores() -> int:
@@ -207,12 +193,10 @@ def reference_arm(args, rank, world):
     if rank != 0:
         return
     sample = args.cpu_sample
-    per_step = []
+    runner = CpuOracle(d, inter, sample)
     for _ in range(max(1, args.warmup)):
-        cpu_oracle_tokens_per_s(d, inter, sample, seconds_budget=0.0)
-    for _ in range(args.steps):
-        tps, secs, _ = cpu_oracle_tokens_per_s(d, inter, sample, seconds_budget=0.0)
-        per_step.append(secs)
+        runner.step()
+    per_step = [runner.step() for _ in range(args.steps)]
     t = statistics.median(per_step)
     value = sample / t
     cores = host_cores()
@@ -241,12 +225,15 @@ def coda_arm(args, rank, world, local_rank):
         import torch.distributed as dist  # noqa: F811
 
         dist.init_process_group("nccl", device_id=device)
+    from paper_2605_19269_b200 import parallel
+
     d, inter, tokens, label = CONFIGS[args.config]
-    m = tokens // world if args.scaling == "strong" else tokens
+    sh = parallel.shard(tokens, rank, world, args.scaling)
+    m = sh.rows
     P = cd.PrecisionMode.SIMBF16
     cfg = cd.PipelineConfig(hidden=d, ffn=2 * inter, precision=P)
-    weights, acts, cos, sin = make_workload(cd, d, inter, m, rank, device)
-    hook = WgradAllReduce(dist, device) if dist is not None else None
+    weights, acts, cos, sin = make_workload(cd, d, inter, m, sh.start, device)
+    hook = parallel.WgradAllReduce(dist, device) if dist is not None else None
 
     def step():
         out = run_step(cd, cfg, weights, acts, cos, sin, hook)
@@ -259,6 +246,14 @@ def coda_arm(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
+    if args.ncu:
+        # profiler pass: a few steps, nothing else (numbers printed under ncu are not bench values)
+        for _ in range(args.warmup + args.steps):
+            step()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.destroy_process_group()
+        return
     for _ in range(args.warmup):
         step()
     barrier()
@@ -281,31 +276,59 @@ def coda_arm(args, rank, world, local_rank):
     ms_step = ms / args.steps
     value = world * m / (ms_step / 1e3)
 
-    # ---- e2e through the public API from pinned host buffers
-    host = {k: v.tensor.cpu().pin_memory() for k, v in acts.items()}
-    dev_in = {k: torch.empty_like(v.tensor) for k, v in acts.items()}
-    h2d = sum(t.numel() * t.element_size() for t in host.values())
-    out_host = torch.empty((m, d), dtype=torch.bfloat16).pin_memory()
-    gam_host = torch.empty((2, d), dtype=torch.float32).pin_memory()
-    d2h = out_host.numel() * 2 + gam_host.numel() * 4
+    # ---- e2e through the public API from pinned host buffers.  Every step copies its
+    # inputs H2D and reads its results D2H inside the timed region; the copies run on
+    # their own streams (double-buffered inputs) so they overlap the previous/next step.
+    host = [{k: (v.tensor * (1.0 + 0.01 * j)).to(v.tensor.dtype).cpu().pin_memory() for k, v in acts.items()}
+            for j in range(2)]
+    dev_in = [{k: torch.empty_like(v.tensor) for k, v in acts.items()} for _ in range(2)]
+    h2d = sum(t.numel() * t.element_size() for t in host[0].values())
+    out_host = [torch.empty((m, d), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+    gam_host = [torch.empty((2, d), dtype=torch.float32).pin_memory() for _ in range(2)]
+    d2h = out_host[0].numel() * 2 + gam_host[0].numel() * 4
+    h2d_stream, d2h_stream = torch.cuda.Stream(device), torch.cuda.Stream(device)
 
-    def e2e_step():
-        for k in host:
-            dev_in[k].copy_(host[k], non_blocking=True)
-        a = {k: cd.DenseMatrix.from_tensor(dev_in[k], P) for k in dev_in}
-        _, bwd = run_step(cd, cfg, weights, a, cos, sin, hook)
-        if hook is not None:
-            hook.wait()
-        out_host.copy_(bwd.x.tensor, non_blocking=True)
-        gam_host[0].copy_(bwd.gamma_ffn.tensor, non_blocking=True)
-        gam_host[1].copy_(bwd.gamma_qkv.tensor, non_blocking=True)
+    def e2e_run(nsteps):
+        copied = [torch.cuda.Event() for _ in range(2)]
+        consumed = [torch.cuda.Event() for _ in range(2)]
+        done = [torch.cuda.Event() for _ in range(2)]
 
-    for _ in range(max(1, args.warmup // 2)):
-        e2e_step()
+        def issue_copy(s):
+            b = s % 2
+            with torch.cuda.stream(h2d_stream):
+                if s >= 2:
+                    h2d_stream.wait_event(consumed[b])
+                for k in host[b]:
+                    dev_in[b][k].copy_(host[b][k], non_blocking=True)
+                copied[b].record(h2d_stream)
+
+        h2d_stream.wait_stream(stream)
+        issue_copy(0)
+        for s in range(nsteps):
+            b = s % 2
+            if s + 1 < nsteps:
+                issue_copy(s + 1)
+            stream.wait_event(copied[b])
+            a = {k: cd.DenseMatrix.from_tensor(dev_in[b][k], P) for k in dev_in[b]}
+            _, bwd = run_step(cd, cfg, weights, a, cos, sin, hook)
+            if hook is not None:
+                hook.wait()
+            consumed[b].record(stream)
+            with torch.cuda.stream(d2h_stream):
+                d2h_stream.wait_event(consumed[b])
+                out_host[b].copy_(bwd.x.tensor, non_blocking=True)
+                gam_host[b][0].copy_(bwd.gamma_ffn.tensor, non_blocking=True)
+                gam_host[b][1].copy_(bwd.gamma_qkv.tensor, non_blocking=True)
+                done[b].record(d2h_stream)
+                for t in (bwd.x.tensor, bwd.gamma_ffn.tensor, bwd.gamma_qkv.tensor):
+                    t.record_stream(d2h_stream)
+        stream.wait_stream(d2h_stream)
+        stream.wait_stream(h2d_stream)
+
+    e2e_run(max(2, args.warmup // 2))
     barrier()
     e0.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
+    e2e_run(args.steps)
     e1.record(stream)
     barrier()
     ms_e2e = e0.elapsed_time(e1)
@@ -336,7 +359,7 @@ def coda_arm(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        tps, secs, reps = cpu_oracle_tokens_per_s(d, inter, args.cpu_sample)
+        tps, secs, reps = cpu_oracle_tokens_per_s(d, inter, args.cpu_sample, seconds_budget=20.0, max_reps=3)
         cpu = {"value": tps, "unit": "tokens/s", "cores": host_cores(), "kind": "port",
                "sample": f"{args.cpu_sample} tokens of the {args.config} block, fused-order SIMBF16 oracle, "
                          f"best of {reps} ({secs:.2f} s each)"}
@@ -376,6 +399,7 @@ def main():
     ap.add_argument("--scaling", choices=("strong", "weak"), default="weak")
     ap.add_argument("--cpu-sample", type=int, default=256)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ncu", action="store_true", help="profiling pass only (no timing / JSON line)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", 0))

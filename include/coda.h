@@ -161,7 +161,9 @@ int coda_cross_entropy_finalize(const float* target, const float* lse, int64_t m
 
 /* rope_backward_stat (kernels.py:560-617): counter-rotated gradient (storage
  * dtype) plus row-dot partials of grad*rotated over row_block_layout
- * (`block_start`, nb+1 device offsets: block b covers [start[b], start[b+1])). */
+ * (`block_start`, nb+1 device offsets: block b covers [start[b], start[b+1])).
+ * block_start == NULL selects the uniform 128-column layout (the default
+ * tile_n = reduction_tile_n = 128), served by a shared-memory-free kernel. */
 int coda_rope_backward_stat(const coda_tensor_t* grad, const coda_tensor_t* rotated,
                             const coda_tensor_t* cos, const coda_tensor_t* sin,
                             const int32_t* block_start, int64_t nb,

@@ -38,9 +38,10 @@ def acc_dtype(mode: str):
 def bf16_round(x) -> np.ndarray:
     """bf16 round-to-nearest-even on the f32 bit pattern (tensors.py:64-79)."""
     f = np.ascontiguousarray(x, dtype=np.float32)
-    u = f.view(np.uint32).astype(np.uint64)
-    lsb = (u >> 16) & 1
-    r = ((u + 0x7FFF + lsb) & 0xFFFF0000).astype(np.uint32).view(np.float32)
+    u = f.view(np.uint32)
+    lsb = (u >> np.uint32(16)) & np.uint32(1)
+    # uint32 wrap-around only happens for NaN payloads, which the mask restores
+    r = ((u + np.uint32(0x7FFF) + lsb) & np.uint32(0xFFFF0000)).view(np.float32)
     return np.where(np.isfinite(f), r, f)
 
 

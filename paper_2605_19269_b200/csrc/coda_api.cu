@@ -560,10 +560,26 @@ int coda_rope_backward_stat(const coda_tensor_t* grad, const coda_tensor_t* rota
                         (long long)grad->cols);
     }
     if (grad->cols % 2) return fail(CODA_E_DIMENSION, "rotary width must be even, got %lld", (long long)grad->cols);
-    const size_t smem = (size_t)grad->cols * 4;
-    if (smem > 200 * 1024) return fail(CODA_E_CONFIG, "rope_backward_stat: row too wide (%lld)", (long long)grad->cols);
     if ((rc = bind_device(grad->ptr))) return rc;
     cudaStream_t st = (cudaStream_t)stream;
+    if (block_start == nullptr) {
+        if (nb != (grad->cols + 127) / 128) return fail(CODA_E_DIMENSION, "rope_backward_stat: nb != ceil(n/128)");
+        const unsigned grid = (unsigned)(grad->rows < 148 * 8 ? grad->rows : 148 * 8);
+        if (dt == CODA_BF16) {
+            coda::rope_backward_stat128_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+                (const __nv_bfloat16*)grad->ptr, grad->ld, (const __nv_bfloat16*)rotated->ptr, rotated->ld,
+                (const __nv_bfloat16*)cos->ptr, cos->ld, (const __nv_bfloat16*)sin->ptr, sin->ld, grad->rows,
+                grad->cols, (__nv_bfloat16*)grad_z->ptr, grad_z->ld, rowdot, ld_rowdot);
+        } else {
+            coda::rope_backward_stat128_kernel<float><<<grid, 256, 0, st>>>(
+                (const float*)grad->ptr, grad->ld, (const float*)rotated->ptr, rotated->ld, (const float*)cos->ptr,
+                cos->ld, (const float*)sin->ptr, sin->ld, grad->rows, grad->cols, (float*)grad_z->ptr, grad_z->ld,
+                rowdot, ld_rowdot);
+        }
+        return cuda_check(cudaGetLastError(), "rope_backward_stat128");
+    }
+    const size_t smem = (size_t)grad->cols * 4;
+    if (smem > 200 * 1024) return fail(CODA_E_CONFIG, "rope_backward_stat: row too wide (%lld)", (long long)grad->cols);
     if (dt == CODA_BF16) {
         auto k = coda::rope_backward_stat_kernel<__nv_bfloat16>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

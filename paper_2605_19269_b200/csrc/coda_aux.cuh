@@ -154,6 +154,65 @@ rope_backward_stat_kernel(const TS* __restrict__ g, int64_t ldg, const TS* __res
     }
 }
 
+// Fast path of the boundary RoPE backward for the default reduction layout
+// (blocks of exactly 128 columns, the last one possibly ragged): no shared
+// memory, every thread owns one 16-byte vector per 2048-column sweep, and the
+// 128/V lanes covering one block reduce their partial dots with a shuffle
+// tree.  Several rows per CTA keep enough loads in flight for HBM.
+template <typename TS>
+__global__ void __launch_bounds__(256)
+rope_backward_stat128_kernel(const TS* __restrict__ g, int64_t ldg, const TS* __restrict__ rot, int64_t ldr,
+                             const TS* __restrict__ cs, int64_t ldc, const TS* __restrict__ sn, int64_t lds,
+                             int64_t m, int64_t n, TS* __restrict__ gz, int64_t ldz, float* __restrict__ rowdot,
+                             int64_t ldd) {
+    constexpr int V = Io<TS>::V;
+    constexpr int LPB = 128 / V;                       // lanes per 128-column block
+    const int lane = threadIdx.x & 31;
+    const int64_t sweep = (int64_t)blockDim.x * V;
+    for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
+        const TS* gr = g + i * ldg;
+        const TS* rr = rot + i * ldr;
+        const TS* cr = cs + i * ldc;
+        const TS* sr = sn + i * lds;
+        TS* zr = gz + i * ldz;
+        for (int64_t base = 0; base < n; base += sweep) {
+            const int64_t c0 = base + (int64_t)threadIdx.x * V;
+            const bool ok = c0 < n;
+            float gv[V], rv[V], cv[V], sv[V], zv[V];
+            float p = 0.0f;
+            if (ok) {
+                if (c0 + V <= n) {
+                    Io<TS>::load(gr + c0, gv);
+                    Io<TS>::load(rr + c0, rv);
+                    Io<TS>::load(cr + c0, cv);
+                    Io<TS>::load(sr + c0, sv);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        const bool in = c0 + e < n;
+                        gv[e] = in ? Io<TS>::load1(gr + c0 + e) : 0.f;
+                        rv[e] = in ? Io<TS>::load1(rr + c0 + e) : 0.f;
+                        cv[e] = in ? Io<TS>::load1(cr + c0 + e) : 0.f;
+                        sv[e] = in ? Io<TS>::load1(sr + c0 + e) : 0.f;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < V / 2; ++k) {
+                    const float g0 = gv[2 * k], g1 = gv[2 * k + 1];
+                    zv[2 * k] = g0 * cv[2 * k] + g1 * sv[2 * k];
+                    zv[2 * k + 1] = -g0 * sv[2 * k + 1] + g1 * cv[2 * k + 1];
+                }
+#pragma unroll
+                for (int e = 0; e < V; ++e) p += gv[e] * rv[e];
+                store_seg<TS, V>(zr, c0, n, zv);
+            }
+#pragma unroll
+            for (int off = LPB / 2; off >= 1; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+            if (ok && (lane % LPB) == 0) rowdot[i * ldd + c0 / 128] = p;
+        }
+    }
+}
+
 // SIM32 split: x = x0 + x1 + x2 with x0 = bf16(x), x1 = bf16(x - x0), x2 = bf16(x - x0 - x1)
 // (each difference is exact in f32).  dst holds 6 K-blocks of kp, block j = term pattern[j].
 struct SplitPattern { int t[6]; };

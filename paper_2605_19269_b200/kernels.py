@@ -319,8 +319,10 @@ def rope_backward_stat(grad: DenseMatrix, rotated: DenseMatrix, cos: DenseMatrix
     rowdot = torch.empty((m, nb), dtype=torch.float32, device=dev)
     descs = [nat.tensor_desc(t) for t in ts]
     gzd = nat.tensor_desc(gz)
-    nat.call("coda_rope_backward_stat", *[ctypes.byref(d) for d in descs], bst.data_ptr(), nb,
-             ctypes.byref(gzd), rowdot.data_ptr(), rowdot.stride(0), torch.cuda.current_stream(dev).cuda_stream)
+    uniform128 = all(int(w) == 128 for w in counts[:-1]) and int(counts[-1]) <= 128
+    nat.call("coda_rope_backward_stat", *[ctypes.byref(d) for d in descs], None if uniform128 else bst.data_ptr(),
+             nb, ctypes.byref(gzd), rowdot.data_ptr(), rowdot.stride(0), torch.cuda.current_stream(dev).cuda_stream,
+             tag="rope_backward_stat", flops=0.0)
     slot = PartialSlot(StoreKind.ROW_SUM, rowdot, counts, precision).freeze()
     w, pw = precision.storage_bytes, precision.partial_bytes
     rec = LaunchRecord(traffic.K_ROPE_BWD_STAT, 4 * m * n * w, m * n * w + m * nb * pw)

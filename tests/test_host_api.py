@@ -1,0 +1,226 @@
+"""CPU tests of the host side: program rules, lowering, layouts, the C-ABI library.
+
+No GPU needed.  The library is loaded and its exports checked, and the
+validation paths that return before any CUDA call are exercised; nothing
+here launches a kernel.
+"""
+
+import ctypes
+import re
+from fractions import Fraction
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2605_19269_b200 as cd
+from paper_2605_19269_b200 import _native as nat
+from paper_2605_19269_b200.engine import col_pieces, row_pieces
+from paper_2605_19269_b200.epilogue import split_at
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+# ---------------------------------------------------------------- program rules (epilogue.py:612-698)
+
+def test_partials_after_width_change_rejected():
+    with pytest.raises(cd.ProgramError):
+        cd.EpilogueProgram([cd.PairwiseSwiglu(), cd.PartialSumSq()])
+
+
+def test_duplicate_operand_and_store_names_rejected():
+    with pytest.raises(cd.ProgramError):
+        cd.EpilogueProgram([cd.RowScale("r"), cd.RowScale("r")])
+    with pytest.raises(cd.ProgramError):
+        cd.EpilogueProgram([cd.AuxTileStore("x"), cd.AuxTileStore("x")])
+    with pytest.raises(cd.ProgramError):
+        cd.EpilogueProgram([cd.ResidualAdd("t"), cd.AuxTileStore("t")])
+
+
+def test_width_algebra_and_scaled_width():
+    p = cd.EpilogueProgram([cd.RowScale("s"), cd.AuxTileStore("pre"), cd.PairwiseSwiglu()])
+    assert p.out_factor == Fraction(1, 2)
+    assert p.scaled_width(256) == 128
+    with pytest.raises(cd.PairingError):
+        p.scaled_width(7)
+    b = cd.EpilogueProgram([cd.PairwiseSwigluBackward("z")])
+    assert b.out_factor == 2
+    assert b.operands["z"].factor == 2
+    assert b.stores["rowdot"].factor == 2
+
+
+def test_pairing_check():
+    p = cd.EpilogueProgram([cd.PairwiseRope()])
+    p.check_pairing([(0, 4), (4, 4)])
+    with pytest.raises(cd.PairingError):
+        p.check_pairing([(0, 3), (3, 3)])
+
+
+def test_not_a_primitive():
+    with pytest.raises(cd.ProgramError):
+        cd.EpilogueProgram(["RowScale"])
+
+
+# ---------------------------------------------------------------- lowering to device op codes
+
+def test_lowering_of_the_reference_programs():
+    k4 = cd.EpilogueProgram([cd.ResidualAdd("residual"), cd.AuxTileStore("pre_norm"), cd.PartialSumSq("sumsq"),
+                             cd.RowVecMul("gamma")])
+    steps, onames, snames = k4.lower()
+    assert [s[0] for s in steps] == [nat.OP_RESIDUAL_ADD, nat.OP_AUX_TILE_STORE, nat.OP_PARTIAL_SUMSQ,
+                                     nat.OP_ROW_VEC_MUL]
+    assert onames == ["residual", "gamma"] and snames == ["pre_norm", "sumsq"]
+    assert all(s[1] == 2 for s in steps)          # factor 1 encoded x2
+    k6 = cd.EpilogueProgram([cd.RowScale("scale"), cd.AuxTileStore("preact"), cd.PairwiseSwiglu()])
+    assert [s[1] for s in k6.lower()[0]] == [2, 2, 2]
+    k10 = cd.EpilogueProgram([cd.PairwiseSwigluBackward("preact", "recompute", "rowdot")])
+    (op, w2, args), = k10.lower()[0]
+    assert op == nat.OP_SWIGLU_BWD and args[:3] == [0, 0, 1]
+    k9 = cd.EpilogueProgram([cd.RmsNormBackwardLocal("pre", "r", "g", "s", accumulate="gin")])
+    (op, _, args), = k9.lower()[0]
+    assert op == nat.OP_RMSNORM_BWD and args == [0, 1, 2, 3, 4, 0, 1]
+    assert cd.EpilogueProgram([cd.RmsNormBackwardLocal("pre", "r", "g", "s")]).lower()[0][0][2][4] == -1
+
+
+def test_unsupported_width_factor_rejected_at_lowering():
+    p = cd.EpilogueProgram([cd.PairwiseSwiglu(), cd.PairwiseSwiglu()])
+    with pytest.raises(cd.ConfigError):
+        p.lower()
+
+
+def test_at_most_two_row_partial_streams():
+    p = cd.EpilogueProgram([cd.PartialSumSq("a"), cd.PartialRowDot("x", "b"), cd.OnlineLse("c")])
+    with pytest.raises(cd.ConfigError):
+        p.lower()
+
+
+# ---------------------------------------------------------------- layouts and pieces
+
+def test_row_block_layout_reference_example():
+    # reference tests/test_epilogue.py:101-104
+    assert [b.width for b in cd.row_block_layout(10, 4, 3)] == [3, 1, 3, 1, 2]
+
+
+@pytest.mark.parametrize("n,tile_n,rtn,scale", [(264, 128, 128, 1), (50, 24, 10, 1), (600, 300, 7, 1),
+                                                (264, 128, 128, 2), (1000, 96, 40, 2)])
+def test_row_pieces_partition_blocks(n, tile_n, rtn, scale):
+    import torch
+
+    blocks = cd.epilogue.scaled_row_blocks(n, tile_n, rtn, scale)
+    starts, ptr = split_at([(b.start, b.stop) for b in blocks], 128 * scale)
+    assert starts[0] == 0 and starts[-1] == n * scale
+    assert np.all(np.diff(starts) > 0)
+    # every piece lies inside one GPU half tile and inside one block
+    for p in range(len(starts) - 1):
+        assert starts[p] // (128 * scale) == (starts[p + 1] - 1) // (128 * scale)
+    for bi, b in enumerate(blocks):
+        assert starts[ptr[bi]] == b.start and starts[ptr[bi + 1]] == b.stop
+    pmap, bptr, npc, nb, counts, aligned = row_pieces(n, tile_n, rtn, scale, torch.device("cpu"))
+    assert npc == len(starts) - 1 and nb == len(blocks)
+    assert list(counts) == [b.width for b in blocks]
+    assert aligned == bool(np.all(starts[:-1] % (32 * scale) == 0))
+    assert pmap.shape[0] == n * scale
+
+
+def test_default_layout_is_aligned_and_unsplit():
+    import torch
+
+    _, _, npc, nb, _, aligned = row_pieces(28672, 128, 128, 1, torch.device("cpu"))
+    assert npc == nb == 224 and aligned
+    _, _, npc, nb, _, aligned = row_pieces(14336, 128, 128, 2, torch.device("cpu"))
+    assert npc == nb and aligned
+    _, _, npc, nb, _, aligned = col_pieces(16384, 128, torch.device("cpu"))
+    assert npc == nb == 128 and aligned
+    _, _, npc, nb, _, aligned = col_pieces(100, 16, torch.device("cpu"))
+    assert nb == 7 and not aligned
+
+
+# ---------------------------------------------------------------- the C-ABI library
+
+def _header_symbols():
+    text = (ROOT / "include" / "coda.h").read_text()
+    return sorted(set(re.findall(r"\b(coda_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2605_19269_b200 import _build
+
+    _build.build()
+    lib = ctypes.CDLL(str(nat.LIB_PATH))
+    syms = _header_symbols()
+    assert len(syms) >= 14
+    for s in syms:
+        assert hasattr(lib, s), f"libcoda.so does not export {s}"
+    assert set(syms) == set(nat.EXPORTS)
+
+
+def test_library_is_sm100a_tcgen05():
+    import shutil
+    import subprocess
+
+    if shutil.which("cuobjdump") is None:
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run(["cuobjdump", "-sass", str(nat.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", str(nat.LIB_PATH)], capture_output=True,
+                                       text=True).stdout
+    for mnemonic in ("UTCHMMA", "UTMALDG", "UTMASTG", "LDTM"):
+        assert mnemonic in out, mnemonic
+
+
+def test_c_abi_validation_before_any_cuda_call():
+    lib = nat.load()
+    assert lib.coda_version().decode().startswith("coda sm_100a")
+    # null problem -> BindingError code, no CUDA involvement
+    rc = lib.coda_gemm_epilogue(None, None, None, None, 0, None, 0, None, 0, None, None, None)
+    assert rc == -2
+    with pytest.raises(cd.BindingError):
+        nat.check(rc)
+    prob = nat.Problem(0, 4, 4, 0, 0, nat.BF16, nat.BF16, 1, 0)
+    rc = lib.coda_gemm_epilogue(ctypes.byref(prob), None, None, None, 0, None, 0, None, 0, None, None, None)
+    assert rc == -1
+    with pytest.raises(cd.DimensionError):
+        nat.check(rc)
+    assert "positive" in lib.coda_last_error().decode()
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    with pytest.raises(nat.NativeUnavailable):
+        nat.load(tmp_path / "nope.so")
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(nat.NativeUnavailable):
+        cd.DenseMatrix.from_array(np.ones((2, 2)), cd.PrecisionMode.SIMBF16)
+
+
+def test_error_taxonomy_matches_reference_names():
+    for name in ("TileFuseError", "DimensionError", "BindingError", "ProgramError", "PairingError", "ConfigError",
+                 "LabelError", "TapeError", "DegenerateError", "MissingGatherError", "ProbeError", "ContainerError"):
+        assert issubclass(getattr(cd, name), cd.TileFuseError)
+    assert issubclass(cd.PairingError, cd.ProgramError)
+
+
+def test_public_names_cover_the_reference_hot_path_api():
+    names = """GemmProblem run_gemm run_gemm_trans KernelResult EpilogueProgram PartialSlot row_block_layout
+    RowVecMul RowScale ResidualAdd AuxTileStore PartialSumSq PartialRowDot PartialColSum OnlineLse TargetGather
+    PairwiseRope PairwiseSwiglu PairwiseSwigluBackward RmsNormBackwardLocal gemm_rope gemm_swiglu
+    gemm_partial_xent gemm_residual_partial_rms gemm_row_scale gemm_rms_swiglu gemm_rms_rope
+    gemm_rms_partial_xent gemm_rmsnorm_backward gemm_swiglu_backward rope_backward_stat finalize_rms
+    finalize_rowdot reduce_row_partials combine_lse cross_entropy_finalize pipeline_grrg_forward layer_forward
+    layer_backward lm_head_forward LayerWeights LayerTape LayerGrads PipelineConfig rope_tables qkv_rope_tables
+    interleave_gate_up split_gate_up ffn_width DenseMatrix Vector PrecisionMode TileShape quantize rel_error
+    stat_mode tile_coords""".split()
+    missing = [n for n in names if not hasattr(cd, n)]
+    assert not missing, missing
+
+
+def test_quantize_matches_oracle_rounding():
+    from oracle import coda_oracle as O
+
+    x = np.random.default_rng(0).standard_normal(10000) * 100
+    assert np.array_equal(cd.quantize(x, cd.PrecisionMode.SIMBF16), O.q(x, O.SIMBF16))
+    assert cd.ffn_width(4096) == 11008

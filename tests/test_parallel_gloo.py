@@ -1,0 +1,98 @@
+"""World-size-2 gloo test of the token-sharded data-parallel decomposition.
+
+Each rank runs the block on its row shard (RoPE tables offset by the shard's
+first position), all-reduces the weight/gain gradients with the same
+`WgradAllReduce` hook object the GPU path uses, and must reproduce the
+single-process full-batch gradients.  The per-rank compute here is the CPU
+oracle (the GPU box runs the same decomposition with CUDA kernels + NCCL).
+"""
+
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _problem():
+    from oracle import coda_oracle as O
+
+    m, d, ffn = 64, 32, 96
+    rng = np.random.default_rng(7)
+    mode = O.SIM32
+    w = O.random_layer(rng, d, ffn, mode)
+    x, z = (O.q(rng.standard_normal((m, d)), mode) for _ in range(2))
+    gq = O.q(rng.standard_normal((m, 3 * d)), mode)
+    gr = O.q(rng.standard_normal((m, d)), mode)
+    return m, d, w, x, z, gq, gr, mode
+
+
+def _worker(rank, world, port, out_dir, scaling):
+    sys.path.insert(0, str(ROOT))
+    import torch
+    import torch.distributed as dist
+
+    from oracle import coda_oracle as O
+    from paper_2605_19269_b200 import parallel
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m, d, w, x, z, gq, gr, mode = _problem()
+    tokens = m if scaling == "strong" else m // world
+    sh = parallel.shard(tokens, rank, world, scaling)
+    sl = slice(sh.start, sh.stop)
+    cos, sin = O.qkv_rope_tables(sh.rows, d, O.EXACT64, start=sh.start)
+    fwd = O.layer_ref_forward(x[sl], z[sl], w, cos, sin)
+    bwd = O.layer_ref_backward(gq[sl], gr[sl], fwd, x[sl], w, cos, sin)
+    hook = parallel.WgradAllReduce(dist)
+    for name in parallel.REDUCED:
+        t = torch.from_numpy(np.ascontiguousarray(bwd[name]))
+        hook(name, t)
+        bwd[name] = t.numpy()
+    hook.wait()
+    np.savez(Path(out_dir) / f"rank{rank}.npz", start=sh.start, stop=sh.stop, **bwd, qkv=fwd["qkv"])
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("scaling", ["strong", "weak"])
+def test_token_sharded_grads_match_full_batch(tmp_path, scaling):
+    import torch.multiprocessing as mp
+
+    from oracle import coda_oracle as O
+    from paper_2605_19269_b200 import parallel
+
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), scaling), nprocs=world, join=True,
+                       start_method="spawn")
+    m, d, w, x, z, gq, gr, mode = _problem()
+    cos, sin = O.qkv_rope_tables(m, d, O.EXACT64)
+    fwd = O.layer_ref_forward(x, z, w, cos, sin)
+    full = O.layer_ref_backward(gq, gr, fwd, x, w, cos, sin)
+    shards = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
+    assert [int(s["start"]) for s in shards] == [0, m // 2]
+    for name in parallel.REDUCED:
+        for s in shards:
+            assert O.rel_error(s[name], full[name]) < 1e-12, name
+    for name in parallel.ROW_LOCAL:
+        got = np.concatenate([s[name] for s in shards], axis=0)
+        assert O.rel_error(got, full[name]) < 1e-12, name
+    qkv = np.concatenate([s["qkv"] for s in shards], axis=0)
+    assert O.rel_error(qkv, fwd["qkv"]) < 1e-12
+
+
+def test_shard_bounds():
+    from paper_2605_19269_b200 import parallel
+
+    assert [(s.start, s.stop) for s in (parallel.shard(10, r, 3) for r in range(3))] == [(0, 4), (4, 7), (7, 10)]
+    assert parallel.shard(16384, 3, 8).rows == 2048
+    assert parallel.shard(8192, 2, 8, "weak").start == 16384
