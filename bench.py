@@ -53,8 +53,67 @@ def peaks() -> dict:
     return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "fallback": True}
 
 
+class NvmlClockSampler:
+    """NVML clocks / throttle reasons sampled every 20 ms during the timed region."""
+
+    # nvmlClocksEventReason bits
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index: int):
+        import pynvml
+
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        nv = self.nv
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                    reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    self.samples.append((sm, reasons))
+                except Exception:
+                    pass
+                self._stop.wait(0.02)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join(timeout=2)
+
+    def summary(self) -> dict:
+        nv = self.nv
+        try:
+            mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception:
+            mx = None
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["unsampled"], "samples": 0}
+        reasons = sorted({name for _, r in self.samples for name, bit in self.BITS.items() if r & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples), "sm_mhz_min": min(s for s, _ in self.samples)}
+
+
+def clock_sampler(index: int):
+    try:
+        return NvmlClockSampler(index)
+    except Exception:
+        return ClockSampler(index)
+
+
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (NVML fallback)."""
 
     FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
@@ -259,15 +318,33 @@ def coda_arm(args, rank, world, local_rank):
     barrier()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = _native.launch_count()
-    with ClockSampler(local_rank) as clocks:
+    graph = None
+    if args.graph:
+        # capture one whole step (19 launches) once; replaying it removes host launch overhead
+        graph = torch.cuda.CUDAGraph()
+        c0 = _native.launch_count()
+        with torch.cuda.graph(graph):
+            step()
+        per_step_launches = _native.launch_count() - c0
+        for _ in range(2):
+            graph.replay()
         barrier()
+    launches0 = _native.launch_count()
+    with clock_sampler(local_rank) as clocks:
+        barrier()
+        h0 = time.perf_counter()
         e0.record(stream)
         for _ in range(args.steps):
-            step()
+            if graph is not None:
+                graph.replay()
+            else:
+                step()
         e1.record(stream)
+        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
         barrier()
     launches = _native.launch_count() - launches0
+    if graph is not None:
+        launches = per_step_launches * args.steps   # replayed graph nodes (captured once)
     ms = e0.elapsed_time(e1)
     if dist is not None:
         t = torch.tensor([ms], device=device)
@@ -380,6 +457,8 @@ def coda_arm(args, rank, world, local_rank):
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
+            "host_enqueue_ms_per_step": host_ms,
+            "cuda_graph": bool(args.graph),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "launch_breakdown_ms": {k: round(v["avg_ms"], 4) for k, v in (prof or {}).items()},
@@ -400,6 +479,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=256)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="profiling pass only (no timing / JSON line)")
+    ap.add_argument("--graph", action="store_true", help="replay the step as one captured CUDA graph")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", 0))

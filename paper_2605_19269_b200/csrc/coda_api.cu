@@ -211,21 +211,44 @@ using coda::F_SWIGLU_BWD;
     X(F_RMSBWD | F_RMSBWD_ACC | F_STORE_MAIN)                         \
     X(F_SWIGLU_BWD | F_STORE_MAIN)
 
-template <int FL>
+template <int FL, int CG>
 int launch_fast_fl(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mm, const CUtensorMap& mx,
                    const coda::FastParams& P, cudaStream_t st) {
     static bool configured = false;
-    const size_t smem = coda::fast_smem_bytes();
-    auto kern = coda::coda_gemm_fast<__nv_bfloat16, FL>;
+    const size_t smem = coda::fast_smem_bytes<CG>();
+    auto kern = coda::coda_gemm_fast<__nv_bfloat16, FL, CG>;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(fast smem)");
+        if (CG > 1) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+            if (e != cudaSuccess) cudaGetLastError();
+        }
         configured = true;
     }
-    const int nsm = num_sms();
-    const int grid = P.mp.ntiles < nsm ? P.mp.ntiles : nsm;
-    kern<<<grid, coda::FAST_THREADS, smem, st>>>(ma, mb, mm, mx, P);
-    return cuda_check(cudaGetLastError(), "coda_gemm_fast launch");
+    const int units = num_sms() / CG;
+    const int grid = (P.mp.ntiles < units ? P.mp.ntiles : units) * CG;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(coda::FAST_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cuda_check(cudaLaunchKernelEx(&cfg, kern, ma, mb, mm, mx, P), "coda_gemm_fast launch");
+}
+
+int fast_cg() {
+    static const int cg = [] {
+        const char* e = getenv("CODA_CG");
+        return (e && e[0] == '1') ? 1 : 2;
+    }();
+    return cg;
 }
 
 bool fast_supported(int fl) {
@@ -235,12 +258,28 @@ bool fast_supported(int fl) {
     return false;
 }
 
-int launch_fast(int fl, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mm, const CUtensorMap& mx,
-                const coda::FastParams& P, cudaStream_t st) {
-#define CODA_FAST_CASE(F) if (fl == (F)) return launch_fast_fl<(F)>(ma, mb, mm, mx, P, st);
+int launch_fast(int fl, int cg, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mm,
+                const CUtensorMap& mx, const coda::FastParams& P, cudaStream_t st) {
+#define CODA_FAST_CASE(F)                                                         \
+    if (fl == (F))                                                                \
+        return cg == 2 ? launch_fast_fl<(F), 2>(ma, mb, mm, mx, P, st)            \
+                       : launch_fast_fl<(F), 1>(ma, mb, mm, mx, P, st);
     CODA_FAST_SETS(CODA_FAST_CASE)
 #undef CODA_FAST_CASE
     return fail(CODA_E_CONFIG, "no specialised kernel for flags 0x%x", fl);
+}
+
+// Raster group: m-tiles swept together across all n-tiles, sized so the group's
+// A panels (tile_m x K bf16 each) stay around 32 MiB of L2.
+int raster_group(int ntm, int tile_m, int64_t k) {
+    static const int forced = [] {
+        const char* e = getenv("CODA_RASTER_GROUP");
+        return e ? atoi(e) : 0;
+    }();
+    int g = forced > 0 ? forced : (int)((32ll << 20) / ((int64_t)tile_m * k * 2));
+    if (g < 1) g = 1;
+    if (g > ntm) g = ntm;
+    return g;
 }
 
 // Map a validated program onto the flag set of a specialised kernel (or -1).
@@ -437,9 +476,13 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
 
     const int fl = match_fast(pr, steps, nsteps, stores);
     if (fl >= 0) {
+        const int cg = fast_cg();
         coda::FastParams F;
         memset(&F, 0, sizeof(F));
-        F.mp = coda::MainParams{P.M, P.N, P.K, P.ntm, P.ntn, P.nk, P.ntiles, P.a_mn, P.b_mn};
+        const int tile_m = coda::BM * cg;
+        const int ntm = (int)((M + tile_m - 1) / tile_m);
+        F.mp = coda::MainParams{P.M, P.N, P.K, ntm, P.ntn, P.nk, ntm * P.ntn, P.a_mn, P.b_mn,
+                                raster_group(ntm, tile_m, K)};
         F.acc_in = P.acc_in;
         F.ld_acc = P.ld_acc;
         F.rope_sign = 1.0f;
@@ -494,7 +537,11 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
                           64);
             if (rc) return rc;
         }
-        return launch_fast(fl, ma, mb, mm, mx, F, st);
+        if (cg == 2 && pr->trans_b) {   // K-major B box covers this CTA's 128-column half
+            rc = make_map(&mb, b->ptr, (uint64_t)K, (uint64_t)N, (uint64_t)b->ld * 2, coda::BK, coda::BN / 2);
+            if (rc) return rc;
+        }
+        return launch_fast(fl, cg, ma, mb, mm, mx, F, st);
     }
     if (sdt == CODA_BF16) return launch_gemm<__nv_bfloat16>(ma, mb, P, st);
     return launch_gemm<float>(ma, mb, P, st);

@@ -79,8 +79,10 @@ struct FastParams {
     const int32_t* colpart_map;
 };
 
+template <int CG>
 constexpr size_t fast_smem_bytes() {
-    return (size_t)STAGES * STAGE_BYTES + (size_t)FAST_EPI_WARPS * STG_BYTES + COLRED_BYTES + (2 * STAGES + 4) * 8 + 16;
+    return (size_t)Geom<CG>::RING + (size_t)FAST_EPI_WARPS * STG_BYTES + COLRED_BYTES +
+           (2 * Geom<CG>::NSTAGE + 4) * 8 + 16;
 }
 
 // -------------------------------------------------------------- row-segment loads
@@ -207,35 +209,39 @@ __device__ __forceinline__ float warp_colsum32(float (&x)[32], int lane) {
 }
 
 // -------------------------------------------------------------- kernel
-template <typename TS, int FL>
+template <typename TS, int FL, int CG>
 __global__ void __launch_bounds__(FAST_THREADS, 1)
 coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                const __grid_constant__ CUtensorMap tma_main, const __grid_constant__ CUtensorMap tma_aux,
                const __grid_constant__ FastParams P) {
+    using G = Geom<CG>;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sA = smem;
-    uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
-    uint8_t* stg = sB + STAGES * B_STAGE_BYTES;
+    uint8_t* sB = smem + G::NSTAGE * G::A_BYTES;
+    uint8_t* stg = smem + G::RING;
     float* colred = reinterpret_cast<float*>(stg + FAST_EPI_WARPS * STG_BYTES);
     uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(colred) + COLRED_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
+    uint64_t* empty = full + G::NSTAGE;
+    uint64_t* tfull = empty + G::NSTAGE;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const MainParams& mp = P.mp;
+    const int rank = CG == 1 ? 0 : (int)cluster_ctarank();
+    const int unit = CG == 1 ? (int)blockIdx.x : (int)cluster_id_x();
+    const int nunits = CG == 1 ? (int)gridDim.x : (int)nclusters_x();
 
     if (threadIdx.x == 0) {
         if (smem_u32(smem) & 1023u) __trap();   // swizzled TMA buffers need 1 KiB alignment
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < G::NSTAGE; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 32 * FAST_EPI_WARPS);
+            mbar_init(&tempty[s], FAST_EPI_WARPS * CG);   // one arrival per epilogue warp of the pair
         }
         fence_mbar_init();
         tma_prefetch_desc(&tma_a);
@@ -243,16 +249,20 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         if (FL & F_STORE_MAIN) tma_prefetch_desc(&tma_main);
         if (FL & (F_AUX | F_SWIGLU_BWD | F_RMSBWD)) tma_prefetch_desc(&tma_aux);
     }
-    if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+    if (warp == 1) {
+        if constexpr (CG == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+        else tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+    }
     tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();   // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) producer_loop(mp, &tma_a, &tma_b, sA, sB, full, empty);
+        if (lane == 0) producer_loop<CG>(mp, &tma_a, &tma_b, sA, sB, full, empty, rank, unit, nunits);
     } else if (warp == 1) {
-        if (lane == 0) mma_loop(mp, tmem_base, sA, sB, full, empty, tfull, tempty);
+        if (lane == 0 && rank == 0) mma_loop<CG>(mp, tmem_base, sA, sB, full, empty, tfull, tempty, unit, nunits);
     } else {
         const int ew = warp - 2;            // 0..7
         const int q = warp & 3;             // TMEM lane quadrant
@@ -263,10 +273,10 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         int cbuf = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < mp.ntiles; t += gridDim.x) {
+        for (int t = unit; t < mp.ntiles; t += nunits) {
             int tm, tn;
             tile_coord(mp, t, tm, tn);
-            const int m0 = tm * BM;
+            const int m0 = tm * G::TILE_M + rank * BM;
             const int n0 = tn * BN;
             const int64_t row = (int64_t)m0 + lrow;
             const bool row_ok = row < M;
@@ -279,7 +289,8 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             float pacc = 0.0f;
             int ppid = -1;
 
-            mbar_wait(&tfull[acc], acc_phase);
+            if constexpr (CG == 1) mbar_wait(&tfull[acc], acc_phase);
+            else mbar_wait_cluster(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + h * 128);
 
@@ -288,8 +299,13 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 float v[32];
                 tmem_ld32(tbase + c * 32, v);
                 if (c == 3) {
+                    // this warp's share of the accumulator is in registers: release it
                     tc_fence_before();
-                    mbar_arrive(&tempty[acc]);
+                    __syncwarp();
+                    if (lane == 0) {
+                        if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
+                        else mbar_arrive_leader(&tempty[acc]);
+                    }
                 }
                 const int gcol0 = n0 + h * 128 + c * 32;
                 if (gcol0 >= N) continue;   // uniform for the 4 warps of this half
@@ -441,9 +457,11 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     __syncwarp();
     tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();   // both CTAs done with the paired TMEM
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<TMEM_COLS>(tmem_base);
+        if constexpr (CG == 1) tmem_dealloc<TMEM_COLS>(tmem_base);
+        else tmem_dealloc_pair<TMEM_COLS>(tmem_base);
     }
 }
 

@@ -321,13 +321,13 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const MainParams mp{P.M, P.N, P.K, P.ntm, P.ntn, P.nk, P.ntiles, P.a_mn, P.b_mn};
+    const MainParams mp{P.M, P.N, P.K, P.ntm, P.ntn, P.nk, P.ntiles, P.a_mn, P.b_mn, 16};
     auto tile_mn = [&](int t, int& tm, int& tn) { tile_coord(mp, t, tm, tn); };
 
     if (warp == 0) {
-        if (lane == 0) producer_loop(mp, &tma_a, &tma_b, sA, sB, full, empty);
+        if (lane == 0) producer_loop<1>(mp, &tma_a, &tma_b, sA, sB, full, empty, 0, blockIdx.x, gridDim.x);
     } else if (warp == 1) {
-        if (lane == 0) mma_loop(mp, tmem_base, sA, sB, full, empty, tfull, tempty);
+        if (lane == 0) mma_loop<1>(mp, tmem_base, sA, sB, full, empty, tfull, tempty, blockIdx.x, gridDim.x);
     } else {
         // ------------------------------------------------ epilogue
         const int q = warp & 3;                 // TMEM lane quadrant this warp may read

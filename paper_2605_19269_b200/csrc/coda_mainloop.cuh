@@ -1,10 +1,17 @@
 // coda_mainloop.cuh — the fixed GEMM mainloop shared by every CODA kernel.
 //
-// Persistent tile loop over 128 x 256 output tiles (raster groups of 16
-// m-tiles for L2 reuse of the B panel), a 4-stage TMA -> smem ring of 64-wide
-// k-blocks in SWIZZLE_128B layout, and a single-thread tcgen05.mma issuer
-// accumulating in TMEM with two accumulator buffers so the epilogue of tile i
-// overlaps the mainloop of tile i+1.
+// Persistent tile loop over output tiles (raster groups of m-tiles for L2
+// reuse), a multi-stage TMA -> smem ring of 64-wide k-blocks in SWIZZLE_128B
+// layout, and a single-thread tcgen05.mma issuer accumulating in TMEM with two
+// accumulator buffers so the epilogue of tile i overlaps the mainloop of i+1.
+//
+// CG = 1: one CTA computes a 128 x 256 tile (tcgen05.mma.cta_group::1, M=128).
+// CG = 2: a cluster of two CTAs computes a 256 x 256 tile with
+//   tcgen05.mma.cta_group::2 (M=256) issued by the leader (rank 0).  Each CTA
+//   loads its own 128 rows of A and one 128-column half of B; the 2-SM TMA
+//   loads count their bytes on the leader's barrier; commits are multicast to
+//   both CTAs; each CTA's TMEM holds its 128 rows x 256 columns.  Halves the
+//   per-SM shared-memory and L2 traffic of the B operand.
 #pragma once
 #include <cstdint>
 #include <cuda.h>
@@ -12,72 +19,95 @@
 
 namespace coda {
 
-constexpr int BM = 128;
-constexpr int BN = 256;
+constexpr int BM = 128;                      // accumulator rows per CTA (TMEM lanes)
+constexpr int BN = 256;                      // accumulator columns per tile
 constexpr int BK = 64;                       // one 128-byte swizzle atom of bf16 along K
-constexpr int STAGES = 4;
+constexpr int STAGES = 4;                    // CG = 1 ring depth (48 KiB stages)
 constexpr int A_STAGE_BYTES = BM * BK * 2;   // 16 KiB
 constexpr int B_STAGE_BYTES = BN * BK * 2;   // 32 KiB
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int TMEM_COLS = 512;               // 2 accumulator buffers x 256 columns
-constexpr int RASTER_GROUP = 16;             // m-tiles per raster group (L2 reuse)
+
+template <int CG>
+struct Geom {
+    static constexpr int TILE_M = BM * CG;                 // rows per (pair) tile
+    static constexpr int B_COLS = BN / CG;                 // B columns loaded per CTA
+    static constexpr int A_BYTES = BM * BK * 2;
+    static constexpr int B_BYTES = B_COLS * BK * 2;
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int NSTAGE = CG == 1 ? 4 : 6;         // 192 KiB of operand ring either way
+    static constexpr int RING = NSTAGE * STAGE;
+};
 
 struct MainParams {
     int M, N, K;
-    int ntm, ntn, nk, ntiles;
-    int a_mn, b_mn;      // operand majorness: 1 = MN-major (transposed storage)
+    int ntm, ntn, nk, ntiles;   // ntm counts (pair) tiles of Geom<CG>::TILE_M rows
+    int a_mn, b_mn;             // operand majorness: 1 = MN-major (transposed storage)
+    int group;                  // raster group: m-tiles swept together across all n-tiles
 };
 
 __device__ __forceinline__ void tile_coord(const MainParams& mp, int t, int& tm, int& tn) {
-    const int per_group = RASTER_GROUP * mp.ntn;
+    const int per_group = mp.group * mp.ntn;
     const int g = t / per_group;
-    const int first = g * RASTER_GROUP;
-    const int gs = min(mp.ntm - first, RASTER_GROUP);
+    const int first = g * mp.group;
+    const int gs = min(mp.ntm - first, mp.group);
     const int r = t - g * per_group;
     tm = first + r % gs;
     tn = r / gs;
 }
 
-// TMA producer (one thread): fills the smem ring for every tile this CTA owns.
+// TMA producer (one thread per CTA): fills this CTA's smem ring for every tile it owns.
+template <int CG>
 __device__ __forceinline__ void producer_loop(const MainParams& mp, const CUtensorMap* tma_a,
                                               const CUtensorMap* tma_b, uint8_t* sA, uint8_t* sB,
-                                              uint64_t* full, uint64_t* empty) {
+                                              uint64_t* full, uint64_t* empty, int rank, int unit, int nunits) {
+    using G = Geom<CG>;
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < mp.ntiles; t += gridDim.x) {
+    for (int t = unit; t < mp.ntiles; t += nunits) {
         int tm, tn;
         tile_coord(mp, t, tm, tn);
-        const int m0 = tm * BM, n0 = tn * BN;
+        const int m0 = tm * G::TILE_M + rank * BM;
+        const int nb0 = tn * BN + rank * G::B_COLS;
         for (int kb = 0; kb < mp.nk; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-            const uint32_t sa = smem_u32(sA + stage * A_STAGE_BYTES);
-            const uint32_t sb = smem_u32(sB + stage * B_STAGE_BYTES);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], G::STAGE * CG);
+            const uint32_t sa = smem_u32(sA + stage * G::A_BYTES);
+            const uint32_t sb = smem_u32(sB + stage * G::B_BYTES);
             const int k0 = kb * BK;
+            auto load = [&](uint32_t dst, const CUtensorMap* map, int c0, int c1) {
+                if constexpr (CG == 1) tma_load_2d(dst, map, c0, c1, &full[stage]);
+                else tma_load_2d_pair(dst, map, c0, c1, &full[stage]);
+            };
             if (!mp.a_mn) {
-                tma_load_2d(sa, tma_a, k0, m0, &full[stage]);
+                load(sa, tma_a, k0, m0);
             } else {
 #pragma unroll
-                for (int b = 0; b < BM / 64; ++b) tma_load_2d(sa + b * (BK * 128), tma_a, m0 + 64 * b, k0, &full[stage]);
+                for (int b = 0; b < BM / 64; ++b) load(sa + b * (BK * 128), tma_a, m0 + 64 * b, k0);
             }
             if (!mp.b_mn) {
-                tma_load_2d(sb, tma_b, k0, n0, &full[stage]);
+                load(sb, tma_b, k0, nb0);
             } else {
 #pragma unroll
-                for (int b = 0; b < BN / 64; ++b) tma_load_2d(sb + b * (BK * 128), tma_b, n0 + 64 * b, k0, &full[stage]);
+                for (int b = 0; b < G::B_COLS / 64; ++b) load(sb + b * (BK * 128), tma_b, nb0 + 64 * b, k0);
             }
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            if (++stage == G::NSTAGE) { stage = 0; phase ^= 1; }
         }
     }
 }
 
-// MMA issuer (one thread): 4 x tcgen05.mma (K=16 each) per k-block into the
-// current TMEM accumulator; commits free smem stages and publish finished tiles.
+// MMA issuer (one thread; for CG = 2 only in the leader CTA): 4 x tcgen05.mma
+// (K = 16 each) per k-block into the current TMEM accumulator; commits free smem
+// stages and publish finished accumulators.
+template <int CG>
 __device__ __forceinline__ void mma_loop(const MainParams& mp, uint32_t tmem_base, uint8_t* sA, uint8_t* sB,
-                                         uint64_t* full, uint64_t* empty, uint64_t* tfull, uint64_t* tempty) {
+                                         uint64_t* full, uint64_t* empty, uint64_t* tfull, uint64_t* tempty,
+                                         int unit, int nunits) {
+    using G = Geom<CG>;
     // kind::f16 instruction descriptor: D f32, A/B bf16, majorness, N>>3, M>>4.
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)mp.a_mn << 15) |
-                           ((uint32_t)mp.b_mn << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+                           ((uint32_t)mp.b_mn << 16) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(G::TILE_M >> 4) << 24);
     // K-major: LBO unused (16), SBO = 8 rows * 128 B; advance 32 B per UMMA_K = 16.
     // MN-major: LBO = next 64-wide MN atom column (BK * 128 B), SBO = 8 K-rows * 128 B;
     //           advance 2 x 1024 B per UMMA_K = 16.
@@ -87,25 +117,29 @@ __device__ __forceinline__ void mma_loop(const MainParams& mp, uint32_t tmem_bas
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < mp.ntiles; t += gridDim.x) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+    for (int t = unit; t < mp.ntiles; t += nunits) {
+        if constexpr (CG == 1) mbar_wait(&tempty[acc], acc_phase ^ 1);
+        else mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
         for (int kb = 0; kb < mp.nk; ++kb) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            const uint32_t sa = smem_u32(sA + stage * A_STAGE_BYTES);
-            const uint32_t sb = smem_u32(sB + stage * B_STAGE_BYTES);
+            const uint32_t sa = smem_u32(sA + stage * G::A_BYTES);
+            const uint32_t sb = smem_u32(sB + stage * G::B_BYTES);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
                 const uint64_t ad = umma_desc_sw128(sa + k * a_step, a_lbo, 1024);
                 const uint64_t bd = umma_desc_sw128(sb + k * b_step, b_lbo, 1024);
-                umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                if constexpr (CG == 1) umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                else umma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
             }
-            umma_commit(&empty[stage]);
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            if constexpr (CG == 1) umma_commit(&empty[stage]);
+            else umma_commit_pair(&empty[stage]);
+            if (++stage == G::NSTAGE) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull[acc]);
+        if constexpr (CG == 1) umma_commit(&tfull[acc]);
+        else umma_commit_pair(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
     }

@@ -197,12 +197,14 @@ outs += [k10.main.data, k10.aux["recompute"].data, k10.aux["rowdot"].data]
 np.savez(sys.argv[1], *outs)
 '''
     res = {}
-    for mode in ("0", "1"):
-        out = f"/tmp/coda_epi_{mode}.npz"
-        env = dict(os.environ, CODA_FORCE_GENERIC=mode)
+    variants = {"fast-2cta": ("0", "2"), "fast-1cta": ("0", "1"), "generic": ("1", "2")}
+    for name, (generic, cg) in variants.items():
+        out = f"/tmp/coda_epi_{name}.npz"
+        env = dict(os.environ, CODA_FORCE_GENERIC=generic, CODA_CG=cg)
         subprocess.run([sys.executable, "-c", code, out], check=True, env=env, cwd=str(__import__("conftest").ROOT))
         with np.load(out) as z:
-            res[mode] = [z[k] for k in z.files]
-    for x, y in zip(res["0"], res["1"]):
-        assert x.shape == y.shape
-        assert O.rel_error(x, y) < 1e-5 if np.linalg.norm(y) else np.all(x == y)
+            res[name] = [z[k] for k in z.files]
+    for other in ("fast-1cta", "fast-2cta"):
+        for x, y in zip(res[other], res["generic"]):
+            assert x.shape == y.shape
+            assert O.rel_error(x, y) < 1e-5 if np.linalg.norm(y) else np.all(x == y)
