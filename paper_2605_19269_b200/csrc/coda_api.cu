@@ -269,14 +269,17 @@ int launch_fast(int fl, int cg, const CUtensorMap& ma, const CUtensorMap& mb, co
     return fail(CODA_E_CONFIG, "no specialised kernel for flags 0x%x", fl);
 }
 
-// Raster group: m-tiles swept together across all n-tiles, sized so the group's
-// A panels (tile_m x K bf16 each) stay around 32 MiB of L2.
+// Raster group: m-tiles swept together across all n-tiles.  8 (pair) m-tiles was
+// measured best on the C4 block (sweep 4/8/16/32/64, profiles/r01_raster_sweep.md);
+// CODA_RASTER_GROUP overrides it for experiments.
 int raster_group(int ntm, int tile_m, int64_t k) {
+    (void)tile_m;
+    (void)k;
     static const int forced = [] {
         const char* e = getenv("CODA_RASTER_GROUP");
         return e ? atoi(e) : 0;
     }();
-    int g = forced > 0 ? forced : (int)((32ll << 20) / ((int64_t)tile_m * k * 2));
+    int g = forced > 0 ? forced : 8;
     if (g < 1) g = 1;
     if (g > ntm) g = ntm;
     return g;
