@@ -33,11 +33,13 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
-    # name: (hidden d, LLaMA intermediate I, tokens per job, label)
+    # name: (hidden d, LLaMA intermediate I, tokens per GPU (weak) / per job (strong), label)
     "c1": (256, 1024, 128, "tiny LLaMA-style block fp32 (d=256, ffn=1024, 128 tokens)"),
     "c3": (2048, 8192, 8192, "LLaMA-3-1B block shapes (d=2048, ffn=8192, 8192 tokens) bf16 fwd+bwd"),
     "c4": (4096, 14336, 16384, "LLaMA-3-8B block shapes (d=4096, ffn=14336, 16384 tokens) bf16 fwd+bwd"),
+    "c5": (4096, 14336, 8192, "LLaMA-3-8B 4-block stack bf16 fwd+bwd, 8192 tokens/GPU/block (65536 over 8 GPUs)"),
 }
+BLOCKS = {"c5": 4}
 
 
 def flops_per_token(d: int, inter: int) -> float:
@@ -161,7 +163,7 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- workload
 
 
-def make_workload(cd, d, inter, m, start, device, seed=0):
+def make_workload(cd, d, inter, m, start, device, seed=0, blocks=1):
     """Synthetic bf16 inputs and random-init weights (N(0, 0.02^2), gains 1 + 0.1 N).
 
     Weights are identical on every rank (same seed); activations differ per
@@ -182,8 +184,12 @@ def make_workload(cd, d, inter, m, start, device, seed=0):
         return cd.Vector.from_tensor(1.0 + 0.1 * torch.randn(n, generator=g, device=device), P)
 
     f = 2 * inter
-    weights = cd.LayerWeights(w_out=w(d, d), gamma_ffn=gain(d), w_gate_up=w(d, f), w_down=w(inter, d),
-                              gamma_qkv=gain(d), w_qkv=w(d, 3 * d))
+
+    def block():
+        return cd.LayerWeights(w_out=w(d, d), gamma_ffn=gain(d), w_gate_up=w(d, f), w_down=w(inter, d),
+                               gamma_qkv=gain(d), w_qkv=w(d, 3 * d))
+
+    weights = block() if blocks == 1 else [block() for _ in range(blocks)]
     acts = {name: w(m, width, scale=1.0, gen=gr) for name, width in
             (("x", d), ("z", d), ("grad_qkv", 3 * d), ("grad_residual", d))}
     cos, sin = cd.qkv_rope_tables(m, d, start=start, precision=P)
@@ -191,6 +197,14 @@ def make_workload(cd, d, inter, m, start, device, seed=0):
 
 
 def run_step(cd, cfg, weights, acts, cos, sin, hook=None):
+    """One fwd+bwd step: a single block, or a stack when `weights` is a list of blocks."""
+    if isinstance(weights, (list, tuple)):
+        from paper_2605_19269_b200 import stack
+
+        fwd = stack.stack_forward(acts["x"], acts["z"], weights, cos, sin, config=cfg)
+        grads = stack.stack_backward(acts["grad_qkv"], acts["grad_residual"], fwd, weights, config=cfg,
+                                     wgrad_hook=hook)
+        return fwd, grads[0]
     fwd = cd.layer_forward(acts["x"], acts["z"], weights, cos, sin, config=cfg)
     bwd = cd.layer_backward(acts["grad_qkv"], fwd.tape, weights, grad_residual=acts["grad_residual"], config=cfg,
                             wgrad_hook=hook)
@@ -291,7 +305,8 @@ def coda_arm(args, rank, world, local_rank):
     m = sh.rows
     P = cd.PrecisionMode.SIMBF16
     cfg = cd.PipelineConfig(hidden=d, ffn=2 * inter, precision=P)
-    weights, acts, cos, sin = make_workload(cd, d, inter, m, sh.start, device)
+    nblocks = BLOCKS.get(args.config, 1)
+    weights, acts, cos, sin = make_workload(cd, d, inter, m, sh.start, device, blocks=nblocks)
     hook = parallel.WgradAllReduce(dist, device) if dist is not None else None
 
     def step():
@@ -431,7 +446,7 @@ def coda_arm(args, rank, world, local_rank):
                     "frac": achieved / peak, "traffic": traffic, "kernel": top["name"],
                     "peak_kind": "measured sustained bf16 (MEASURED_PEAKS.json)",
                     "share_of_step": top["total_ms"] / sum(r["total_ms"] for r in prof.values())}
-    total_flops = flops_per_token(d, inter) * m
+    total_flops = flops_per_token(d, inter) * m * nblocks
     block_tflops = total_flops / (ms_step / 1e3) / 1e12
 
     cpu = None
@@ -447,7 +462,8 @@ def coda_arm(args, rank, world, local_rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if args.scaling == "strong" and world > 1 else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, N(0,1) activations)",
-            "config": {"workload": label, "tokens_per_gpu": m, "global_tokens": world * m, "hidden": d,
+            "config": {"workload": label, "blocks": nblocks, "tokens_per_gpu": m, "global_tokens": world * m,
+                       "hidden": d,
                        "intermediate": inter, "ffn_interleaved": 2 * inter, "qkv": 3 * d,
                        "parallelism": f"token-sharded dp{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (>=100 MB activations per launch)"},

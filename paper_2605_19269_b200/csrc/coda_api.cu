@@ -209,7 +209,9 @@ using coda::F_SWIGLU_BWD;
     X(F_ROWSCALE | F_ROPE | F_STORE_MAIN)                             \
     X(F_RMSBWD | F_STORE_MAIN)                                        \
     X(F_RMSBWD | F_RMSBWD_ACC | F_STORE_MAIN)                         \
-    X(F_SWIGLU_BWD | F_STORE_MAIN)
+    X(F_SWIGLU_BWD | F_STORE_MAIN)                                    \
+    X(F_SUMSQ | F_STORE_MAIN)                                         \
+    X(F_RESIDUAL | F_STORE_MAIN)
 
 template <int FL, int CG>
 int launch_fast_fl(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mm, const CUtensorMap& mx,

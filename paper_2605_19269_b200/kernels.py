@@ -354,6 +354,32 @@ def pipeline_grrg_forward(x, w0, z, gamma, w1, *, config: PipelineConfig) -> Grr
     return GrrgResult(y=k5.main, pre_norm=k4.aux["pre_norm"], normed=k4.main, inv_rms=r, ledger=ledger)
 
 
+def pipeline_grrg_canonical(x, w0, z, gamma, w1, *, config: PipelineConfig):
+    """Unfused reference schedule (kernels.py:677-713) on cuBLAS + torch elementwise.
+
+    A comparator, not the product path: four standalone ops with every
+    intermediate stored at the storage precision.  Returns (y, canonical ledger).
+    """
+    from . import unfused
+
+    if config.precision is PrecisionMode.EXACT64:
+        raise ConfigError("EXACT64 runs only in the CPU oracle; the GPU engine supports SIM32 and SIMBF16")
+    P = config.precision
+    t = lambda m: m.tensor.to(P.torch_dtype)  # noqa: E731
+    y = unfused.grrg(t(x), t(w0), t(z), gamma.tensor.float(), t(w1), config.eps)
+    m, k = x.shape
+    d, n = w0.shape[1], w1.shape[1]
+    ledger = TrafficLedger()
+    w, pw = P.storage_bytes, P.partial_bytes
+    ledger.record("gemm", (m * k + k * d) * w, m * d * w)
+    ledger.record("residual_add", 2 * m * d * w, m * d * w)
+    ledger.record("rmsnorm", (m * d + d) * w, m * d * w)
+    ledger.record("gemm", (m * d + d * n) * w, m * n * w)
+    out = alloc_matrix(y.shape[0], y.shape[1], y.dtype, y.device)
+    out.copy_(y)
+    return DenseMatrix._wrap(out, P), ledger
+
+
 # ---------------------------------------------------------------------------
 # transformer layer (kernels.py:716-1013)
 

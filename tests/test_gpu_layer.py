@@ -125,3 +125,50 @@ def test_eps_path_all_zero_input(cuda_ready):
     fwd = cd.layer_forward(zero, zero, w, cos, sin, config=cfg)
     assert np.all(fwd.qkv.data == 0.0)
     np.testing.assert_allclose(fwd.tape.inv_rms_a.data, np.float32(1.0 / np.sqrt(np.float32(1e-6))), rtol=1e-6)
+
+
+@pytest.mark.parametrize("mode_name", ["sim32", "simbf16"])
+def test_block_stack_vs_chained_oracle(cuda_ready, mode_name):
+    """3-block stack (x_{l+1} = V span of qkv_l, z_{l+1} = residual_l) vs the oracle chained the same way."""
+    cd = _cd()
+    from paper_2605_19269_b200 import stack
+
+    m, d, ffn, L = 192, 128, 512, 3
+    mode = O.SIM32 if mode_name == "sim32" else O.SIMBF16
+    P = cd.PrecisionMode.SIM32 if mode_name == "sim32" else cd.PrecisionMode.SIMBF16
+    rng = np.random.default_rng(4)
+    ws = [O.random_layer(rng, d, ffn, mode, scale=0.1) for _ in range(L)]
+    x = O.q(rng.standard_normal((m, d)), mode)
+    z = O.q(rng.standard_normal((m, d)), mode)
+    cos, sin = O.qkv_rope_tables(m, d, mode)
+    gq = O.q(rng.standard_normal((m, 3 * d)), mode)
+    gr = O.q(rng.standard_normal((m, d)), mode)
+    # oracle chain
+    fw, xi, zi = [], x, z
+    for w in ws:
+        f = O.layer_forward(xi, zi, w, cos, sin, mode)
+        fw.append(f)
+        xi, zi = f["qkv"][:, 2 * d:], f["residual"]
+    ref_grads = [None] * L
+    g_q, g_r = gq, gr
+    for l in range(L - 1, -1, -1):
+        b = O.layer_backward(g_q, fw[l], ws[l], mode, grad_residual=g_r)
+        ref_grads[l] = b
+        g_q = np.concatenate([np.zeros((m, 2 * d)), b["x"]], axis=1)
+        g_r = b["z"]
+    # device stack
+    M = lambda a: cd.DenseMatrix.from_array(a, P)  # noqa: E731
+    dws = [cd.LayerWeights(w_out=M(w["w_out"]), gamma_ffn=cd.Vector.from_array(w["gamma_ffn"], P),
+                           w_gate_up=M(w["w_gate_up"]), w_down=M(w["w_down"]),
+                           gamma_qkv=cd.Vector.from_array(w["gamma_qkv"], P), w_qkv=M(w["w_qkv"])) for w in ws]
+    cfg = cd.PipelineConfig(hidden=d, ffn=ffn, precision=P)
+    res = stack.stack_forward(M(x), M(z), dws, M(cos), M(sin), config=cfg)
+    grads = stack.stack_backward(M(gq), M(gr), res, dws, config=cfg)
+    tol = 1e-5 if mode_name == "sim32" else 2e-2
+    assert O.rel_error(res.qkv.data, fw[-1]["qkv"]) <= tol
+    worst = 0.0
+    for l in range(L):
+        for key in O.GRAD_KEYS:
+            worst = max(worst, O.rel_error(getattr(grads[l], key).data, ref_grads[l][key]))
+    print(f"\n[stack {mode_name}] worst grad rel err {worst:.2e}")
+    assert worst <= tol
