@@ -322,9 +322,14 @@ def coda_arm(args, rank, world, local_rank):
 
     if args.ncu:
         # profiler pass: a few steps, nothing else (numbers printed under ncu are not bench values)
-        for _ in range(args.warmup + args.steps):
+        for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("measure")   # ncu --nvtx --nvtx-include "measure/" = one step
+        for _ in range(max(1, args.steps)):
+            step()
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
         if dist is not None:
             dist.destroy_process_group()
         return

@@ -558,7 +558,7 @@ int coda_finalize_rms(const float* p, int64_t m, int64_t nb, int64_t ld, int64_t
     if (d <= 0) return fail(CODA_E_DEGENERATE, "partial blocks cover no columns");
     int rc;
     if ((rc = bind_device(p))) return rc;
-    coda::finalize_rms_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(p, m, nb, ld, (float)d, eps, r);
+    coda::coda_finalize_rms_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(p, m, nb, ld, (float)d, eps, r);
     return cuda_check(cudaGetLastError(), "finalize_rms");
 }
 
@@ -567,7 +567,7 @@ int coda_finalize_rowdot(const float* p, int64_t m, int64_t nb, int64_t ld, int6
     if (d <= 0) return fail(CODA_E_CONFIG, "normalized width must be positive, got %lld", (long long)d);
     int rc;
     if ((rc = bind_device(p))) return rc;
-    coda::finalize_rowdot_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(p, m, nb, ld, (float)d, s);
+    coda::coda_finalize_rowdot_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(p, m, nb, ld, (float)d, s);
     return cuda_check(cudaGetLastError(), "finalize_rowdot");
 }
 
@@ -575,7 +575,7 @@ int coda_reduce_row_partials(const float* p, int64_t tm, int64_t n, int64_t ld, 
     if (tm <= 0 || n <= 0) return fail(CODA_E_DIMENSION, "reduce_row_partials: empty partials");
     int rc;
     if ((rc = bind_device(p))) return rc;
-    coda::reduce_row_partials_kernel<<<grid1d(n, 256), 256, 0, (cudaStream_t)stream>>>(p, tm, n, ld, out);
+    coda::coda_reduce_row_partials_kernel<<<grid1d(n, 256), 256, 0, (cudaStream_t)stream>>>(p, tm, n, ld, out);
     return cuda_check(cudaGetLastError(), "reduce_row_partials");
 }
 
@@ -583,7 +583,7 @@ int coda_combine_lse(const float* p, int64_t m, int64_t nb, int64_t ld, float* l
     if (m <= 0 || nb <= 0) return fail(CODA_E_DIMENSION, "combine_lse: empty partials");
     int rc;
     if ((rc = bind_device(p))) return rc;
-    coda::combine_lse_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(p, m, nb, ld, lse);
+    coda::coda_combine_lse_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(p, m, nb, ld, lse);
     return cuda_check(cudaGetLastError(), "combine_lse");
 }
 
@@ -591,7 +591,7 @@ int coda_cross_entropy_finalize(const float* target, const float* lse, int64_t m
     if (m <= 0) return fail(CODA_E_DIMENSION, "cross_entropy_finalize: empty");
     int rc;
     if ((rc = bind_device(lse))) return rc;
-    coda::ce_finalize_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(target, lse, m, losses);
+    coda::coda_ce_finalize_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(target, lse, m, losses);
     return cuda_check(cudaGetLastError(), "cross_entropy_finalize");
 }
 
@@ -618,12 +618,12 @@ int coda_rope_backward_stat(const coda_tensor_t* grad, const coda_tensor_t* rota
         if (nb != (grad->cols + 127) / 128) return fail(CODA_E_DIMENSION, "rope_backward_stat: nb != ceil(n/128)");
         const unsigned grid = (unsigned)(grad->rows < 148 * 8 ? grad->rows : 148 * 8);
         if (dt == CODA_BF16) {
-            coda::rope_backward_stat128_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+            coda::coda_rope_backward_stat128_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
                 (const __nv_bfloat16*)grad->ptr, grad->ld, (const __nv_bfloat16*)rotated->ptr, rotated->ld,
                 (const __nv_bfloat16*)cos->ptr, cos->ld, (const __nv_bfloat16*)sin->ptr, sin->ld, grad->rows,
                 grad->cols, (__nv_bfloat16*)grad_z->ptr, grad_z->ld, rowdot, ld_rowdot);
         } else {
-            coda::rope_backward_stat128_kernel<float><<<grid, 256, 0, st>>>(
+            coda::coda_rope_backward_stat128_kernel<float><<<grid, 256, 0, st>>>(
                 (const float*)grad->ptr, grad->ld, (const float*)rotated->ptr, rotated->ld, (const float*)cos->ptr,
                 cos->ld, (const float*)sin->ptr, sin->ld, grad->rows, grad->cols, (float*)grad_z->ptr, grad_z->ld,
                 rowdot, ld_rowdot);
@@ -633,14 +633,14 @@ int coda_rope_backward_stat(const coda_tensor_t* grad, const coda_tensor_t* rota
     const size_t smem = (size_t)grad->cols * 4;
     if (smem > 200 * 1024) return fail(CODA_E_CONFIG, "rope_backward_stat: row too wide (%lld)", (long long)grad->cols);
     if (dt == CODA_BF16) {
-        auto k = coda::rope_backward_stat_kernel<__nv_bfloat16>;
+        auto k = coda::coda_rope_backward_stat_kernel<__nv_bfloat16>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         k<<<(unsigned)grad->rows, 256, smem, st>>>(
             (const __nv_bfloat16*)grad->ptr, grad->ld, (const __nv_bfloat16*)rotated->ptr, rotated->ld,
             (const __nv_bfloat16*)cos->ptr, cos->ld, (const __nv_bfloat16*)sin->ptr, sin->ld, grad->cols, block_start,
             nb, (__nv_bfloat16*)grad_z->ptr, grad_z->ld, rowdot, ld_rowdot);
     } else {
-        auto k = coda::rope_backward_stat_kernel<float>;
+        auto k = coda::coda_rope_backward_stat_kernel<float>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         k<<<(unsigned)grad->rows, 256, smem, st>>>(
             (const float*)grad->ptr, grad->ld, (const float*)rotated->ptr, rotated->ld, (const float*)cos->ptr, cos->ld,
@@ -655,7 +655,7 @@ int coda_combine_row_pieces(const float* pieces, int64_t m, int64_t np, int64_t 
     if (m <= 0 || np <= 0 || nb <= 0) return fail(CODA_E_DIMENSION, "combine_row_pieces: empty");
     int rc;
     if ((rc = bind_device(pieces))) return rc;
-    coda::combine_row_pieces_kernel<<<grid1d(m * nb, 256), 256, 0, (cudaStream_t)stream>>>(
+    coda::coda_combine_row_pieces_kernel<<<grid1d(m * nb, 256), 256, 0, (cudaStream_t)stream>>>(
         pieces, m, np, ldp, block_ptr, nb, pairs, out, ldo);
     return cuda_check(cudaGetLastError(), "combine_row_pieces");
 }
@@ -667,7 +667,7 @@ int coda_combine_col_pieces(const float* pieces, int64_t np, int64_t n, int64_t 
     int rc;
     if ((rc = bind_device(pieces))) return rc;
     dim3 grid(grid1d(n, 256), (unsigned)nb);
-    coda::combine_col_pieces_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(pieces, np, n, ldp, block_ptr, nb, out, ldo);
+    coda::coda_combine_col_pieces_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(pieces, np, n, ldp, block_ptr, nb, out, ldo);
     return cuda_check(cudaGetLastError(), "combine_col_pieces");
 }
 
@@ -686,7 +686,7 @@ int coda_split_operand(const coda_tensor_t* src, int k_axis, int64_t kp, const i
         pat.t[i] = pattern[i];
     }
     if ((rc = bind_device(src->ptr))) return rc;
-    coda::split_operand_kernel<<<grid1d(drows * dcols, 256), 256, 0, (cudaStream_t)stream>>>(
+    coda::coda_split_operand_kernel<<<grid1d(drows * dcols, 256), 256, 0, (cudaStream_t)stream>>>(
         (const float*)src->ptr, src->rows, src->cols, src->ld, k_axis, kp, pat, (__nv_bfloat16*)dst->ptr, drows,
         dcols, dst->ld);
     return cuda_check(cudaGetLastError(), "split_operand");
@@ -698,7 +698,7 @@ int coda_convert_f32_bf16(const coda_tensor_t* src, coda_tensor_t* dst, void* st
     if (src->rows != dst->rows || src->cols != dst->cols) return fail(CODA_E_DIMENSION, "convert: shapes differ");
     int rc;
     if ((rc = bind_device(src->ptr))) return rc;
-    coda::convert_f32_bf16_kernel<<<grid1d(src->rows * src->cols, 256), 256, 0, (cudaStream_t)stream>>>(
+    coda::coda_convert_f32_bf16_kernel<<<grid1d(src->rows * src->cols, 256), 256, 0, (cudaStream_t)stream>>>(
         (const float*)src->ptr, src->rows, src->cols, src->ld, (__nv_bfloat16*)dst->ptr, dst->ld);
     return cuda_check(cudaGetLastError(), "convert_f32_bf16");
 }

@@ -13,7 +13,7 @@ namespace coda {
 
 // r = 1 / sqrt(total / d + eps), total summed over blocks in ascending order.
 // IEEE-rounded intrinsics keep the float32 op sequence of reductions.py:74-78.
-__global__ void finalize_rms_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
+__global__ void coda_finalize_rms_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
                                     float d, float eps, float* __restrict__ r) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
@@ -23,7 +23,7 @@ __global__ void finalize_rms_kernel(const float* __restrict__ p, int64_t m, int6
     r[i] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(t, d), eps)));
 }
 
-__global__ void finalize_rowdot_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
+__global__ void coda_finalize_rowdot_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
                                        float d, float* __restrict__ s) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
@@ -34,7 +34,7 @@ __global__ void finalize_rowdot_kernel(const float* __restrict__ p, int64_t m, i
 }
 
 // Column totals over tile rows (coalesced: one thread per column).
-__global__ void reduce_row_partials_kernel(const float* __restrict__ p, int64_t tm, int64_t n, int64_t ld,
+__global__ void coda_reduce_row_partials_kernel(const float* __restrict__ p, int64_t tm, int64_t n, int64_t ld,
                                            float* __restrict__ out) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
@@ -51,7 +51,7 @@ __device__ __forceinline__ void lse_merge(float& m, float& s, float mb, float sb
     m = mn;
 }
 
-__global__ void combine_lse_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
+__global__ void coda_combine_lse_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
                                    float* __restrict__ lse) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
@@ -60,14 +60,14 @@ __global__ void combine_lse_kernel(const float* __restrict__ p, int64_t m, int64
     lse[i] = (mx == -INFINITY) ? NAN : mx + logf(s);
 }
 
-__global__ void ce_finalize_kernel(const float* __restrict__ target, const float* __restrict__ lse, int64_t m,
+__global__ void coda_ce_finalize_kernel(const float* __restrict__ target, const float* __restrict__ lse, int64_t m,
                                    float* __restrict__ loss) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) loss[i] = lse[i] - target[i];
 }
 
 // pieces (m, np) -> blocks (m, nb): block b sums pieces [ptr[b], ptr[b+1]).
-__global__ void combine_row_pieces_kernel(const float* __restrict__ pc, int64_t m, int64_t np, int64_t ldp,
+__global__ void coda_combine_row_pieces_kernel(const float* __restrict__ pc, int64_t m, int64_t np, int64_t ldp,
                                           const int32_t* __restrict__ ptr, int64_t nb, int pairs,
                                           float* __restrict__ out, int64_t ldo) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -87,7 +87,7 @@ __global__ void combine_row_pieces_kernel(const float* __restrict__ pc, int64_t 
 }
 
 // pieces (np, n) -> blocks (nb, n)
-__global__ void combine_col_pieces_kernel(const float* __restrict__ pc, int64_t np, int64_t n, int64_t ldp,
+__global__ void coda_combine_col_pieces_kernel(const float* __restrict__ pc, int64_t np, int64_t n, int64_t ldp,
                                           const int32_t* __restrict__ ptr, int64_t nb,
                                           float* __restrict__ out, int64_t ldo) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -106,7 +106,7 @@ __global__ void combine_col_pieces_kernel(const float* __restrict__ pc, int64_t 
 // thread in column order (deterministic, no atomics).
 template <typename TS>
 __global__ void __launch_bounds__(256)
-rope_backward_stat_kernel(const TS* __restrict__ g, int64_t ldg, const TS* __restrict__ rot, int64_t ldr,
+coda_rope_backward_stat_kernel(const TS* __restrict__ g, int64_t ldg, const TS* __restrict__ rot, int64_t ldr,
                           const TS* __restrict__ cs, int64_t ldc, const TS* __restrict__ sn, int64_t lds,
                           int64_t n, const int32_t* __restrict__ bstart, int64_t nb,
                           TS* __restrict__ gz, int64_t ldz, float* __restrict__ rowdot, int64_t ldd) {
@@ -161,7 +161,7 @@ rope_backward_stat_kernel(const TS* __restrict__ g, int64_t ldg, const TS* __res
 // tree.  Several rows per CTA keep enough loads in flight for HBM.
 template <typename TS>
 __global__ void __launch_bounds__(256)
-rope_backward_stat128_kernel(const TS* __restrict__ g, int64_t ldg, const TS* __restrict__ rot, int64_t ldr,
+coda_rope_backward_stat128_kernel(const TS* __restrict__ g, int64_t ldg, const TS* __restrict__ rot, int64_t ldr,
                              const TS* __restrict__ cs, int64_t ldc, const TS* __restrict__ sn, int64_t lds,
                              int64_t m, int64_t n, TS* __restrict__ gz, int64_t ldz, float* __restrict__ rowdot,
                              int64_t ldd) {
@@ -226,7 +226,7 @@ __device__ __forceinline__ float split_term(float x, int term) {
     return r1 - x1;   // rounded to bf16 on store
 }
 
-__global__ void split_operand_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
+__global__ void coda_split_operand_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
                                      int k_axis, int64_t kp, SplitPattern pat,
                                      __nv_bfloat16* __restrict__ dst, int64_t drows, int64_t dcols, int64_t ldd) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -245,7 +245,7 @@ __global__ void split_operand_kernel(const float* __restrict__ src, int64_t rows
     dst[r * ldd + c] = __float2bfloat16_rn(val);
 }
 
-__global__ void convert_f32_bf16_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
+__global__ void coda_convert_f32_bf16_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
                                         __nv_bfloat16* __restrict__ dst, int64_t ldd) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= rows * cols) return;

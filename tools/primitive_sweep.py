@@ -81,6 +81,14 @@ def main():
             fused()
             unf()
         torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("measure")   # ncu --nvtx --nvtx-include "measure/"
+        for name, (fused, unf) in variants.items():
+            torch.cuda.nvtx.range_push(name)
+            fused()
+            unf()
+            torch.cuda.nvtx.range_pop()
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
         return
     flops = 2.0 * n ** 3
     rows = []
