@@ -184,6 +184,8 @@ inline unsigned grid1d(int64_t n, int threads) { return (unsigned)((n + threads 
 
 // ---------------------------------------------------------------- specialised epilogues
 using coda::F_AUX;
+using coda::F_GATHER;
+using coda::F_LSE;
 using coda::F_OUT_F32;
 using coda::F_RESIDUAL;
 using coda::F_RMSBWD;
@@ -211,7 +213,11 @@ using coda::F_SWIGLU_BWD;
     X(F_RMSBWD | F_RMSBWD_ACC | F_STORE_MAIN)                         \
     X(F_SWIGLU_BWD | F_STORE_MAIN)                                    \
     X(F_SUMSQ | F_STORE_MAIN)                                         \
-    X(F_RESIDUAL | F_STORE_MAIN)
+    X(F_RESIDUAL | F_STORE_MAIN)                                      \
+    X(F_GATHER | F_LSE | F_STORE_MAIN)                                \
+    X(F_GATHER | F_LSE)                                               \
+    X(F_ROWSCALE | F_GATHER | F_LSE)                                  \
+    X(F_ROWSCALE | F_GATHER | F_LSE | F_STORE_MAIN)
 
 template <int FL, int CG>
 int launch_fast_fl(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mm, const CUtensorMap& mx,
@@ -312,12 +318,16 @@ int match_fast(const coda_problem_t* pr, const coda_step_t* steps, int nsteps, c
             fl |= F_SUMSQ; break;
         case CODA_OP_ROW_VEC_MUL: if (!rank_ok(5)) return -1; fl |= F_ROWVEC; break;
         case CODA_OP_ROPE: if (!rank_ok(6)) return -1; fl |= F_ROPE; break;
-        case CODA_OP_SWIGLU: if (!rank_ok(7)) return -1; fl |= F_SWIGLU; break;
+        case CODA_OP_TARGET_GATHER: if (!rank_ok(7)) return -1; fl |= F_GATHER; break;
+        case CODA_OP_ONLINE_LSE:
+            if (!rank_ok(8) || !stores[st.arg[0]].aligned) return -1;
+            fl |= F_LSE; break;
+        case CODA_OP_SWIGLU: if (!rank_ok(9)) return -1; fl |= F_SWIGLU; break;
         case CODA_OP_SWIGLU_BWD:
-            if (!rank_ok(7) || !stores[st.arg[2]].aligned) return -1;
+            if (!rank_ok(9) || !stores[st.arg[2]].aligned) return -1;
             fl |= F_SWIGLU_BWD; break;
         case CODA_OP_RMSNORM_BWD:
-            if (!rank_ok(7) || !stores[st.arg[6]].aligned) return -1;
+            if (!rank_ok(9) || !stores[st.arg[6]].aligned) return -1;
             fl |= F_RMSBWD | (st.arg[4] >= 0 ? F_RMSBWD_ACC : 0); break;
         default: return -1;
         }
@@ -503,6 +513,12 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
                 F.rowpart = (float*)P.store[cs.arg[0]].ptr; F.ld_rowpart = P.store[cs.arg[0]].ld;
                 F.rowpart_map = P.store[cs.arg[0]].map; break;
             case CODA_OP_ROW_VEC_MUL: F.rowvec = (const float*)o[cs.arg[0]].ptr; break;
+            case CODA_OP_TARGET_GATHER:
+                F.labels = (const int64_t*)o[cs.arg[0]].ptr;
+                F.target = (float*)P.store[cs.arg[1]].ptr; break;
+            case CODA_OP_ONLINE_LSE:
+                F.rowpart = (float*)P.store[cs.arg[0]].ptr; F.ld_rowpart = P.store[cs.arg[0]].ld;
+                F.rowpart_map = P.store[cs.arg[0]].map; break;
             case CODA_OP_ROPE:
                 F.cosp = o[cs.arg[0]].ptr; F.ld_cos = o[cs.arg[0]].ld;
                 F.sinp = o[cs.arg[1]].ptr; F.ld_sin = o[cs.arg[1]].ld;

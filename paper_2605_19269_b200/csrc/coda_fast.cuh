@@ -42,6 +42,8 @@ enum FastFlags : int {
     F_RMSBWD_ACC = 1 << 9,
     F_STORE_MAIN = 1 << 10,
     F_OUT_F32 = 1 << 11,
+    F_GATHER = 1 << 12,     // TargetGather: target[row] = tile[row, label[row]]
+    F_LSE = 1 << 13,        // OnlineLse: (max, scaled sum) pairs per piece (rowpart holds pairs)
 };
 
 constexpr int FAST_EPI_WARPS = 8;
@@ -77,6 +79,8 @@ struct FastParams {
     float* colpart;
     int64_t ld_colpart;
     const int32_t* colpart_map;
+    const int64_t* labels;
+    float* target;
 };
 
 template <int CG>
@@ -286,8 +290,10 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 rr = __ldg(P.inv_rms + row);
                 ss = __ldg(P.stat + row);
             }
-            float pacc = 0.0f;
+            float pacc = 0.0f, pmax = -INFINITY;
             int ppid = -1;
+            int64_t label = -1;
+            if ((FL & F_GATHER) && row_ok) label = __ldg(P.labels + row);
 
             if constexpr (CG == 1) mbar_wait(&tfull[acc], acc_phase);
             else mbar_wait_cluster(&tfull[acc], acc_phase);
@@ -356,6 +362,40 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         v[2 * k] = x0 * cs[2 * k] - x1 * se;
                         v[2 * k + 1] = x0 * so + x1 * cs[2 * k + 1];
                     }
+                }
+                if (FL & F_GATHER) {
+                    const int64_t local = label - gcol0;
+                    if (local >= 0 && local < 32 && label < N) {
+                        float val = 0.0f;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (i == (int)local) val = v[i];
+                        P.target[row] = val;
+                    }
+                }
+                if (FL & F_LSE) {
+                    // chunk-level (max, sum exp) merged into the running pair of this piece
+                    float mc = -INFINITY;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (!edge || gcol0 + i < N) mc = fmaxf(mc, v[i]);
+                    float sc = 0.0f;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (!edge || gcol0 + i < N) sc += __expf(v[i] - mc);
+                    const int pid = __ldg(P.rowpart_map + gcol0);
+                    if (pid != ppid) {
+                        if (ppid >= 0 && row_ok) {
+                            P.rowpart[row * P.ld_rowpart + 2 * ppid] = pmax;
+                            P.rowpart[row * P.ld_rowpart + 2 * ppid + 1] = pacc;
+                        }
+                        ppid = pid;
+                        pacc = 0.0f;
+                        pmax = -INFINITY;
+                    }
+                    const float mn = fmaxf(pmax, mc);
+                    pacc = pacc * (pmax == -INFINITY ? 0.0f : __expf(pmax - mn)) + sc * __expf(mc - mn);
+                    pmax = mn;
                 }
                 if (FL & F_SWIGLU) {
 #pragma unroll
@@ -444,9 +484,12 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     if (FL & F_OUT_F32) staged_store<float, 32>(sg, &tma_main, gcol0, m0 + q * 32, v, lane);
                     else staged_store<TS, 32>(sg, &tma_main, gcol0, m0 + q * 32, v, lane);
                 }
-                (void)edge;
             }
             if ((FL & (F_SUMSQ | F_SWIGLU_BWD)) && ppid >= 0 && row_ok) P.rowpart[row * P.ld_rowpart + ppid] = pacc;
+            if ((FL & F_LSE) && ppid >= 0 && row_ok) {
+                P.rowpart[row * P.ld_rowpart + 2 * ppid] = pmax;
+                P.rowpart[row * P.ld_rowpart + 2 * ppid + 1] = pacc;
+            }
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }

@@ -194,6 +194,11 @@ k9 = cd.gemm_rmsnorm_backward(a, bt, pre, r, gamma, s, grad_in=gin, trans_b=True
 outs += [k9.main.data, k9.aux["normed"].data, k9.aux["gamma_grad"].data]
 k10 = cd.gemm_swiglu_backward(a, bt, pre2, trans_b=True, **kw)
 outs += [k10.main.data, k10.aux["recompute"].data, k10.aux["rowdot"].data]
+lab = g["labels"].astype(np.int64)
+k3 = cd.gemm_partial_xent(a, b, lab, store_logits=True, **kw)
+outs += [k3.main.data, k3.aux["target"].data, cd.combine_lse(k3.aux["lse"]).data]
+k8 = cd.gemm_rms_partial_xent(a, b, r, lab, **kw)
+outs += [k8.aux["target"].data, cd.combine_lse(k8.aux["lse"]).data]
 np.savez(sys.argv[1], *outs)
 '''
     res = {}

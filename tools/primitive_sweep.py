@@ -25,18 +25,26 @@ import paper_2605_19269_b200 as cd  # noqa: E402
 from paper_2605_19269_b200 import unfused  # noqa: E402
 
 
-def timeit(fn, reps, warmup=5):
+def timeit(fn, reps, warmup=5, inner=10):
+    """Median device time of one call: `inner` calls captured in a CUDA graph and
+    replayed, so host launch latency (Python) is excluded for both variants."""
     for _ in range(warmup):
         fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(inner):
+            fn()
+    g.replay()
     torch.cuda.synchronize()
     times = []
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        fn()
+        g.replay()
         e1.record()
         torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1))
+        times.append(e0.elapsed_time(e1) / inner)
     return statistics.median(times)
 
 
