@@ -14,6 +14,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <utility>
 
 #include "../../include/coda.h"
 #include "coda_aux.cuh"
@@ -164,6 +165,45 @@ int num_sms() {
     return g_num_sms;
 }
 
+// ---------------------------------------------------------------- launches (PDL + clusters)
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("CODA_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// Launch with programmatic stream serialization (kernel N+1's prologue overlaps
+// kernel N's tail; every kernel calls griddep_wait() before touching global
+// memory) and an optional cluster shape.
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,
+               const char* what, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    if (pdl_enabled()) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    if (cluster > 1) {
+        attr[n].id = cudaLaunchAttributeClusterDimension;
+        attr[n].val.clusterDim.x = (unsigned)cluster;
+        attr[n].val.clusterDim.y = 1;
+        attr[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    return cuda_check(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...), what);
+}
+
 template <typename TS>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const coda::GemmParams& P, cudaStream_t st) {
     static bool configured = false;
@@ -176,11 +216,12 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const coda::GemmPa
     }
     const int nsm = num_sms();
     const int grid = P.ntiles < nsm ? P.ntiles : nsm;
-    coda::coda_gemm_kernel<TS><<<grid, coda::NUM_THREADS, smem, st>>>(ma, mb, P);
-    return cuda_check(cudaGetLastError(), "coda_gemm_kernel launch");
+    return launch_pdl(coda::coda_gemm_kernel<TS>, dim3(grid), dim3(coda::NUM_THREADS), smem, st, 1,
+                      "coda_gemm_kernel launch", ma, mb, P);
 }
 
 inline unsigned grid1d(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
 
 // ---------------------------------------------------------------- specialised epilogues
 using coda::F_AUX;
@@ -236,19 +277,8 @@ int launch_fast_fl(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorM
     }
     const int units = num_sms() / CG;
     const int grid = (P.mp.ntiles < units ? P.mp.ntiles : units) * CG;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(coda::FAST_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cuda_check(cudaLaunchKernelEx(&cfg, kern, ma, mb, mm, mx, P), "coda_gemm_fast launch");
+    return launch_pdl(kern, dim3((unsigned)grid), dim3(coda::FAST_THREADS), smem, st, CG, "coda_gemm_fast launch",
+                      ma, mb, mm, mx, P);
 }
 
 int fast_cg() {
@@ -574,8 +604,18 @@ int coda_finalize_rms(const float* p, int64_t m, int64_t nb, int64_t ld, int64_t
     if (d <= 0) return fail(CODA_E_DEGENERATE, "partial blocks cover no columns");
     int rc;
     if ((rc = bind_device(p))) return rc;
-    coda::coda_finalize_rms_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(p, m, nb, ld, (float)d, eps, r);
-    return cuda_check(cudaGetLastError(), "finalize_rms");
+    if (nb <= 1024) {
+        static bool cfg_done = false;
+        if (!cfg_done) {
+            cudaFuncSetAttribute(coda::coda_finalize_rms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+            cfg_done = true;
+        }
+        const size_t smem = (size_t)coda::FIN_ROWS * (nb + 1) * 4;
+        return launch_pdl(coda::coda_finalize_rms_kernel, dim3((unsigned)((m + coda::FIN_ROWS - 1) / coda::FIN_ROWS)),
+                          dim3(256), smem, (cudaStream_t)stream, 1, "finalize_rms", p, m, nb, ld, (float)d, eps, r);
+    }
+    return launch_pdl(coda::coda_finalize_rms_wide_kernel, dim3(grid1d(m, 256)), dim3(256), 0, (cudaStream_t)stream, 1,
+                      "finalize_rms_wide", p, m, nb, ld, (float)d, eps, r);
 }
 
 int coda_finalize_rowdot(const float* p, int64_t m, int64_t nb, int64_t ld, int64_t d, float* s, void* stream) {
@@ -583,32 +623,43 @@ int coda_finalize_rowdot(const float* p, int64_t m, int64_t nb, int64_t ld, int6
     if (d <= 0) return fail(CODA_E_CONFIG, "normalized width must be positive, got %lld", (long long)d);
     int rc;
     if ((rc = bind_device(p))) return rc;
-    coda::coda_finalize_rowdot_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(p, m, nb, ld, (float)d, s);
-    return cuda_check(cudaGetLastError(), "finalize_rowdot");
+    if (nb <= 1024) {
+        static bool cfg_done = false;
+        if (!cfg_done) {
+            cudaFuncSetAttribute(coda::coda_finalize_rowdot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 140 * 1024);
+            cfg_done = true;
+        }
+        const size_t smem = (size_t)coda::FIN_ROWS * (nb + 1) * 4;
+        return launch_pdl(coda::coda_finalize_rowdot_kernel, dim3((unsigned)((m + coda::FIN_ROWS - 1) / coda::FIN_ROWS)),
+                          dim3(256), smem, (cudaStream_t)stream, 1, "finalize_rowdot", p, m, nb, ld, (float)d, s);
+    }
+    return launch_pdl(coda::coda_finalize_rowdot_wide_kernel, dim3(grid1d(m, 256)), dim3(256), 0, (cudaStream_t)stream,
+                      1, "finalize_rowdot_wide", p, m, nb, ld, (float)d, s);
 }
 
 int coda_reduce_row_partials(const float* p, int64_t tm, int64_t n, int64_t ld, float* out, void* stream) {
     if (tm <= 0 || n <= 0) return fail(CODA_E_DIMENSION, "reduce_row_partials: empty partials");
     int rc;
     if ((rc = bind_device(p))) return rc;
-    coda::coda_reduce_row_partials_kernel<<<grid1d(n, 256), 256, 0, (cudaStream_t)stream>>>(p, tm, n, ld, out);
-    return cuda_check(cudaGetLastError(), "reduce_row_partials");
+    return launch_pdl(coda::coda_reduce_row_partials_kernel, dim3(grid1d(n, 256)), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_reduce_row_partials_kernel",
+        p, tm, n, ld, out);
 }
 
 int coda_combine_lse(const float* p, int64_t m, int64_t nb, int64_t ld, float* lse, void* stream) {
     if (m <= 0 || nb <= 0) return fail(CODA_E_DIMENSION, "combine_lse: empty partials");
     int rc;
     if ((rc = bind_device(p))) return rc;
-    coda::coda_combine_lse_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(p, m, nb, ld, lse);
-    return cuda_check(cudaGetLastError(), "combine_lse");
+    return launch_pdl(coda::coda_combine_lse_kernel, dim3(grid1d(m, 256)), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_combine_lse_kernel",
+        p, m, nb, ld, lse);
 }
 
 int coda_cross_entropy_finalize(const float* target, const float* lse, int64_t m, float* losses, void* stream) {
     if (m <= 0) return fail(CODA_E_DIMENSION, "cross_entropy_finalize: empty");
     int rc;
     if ((rc = bind_device(lse))) return rc;
-    coda::coda_ce_finalize_kernel<<<grid1d(m, 256), 256, 0, (cudaStream_t)stream>>>(target, lse, m, losses);
-    return cuda_check(cudaGetLastError(), "cross_entropy_finalize");
+    return launch_pdl(coda::coda_ce_finalize_kernel, dim3(grid1d(m, 256)), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_ce_finalize_kernel",
+        target, lse, m, losses);
 }
 
 int coda_rope_backward_stat(const coda_tensor_t* grad, const coda_tensor_t* rotated, const coda_tensor_t* cos,
@@ -634,13 +685,13 @@ int coda_rope_backward_stat(const coda_tensor_t* grad, const coda_tensor_t* rota
         if (nb != (grad->cols + 127) / 128) return fail(CODA_E_DIMENSION, "rope_backward_stat: nb != ceil(n/128)");
         const unsigned grid = (unsigned)(grad->rows < 148 * 8 ? grad->rows : 148 * 8);
         if (dt == CODA_BF16) {
-            coda::coda_rope_backward_stat128_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
-                (const __nv_bfloat16*)grad->ptr, grad->ld, (const __nv_bfloat16*)rotated->ptr, rotated->ld,
+            return launch_pdl(coda::coda_rope_backward_stat128_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, st, 1, "coda::coda_rope_backward_stat128_kernel<__nv_bfloat16>",
+        (const __nv_bfloat16*)grad->ptr, grad->ld, (const __nv_bfloat16*)rotated->ptr, rotated->ld,
                 (const __nv_bfloat16*)cos->ptr, cos->ld, (const __nv_bfloat16*)sin->ptr, sin->ld, grad->rows,
                 grad->cols, (__nv_bfloat16*)grad_z->ptr, grad_z->ld, rowdot, ld_rowdot);
         } else {
-            coda::coda_rope_backward_stat128_kernel<float><<<grid, 256, 0, st>>>(
-                (const float*)grad->ptr, grad->ld, (const float*)rotated->ptr, rotated->ld, (const float*)cos->ptr,
+            return launch_pdl(coda::coda_rope_backward_stat128_kernel<float>, dim3(grid), dim3(256), 0, st, 1, "coda::coda_rope_backward_stat128_kernel<float>",
+        (const float*)grad->ptr, grad->ld, (const float*)rotated->ptr, rotated->ld, (const float*)cos->ptr,
                 cos->ld, (const float*)sin->ptr, sin->ld, grad->rows, grad->cols, (float*)grad_z->ptr, grad_z->ld,
                 rowdot, ld_rowdot);
         }
@@ -651,15 +702,15 @@ int coda_rope_backward_stat(const coda_tensor_t* grad, const coda_tensor_t* rota
     if (dt == CODA_BF16) {
         auto k = coda::coda_rope_backward_stat_kernel<__nv_bfloat16>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        k<<<(unsigned)grad->rows, 256, smem, st>>>(
-            (const __nv_bfloat16*)grad->ptr, grad->ld, (const __nv_bfloat16*)rotated->ptr, rotated->ld,
+        return launch_pdl(k, dim3((unsigned)grad->rows), dim3(256), smem, st, 1, "k",
+        (const __nv_bfloat16*)grad->ptr, grad->ld, (const __nv_bfloat16*)rotated->ptr, rotated->ld,
             (const __nv_bfloat16*)cos->ptr, cos->ld, (const __nv_bfloat16*)sin->ptr, sin->ld, grad->cols, block_start,
             nb, (__nv_bfloat16*)grad_z->ptr, grad_z->ld, rowdot, ld_rowdot);
     } else {
         auto k = coda::coda_rope_backward_stat_kernel<float>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        k<<<(unsigned)grad->rows, 256, smem, st>>>(
-            (const float*)grad->ptr, grad->ld, (const float*)rotated->ptr, rotated->ld, (const float*)cos->ptr, cos->ld,
+        return launch_pdl(k, dim3((unsigned)grad->rows), dim3(256), smem, st, 1, "k",
+        (const float*)grad->ptr, grad->ld, (const float*)rotated->ptr, rotated->ld, (const float*)cos->ptr, cos->ld,
             (const float*)sin->ptr, sin->ld, grad->cols, block_start, nb, (float*)grad_z->ptr, grad_z->ld, rowdot,
             ld_rowdot);
     }
@@ -671,9 +722,8 @@ int coda_combine_row_pieces(const float* pieces, int64_t m, int64_t np, int64_t 
     if (m <= 0 || np <= 0 || nb <= 0) return fail(CODA_E_DIMENSION, "combine_row_pieces: empty");
     int rc;
     if ((rc = bind_device(pieces))) return rc;
-    coda::coda_combine_row_pieces_kernel<<<grid1d(m * nb, 256), 256, 0, (cudaStream_t)stream>>>(
+    return launch_pdl(coda::coda_combine_row_pieces_kernel, dim3(grid1d(m * nb, 256)), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_combine_row_pieces_kernel",
         pieces, m, np, ldp, block_ptr, nb, pairs, out, ldo);
-    return cuda_check(cudaGetLastError(), "combine_row_pieces");
 }
 
 int coda_combine_col_pieces(const float* pieces, int64_t np, int64_t n, int64_t ldp, const int32_t* block_ptr,
@@ -683,8 +733,8 @@ int coda_combine_col_pieces(const float* pieces, int64_t np, int64_t n, int64_t 
     int rc;
     if ((rc = bind_device(pieces))) return rc;
     dim3 grid(grid1d(n, 256), (unsigned)nb);
-    coda::coda_combine_col_pieces_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(pieces, np, n, ldp, block_ptr, nb, out, ldo);
-    return cuda_check(cudaGetLastError(), "combine_col_pieces");
+    return launch_pdl(coda::coda_combine_col_pieces_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_combine_col_pieces_kernel",
+        pieces, np, n, ldp, block_ptr, nb, out, ldo);
 }
 
 int coda_split_operand(const coda_tensor_t* src, int k_axis, int64_t kp, const int32_t pattern[6],
@@ -702,10 +752,9 @@ int coda_split_operand(const coda_tensor_t* src, int k_axis, int64_t kp, const i
         pat.t[i] = pattern[i];
     }
     if ((rc = bind_device(src->ptr))) return rc;
-    coda::coda_split_operand_kernel<<<grid1d(drows * dcols, 256), 256, 0, (cudaStream_t)stream>>>(
+    return launch_pdl(coda::coda_split_operand_kernel, dim3(grid1d(drows * dcols, 256)), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_split_operand_kernel",
         (const float*)src->ptr, src->rows, src->cols, src->ld, k_axis, kp, pat, (__nv_bfloat16*)dst->ptr, drows,
         dcols, dst->ld);
-    return cuda_check(cudaGetLastError(), "split_operand");
 }
 
 int coda_convert_f32_bf16(const coda_tensor_t* src, coda_tensor_t* dst, void* stream) {
@@ -714,9 +763,8 @@ int coda_convert_f32_bf16(const coda_tensor_t* src, coda_tensor_t* dst, void* st
     if (src->rows != dst->rows || src->cols != dst->cols) return fail(CODA_E_DIMENSION, "convert: shapes differ");
     int rc;
     if ((rc = bind_device(src->ptr))) return rc;
-    coda::coda_convert_f32_bf16_kernel<<<grid1d(src->rows * src->cols, 256), 256, 0, (cudaStream_t)stream>>>(
+    return launch_pdl(coda::coda_convert_f32_bf16_kernel, dim3(grid1d(src->rows * src->cols, 256)), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_convert_f32_bf16_kernel",
         (const float*)src->ptr, src->rows, src->cols, src->ld, (__nv_bfloat16*)dst->ptr, dst->ld);
-    return cuda_check(cudaGetLastError(), "convert_f32_bf16");
 }
 
 }  // extern "C"

@@ -11,31 +11,72 @@
 
 namespace coda {
 
-// r = 1 / sqrt(total / d + eps), total summed over blocks in ascending order.
-// IEEE-rounded intrinsics keep the float32 op sequence of reductions.py:74-78.
-__global__ void coda_finalize_rms_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
-                                    float d, float eps, float* __restrict__ r) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= m) return;
-    const float* row = p + i * ld;
+// Row totals of (m, nb) partials in ascending block order.  A CTA stages 32
+// rows through shared memory with coalesced loads, then thread r sums row r
+// sequentially — the float32 op order of reductions.py:_row_sum_total.
+constexpr int FIN_ROWS = 32;
+constexpr int FIN_MAXNB = 512;
+
+__device__ __forceinline__ float staged_row_total(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
+                                                  float* tile, int64_t row0) {
+    for (int64_t idx = threadIdx.x; idx < (int64_t)FIN_ROWS * nb; idx += blockDim.x) {
+        const int64_t r = idx / nb, b = idx % nb;
+        tile[r * (nb + 1) + b] = (row0 + r < m) ? p[(row0 + r) * ld + b] : 0.0f;
+    }
+    __syncthreads();
     float t = 0.0f;
-    for (int64_t b = 0; b < nb; ++b) t = __fadd_rn(t, row[b]);
-    r[i] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(t, d), eps)));
+    if (threadIdx.x < FIN_ROWS) {
+        const float* row = tile + threadIdx.x * (nb + 1);
+        for (int64_t b = 0; b < nb; ++b) t = __fadd_rn(t, row[b]);
+    }
+    return t;
+}
+
+// r = 1 / sqrt(total / d + eps) with IEEE-rounded intrinsics (reductions.py:74-78).
+__global__ void coda_finalize_rms_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
+                                         float d, float eps, float* __restrict__ r) {
+    extern __shared__ float tile[];
+    griddep_wait();
+    const int64_t row0 = (int64_t)blockIdx.x * FIN_ROWS;
+    const float t = staged_row_total(p, m, nb, ld, tile, row0);
+    if (threadIdx.x < FIN_ROWS && row0 + threadIdx.x < m)
+        r[row0 + threadIdx.x] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(t, d), eps)));
 }
 
 __global__ void coda_finalize_rowdot_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
-                                       float d, float* __restrict__ s) {
+                                            float d, float* __restrict__ s) {
+    extern __shared__ float tile[];
+    griddep_wait();
+    const int64_t row0 = (int64_t)blockIdx.x * FIN_ROWS;
+    const float t = staged_row_total(p, m, nb, ld, tile, row0);
+    if (threadIdx.x < FIN_ROWS && row0 + threadIdx.x < m) s[row0 + threadIdx.x] = __fdiv_rn(t, d);
+}
+
+// Very wide partial rows (tiny reduction blocks): one thread per row, same order.
+__global__ void coda_finalize_rms_wide_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld, float d,
+                                              float eps, float* __restrict__ r) {
+    griddep_wait();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
-    const float* row = p + i * ld;
     float t = 0.0f;
-    for (int64_t b = 0; b < nb; ++b) t = __fadd_rn(t, row[b]);
+    for (int64_t b = 0; b < nb; ++b) t = __fadd_rn(t, p[i * ld + b]);
+    r[i] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(t, d), eps)));
+}
+
+__global__ void coda_finalize_rowdot_wide_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
+                                                 float d, float* __restrict__ s) {
+    griddep_wait();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    float t = 0.0f;
+    for (int64_t b = 0; b < nb; ++b) t = __fadd_rn(t, p[i * ld + b]);
     s[i] = __fdiv_rn(t, d);
 }
 
 // Column totals over tile rows (coalesced: one thread per column).
 __global__ void coda_reduce_row_partials_kernel(const float* __restrict__ p, int64_t tm, int64_t n, int64_t ld,
                                            float* __restrict__ out) {
+    griddep_wait();
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     float t = 0.0f;
@@ -53,6 +94,7 @@ __device__ __forceinline__ void lse_merge(float& m, float& s, float mb, float sb
 
 __global__ void coda_combine_lse_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
                                    float* __restrict__ lse) {
+    griddep_wait();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
     float mx = -INFINITY, s = 0.0f;
@@ -62,6 +104,7 @@ __global__ void coda_combine_lse_kernel(const float* __restrict__ p, int64_t m, 
 
 __global__ void coda_ce_finalize_kernel(const float* __restrict__ target, const float* __restrict__ lse, int64_t m,
                                    float* __restrict__ loss) {
+    griddep_wait();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) loss[i] = lse[i] - target[i];
 }
@@ -70,6 +113,7 @@ __global__ void coda_ce_finalize_kernel(const float* __restrict__ target, const 
 __global__ void coda_combine_row_pieces_kernel(const float* __restrict__ pc, int64_t m, int64_t np, int64_t ldp,
                                           const int32_t* __restrict__ ptr, int64_t nb, int pairs,
                                           float* __restrict__ out, int64_t ldo) {
+    griddep_wait();
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= m * nb) return;
     const int64_t i = idx / nb, b = idx % nb;
@@ -90,6 +134,7 @@ __global__ void coda_combine_row_pieces_kernel(const float* __restrict__ pc, int
 __global__ void coda_combine_col_pieces_kernel(const float* __restrict__ pc, int64_t np, int64_t n, int64_t ldp,
                                           const int32_t* __restrict__ ptr, int64_t nb,
                                           float* __restrict__ out, int64_t ldo) {
+    griddep_wait();
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t b = blockIdx.y;
     if (j >= n || b >= nb) return;
@@ -110,6 +155,7 @@ coda_rope_backward_stat_kernel(const TS* __restrict__ g, int64_t ldg, const TS* 
                           const TS* __restrict__ cs, int64_t ldc, const TS* __restrict__ sn, int64_t lds,
                           int64_t n, const int32_t* __restrict__ bstart, int64_t nb,
                           TS* __restrict__ gz, int64_t ldz, float* __restrict__ rowdot, int64_t ldd) {
+    griddep_wait();
     extern __shared__ float prod[];
     const int64_t i = blockIdx.x;
     constexpr int V = Io<TS>::V;
@@ -165,6 +211,7 @@ coda_rope_backward_stat128_kernel(const TS* __restrict__ g, int64_t ldg, const T
                              const TS* __restrict__ cs, int64_t ldc, const TS* __restrict__ sn, int64_t lds,
                              int64_t m, int64_t n, TS* __restrict__ gz, int64_t ldz, float* __restrict__ rowdot,
                              int64_t ldd) {
+    griddep_wait();
     constexpr int V = Io<TS>::V;
     constexpr int LPB = 128 / V;                       // lanes per 128-column block
     const int lane = threadIdx.x & 31;
@@ -229,6 +276,7 @@ __device__ __forceinline__ float split_term(float x, int term) {
 __global__ void coda_split_operand_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
                                      int k_axis, int64_t kp, SplitPattern pat,
                                      __nv_bfloat16* __restrict__ dst, int64_t drows, int64_t dcols, int64_t ldd) {
+    griddep_wait();
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= drows * dcols) return;
     const int64_t r = idx / dcols, c = idx % dcols;
@@ -247,6 +295,7 @@ __global__ void coda_split_operand_kernel(const float* __restrict__ src, int64_t
 
 __global__ void coda_convert_f32_bf16_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
                                         __nv_bfloat16* __restrict__ dst, int64_t ldd) {
+    griddep_wait();
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= rows * cols) return;
     const int64_t r = idx / cols, c = idx % cols;

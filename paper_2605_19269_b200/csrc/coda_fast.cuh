@@ -262,6 +262,10 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     if constexpr (CG == 2) cluster_sync_all();   // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // PDL: let the next launch start its prologue, and wait for the previous one's
+    // results before any global-memory access.
+    griddep_launch_dependents();
+    griddep_wait();
 
     if (warp == 0) {
         if (lane == 0) producer_loop<CG>(mp, &tma_a, &tma_b, sA, sB, full, empty, rank, unit, nunits);

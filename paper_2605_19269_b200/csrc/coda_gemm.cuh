@@ -320,6 +320,8 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    griddep_launch_dependents();
+    griddep_wait();
 
     const MainParams mp{P.M, P.N, P.K, P.ntm, P.ntn, P.nk, P.ntiles, P.a_mn, P.b_mn, 16};
     auto tile_mn = [&](int t, int& tm, int& tn) { tile_coord(mp, t, tm, tn); };

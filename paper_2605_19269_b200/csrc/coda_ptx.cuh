@@ -236,3 +236,14 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
         :: "r"(smem_u32(bar)) : "memory");
 }
 }  // namespace coda
+
+namespace coda {
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every CODA kernel is launched with programmatic stream serialization: it may
+// start while the previous kernel drains, runs its prologue (barriers, TMEM,
+// descriptor prefetch), and touches global memory only after griddep_wait().
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+}  // namespace coda
