@@ -299,8 +299,9 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             int64_t label = -1;
             if ((FL & F_GATHER) && row_ok) label = __ldg(P.labels + row);
 
-            if constexpr (CG == 1) mbar_wait(&tfull[acc], acc_phase);
-            else mbar_wait_cluster(&tfull[acc], acc_phase);
+            // CTA-scope wait: the accumulator is read through tcgen05.ld after the fence below;
+            // a cluster-scope acquire would emit an L1 invalidate (CCTL.IVALL) on every poll.
+            mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + h * 128);
 

@@ -118,8 +118,7 @@ __device__ __forceinline__ void mma_loop(const MainParams& mp, uint32_t tmem_bas
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = unit; t < mp.ntiles; t += nunits) {
-        if constexpr (CG == 1) mbar_wait(&tempty[acc], acc_phase ^ 1);
-        else mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
         for (int kb = 0; kb < mp.nk; ++kb) {

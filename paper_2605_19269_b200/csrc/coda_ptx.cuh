@@ -195,7 +195,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
 }
 // Arrive on the leader CTA's copy of `bar` (works from either CTA of the pair).
 __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];"
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];"
                  :: "r"(smem_u32(bar) & PEER_BIT_MASK) : "memory");
 }
 // 2-SM TMA load: data lands in this CTA's smem, bytes are counted on the leader's barrier.

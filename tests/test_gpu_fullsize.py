@@ -1,0 +1,132 @@
+"""Parity at BASELINE.json's full C4 size through size-independent properties.
+
+The float64 oracle cannot run the whole 16384-token block quickly, so:
+
+* row locality — every forward output and the activation gradients (x, z) of a
+  token depend only on that token's row (plus the weights): a random subset of
+  rows is recomputed by the oracle and compared to the GPU rows;
+* linearity checksums — each full-size weight-gradient GEMM dW = A^T B is
+  checked as dW @ u == A^T (B @ u) for a random probe u, in float64 on the device;
+* the gain gradients are checked the same way against dγ = colsum(D * c_n) of
+  the GPU's own K9 inputs.
+
+Tolerance: bf16 path <= 2e-2 relative (north star), max abs reported.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import coda_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+C4 = dict(m=16384, d=4096, inter=14336)
+
+
+def _cd():
+    import paper_2605_19269_b200 as cd
+
+    return cd
+
+
+@pytest.fixture(scope="module")
+def c4_run(cuda_ready):
+    import torch
+
+    cd = _cd()
+    m, d, inter = C4["m"], C4["d"], C4["inter"]
+    dev = torch.device("cuda", 0)
+    P = cd.PrecisionMode.SIMBF16
+    g = torch.Generator(device=dev).manual_seed(123)
+
+    def mat(r, c, scale):
+        t = cd.tensors.alloc_matrix(r, c, torch.bfloat16, dev)
+        t.copy_(torch.randn((r, c), generator=g, device=dev) * scale)
+        return cd.DenseMatrix.from_tensor(t, P)
+
+    f = 2 * inter
+    w = cd.LayerWeights(w_out=mat(d, d, 0.02), gamma_ffn=cd.Vector.from_tensor(1 + 0.1 * torch.randn(d, generator=g,
+                        device=dev), P), w_gate_up=mat(d, f, 0.02), w_down=mat(inter, d, 0.02),
+                        gamma_qkv=cd.Vector.from_tensor(1 + 0.1 * torch.randn(d, generator=g, device=dev), P),
+                        w_qkv=mat(d, 3 * d, 0.02))
+    x, z, gq, gr = mat(m, d, 1), mat(m, d, 1), mat(m, 3 * d, 1), mat(m, d, 1)
+    cos, sin = cd.qkv_rope_tables(m, d, precision=P)
+    cfg = cd.PipelineConfig(hidden=d, ffn=f, precision=P)
+    fwd = cd.layer_forward(x, z, w, cos, sin, config=cfg)
+    bwd = cd.layer_backward(gq, fwd.tape, w, grad_residual=gr, config=cfg)
+    torch.cuda.synchronize()
+    return dict(cd=cd, w=w, x=x, z=z, gq=gq, gr=gr, cos=cos, sin=sin, fwd=fwd, bwd=bwd, cfg=cfg)
+
+
+def test_c4_row_subset_vs_oracle(c4_run):
+    """Row-local outputs of the full 16384-token block equal the oracle on 24 sampled rows."""
+    import torch
+
+    r = c4_run
+    m, d = C4["m"], C4["d"]
+    rows = np.sort(np.random.default_rng(5).choice(m, size=24, replace=False))
+    idx = torch.as_tensor(rows, device="cuda")
+    take = lambda mat: mat.tensor.index_select(0, idx).double().cpu().numpy()  # noqa: E731
+    host = lambda mat: mat.tensor.double().cpu().numpy()  # noqa: E731
+    w = {k: host(getattr(r["w"], k)) for k in ("w_out", "w_gate_up", "w_down", "w_qkv")}
+    w["gamma_ffn"] = r["w"].gamma_ffn.tensor.double().cpu().numpy()
+    w["gamma_qkv"] = r["w"].gamma_qkv.tensor.double().cpu().numpy()
+    mode = O.SIMBF16
+    of = O.layer_forward(take(r["x"]), take(r["z"]), w, take(r["cos"]), take(r["sin"]), mode)
+    errs = {"qkv": O.rel_error(take(r["fwd"].qkv), of["qkv"]),
+            "residual": O.rel_error(take(r["fwd"].residual), of["residual"])}
+    ob = O.layer_backward(take(r["gq"]), of, w, mode, grad_residual=take(r["gr"]))
+    errs["x"] = O.rel_error(take(r["bwd"].x), ob["x"])
+    errs["z"] = O.rel_error(take(r["bwd"].z), ob["z"])
+    print("\n[C4 row subset] " + ", ".join(f"{k}={v:.2e}" for k, v in errs.items()))
+    assert max(errs.values()) <= 2e-2, errs
+
+
+@pytest.mark.parametrize("shape", [(4096, 12288), (14336, 4096), (4096, 28672), (4096, 4096)])
+def test_c4_wgrad_checksum(cuda_ready, shape):
+    """dW = A^T B at the block's full wgrad shapes (K = 16384 tokens): dW u == A^T (B u)."""
+    import torch
+
+    cd = _cd()
+    P = cd.PrecisionMode.SIMBF16
+    mdim, ndim = shape
+    k = C4["m"]
+    g = torch.Generator(device="cuda").manual_seed(mdim * 7 + ndim)
+    A = torch.randn((k, mdim), generator=g, device="cuda").to(torch.bfloat16)
+    B = torch.randn((k, ndim), generator=g, device="cuda").to(torch.bfloat16)
+    prob = cd.GemmProblem(m=mdim, n=ndim, k=k, trans_a=True, precision=P)
+    dW = cd.run_gemm(prob, cd.DenseMatrix.from_tensor(A, P), cd.DenseMatrix.from_tensor(B, P)).main.tensor
+    u = torch.randn(ndim, generator=g, device="cuda", dtype=torch.float64)
+    lhs = dW.double() @ u
+    rhs = A.double().t() @ (B.double() @ u)
+    err = float((lhs - rhs).norm() / rhs.norm())
+    assert err < 2e-2, err
+
+
+def test_c4_gain_gradient_checksum(c4_run):
+    """dγ_ffn equals colsum(D * c_n) recomputed in float64 from the GPU's own K9a operands."""
+    import torch
+
+    r = c4_run
+    cd = r["cd"]
+    tape, w, bwd = r["fwd"].tape, r["w"], r["bwd"]
+    # D = grad_za @ w_gate_up^T is the K9a GEMM; rebuild grad_za with the GPU's K10 launch
+    k10 = cd.gemm_swiglu_backward(bwd_grad_h1b(r), w.w_down, tape.preact, trans_b=True,
+                                  precision=cd.PrecisionMode.SIMBF16)
+    D = k10.main.tensor.double() @ w.w_gate_up.tensor.double().t()
+    cn = tape.pre_norm_a.tensor.double() * tape.inv_rms_a.tensor.double()[:, None]
+    ref = (D * cn).sum(dim=0)
+    got = bwd.gamma_ffn.tensor.double()
+    err = float((got - ref).norm() / ref.norm())
+    assert err < 2e-2, err
+
+
+def bwd_grad_h1b(r):
+    """grad_h1b = z-gradient minus the skip term: grad_h1a = K9a(...) + grad_h1b, so use K9b directly."""
+    cd = r["cd"]
+    tape, w = r["fwd"].tape, r["w"]
+    gz, rd = cd.rope_backward_stat(r["gq"], tape.qkv, tape.cos, tape.sin, precision=cd.PrecisionMode.SIMBF16)
+    s_b = cd.finalize_rowdot(rd, C4["d"])
+    k9b = cd.gemm_rmsnorm_backward(gz, w.w_qkv, tape.pre_norm_b, tape.inv_rms_b, w.gamma_qkv, s_b,
+                                   grad_in=r["gr"], trans_b=True, precision=cd.PrecisionMode.SIMBF16)
+    return k9b.main
