@@ -191,6 +191,11 @@ int coda_split_operand(const coda_tensor_t* src, int k_axis, int64_t kp,
  * allreduce of weight gradients so rounding happens once (engine.py:443-447). */
 int coda_convert_f32_bf16(const coda_tensor_t* src, coda_tensor_t* dst, void* stream);
 
+/* Engine options (defaults from the environment): "pdl" 0/1 programmatic
+ * dependent launch, "cg" 1/2 CTA-pair mainloop, "generic" 0/1 force the generic
+ * epilogue interpreter, "raster" >= 1 raster group.  Process-wide. */
+int coda_set_option(const char* name, int value);
+
 /* Number of SMs the persistent kernel sizes its grid for (0 if no device). */
 int coda_num_sms(void);
 

@@ -55,6 +55,7 @@ EXPORTS = (
     "coda_split_operand",
     "coda_convert_f32_bf16",
     "coda_num_sms",
+    "coda_set_option",
     "coda_version",
     "coda_last_error",
 )
@@ -138,6 +139,7 @@ def _declare(lib) -> None:
     lib.coda_split_operand.argtypes = [P(Tensor), i32, i64, P(ctypes.c_int32), P(Tensor), vp]
     lib.coda_convert_f32_bf16.argtypes = [P(Tensor), P(Tensor), vp]
     lib.coda_num_sms.argtypes = []
+    lib.coda_set_option.argtypes = [ctypes.c_char_p, i32]
     lib.coda_version.argtypes = []
     lib.coda_version.restype = ctypes.c_char_p
     lib.coda_last_error.argtypes = []
@@ -199,6 +201,11 @@ def call(name: str, *args, tag: str | None = None, flops: float = 0.0) -> None:
     else:
         check(getattr(lib, name)(*args))
     _launches += 1
+
+
+def set_option(name: str, value: int) -> None:
+    """Process-wide engine option ("pdl", "cg", "generic", "raster"); see include/coda.h."""
+    check(load().coda_set_option(name.encode(), int(value)))
 
 
 def launch_count() -> int:

@@ -166,13 +166,26 @@ int num_sms() {
 }
 
 // ---------------------------------------------------------------- launches (PDL + clusters)
-bool pdl_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("CODA_PDL");
-        return !(e && e[0] == '0');
-    }();
-    return on;
+// Runtime options (environment defaults, overridable through coda_set_option so
+// variants can be compared interleaved inside one process).
+struct Options {
+    int pdl = 1;          // programmatic dependent launch
+    int cg = 2;           // CTA-pair (2) or single-CTA (1) specialised kernels
+    int generic = 0;      // force the generic epilogue interpreter
+    int raster = 8;       // raster group (pair m-tiles)
+    Options() {
+        if (const char* e = getenv("CODA_PDL")) pdl = e[0] != '0';
+        if (const char* e = getenv("CODA_CG")) cg = e[0] == '1' ? 1 : 2;
+        if (const char* e = getenv("CODA_FORCE_GENERIC")) generic = e[0] && e[0] != '0';
+        if (const char* e = getenv("CODA_RASTER_GROUP")) { const int g = atoi(e); if (g > 0) raster = g; }
+    }
+};
+Options& opts() {
+    static Options o;
+    return o;
 }
+
+bool pdl_enabled() { return opts().pdl != 0; }
 
 // Launch with programmatic stream serialization (kernel N+1's prologue overlaps
 // kernel N's tail; every kernel calls griddep_wait() before touching global
@@ -281,13 +294,7 @@ int launch_fast_fl(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorM
                       ma, mb, mm, mx, P);
 }
 
-int fast_cg() {
-    static const int cg = [] {
-        const char* e = getenv("CODA_CG");
-        return (e && e[0] == '1') ? 1 : 2;
-    }();
-    return cg;
-}
+int fast_cg() { return opts().cg; }
 
 bool fast_supported(int fl) {
 #define CODA_FAST_CASE(F) if (fl == (F)) return true;
@@ -313,11 +320,7 @@ int launch_fast(int fl, int cg, const CUtensorMap& ma, const CUtensorMap& mb, co
 int raster_group(int ntm, int tile_m, int64_t k) {
     (void)tile_m;
     (void)k;
-    static const int forced = [] {
-        const char* e = getenv("CODA_RASTER_GROUP");
-        return e ? atoi(e) : 0;
-    }();
-    int g = forced > 0 ? forced : 8;
+    int g = opts().raster;
     if (g < 1) g = 1;
     if (g > ntm) g = ntm;
     return g;
@@ -325,11 +328,7 @@ int raster_group(int ntm, int tile_m, int64_t k) {
 
 // Map a validated program onto the flag set of a specialised kernel (or -1).
 int match_fast(const coda_problem_t* pr, const coda_step_t* steps, int nsteps, const coda_store_t* stores) {
-    static const bool force_generic = [] {
-        const char* e = getenv("CODA_FORCE_GENERIC");
-        return e && e[0] && e[0] != '0';
-    }();
-    if (force_generic || pr->storage != CODA_BF16) return -1;
+    if (opts().generic || pr->storage != CODA_BF16) return -1;
     int fl = 0, last_rank = 0;
     auto rank_ok = [&](int rk) {
         if (rk <= last_rank) return false;
@@ -381,6 +380,21 @@ const char* coda_last_error(void) { return g_err.c_str(); }
 const char* coda_version(void) { return "coda sm_100a tcgen05 128x256x64 4-stage persistent"; }
 
 int coda_num_sms(void) { return num_sms(); }
+
+int coda_set_option(const char* name, int value) {
+    if (!name) return fail(CODA_E_BINDING, "null option name");
+    const std::string n(name);
+    if (n == "pdl") opts().pdl = value != 0;
+    else if (n == "cg") {
+        if (value != 1 && value != 2) return fail(CODA_E_CONFIG, "cg must be 1 or 2");
+        opts().cg = value;
+    } else if (n == "generic") opts().generic = value != 0;
+    else if (n == "raster") {
+        if (value < 1) return fail(CODA_E_CONFIG, "raster group must be >= 1");
+        opts().raster = value;
+    } else return fail(CODA_E_CONFIG, "unknown option %s", name);
+    return CODA_OK;
+}
 
 int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const coda_tensor_t* b,
                        const coda_step_t* steps, int nsteps, const coda_tensor_t* operands, int noperands,
