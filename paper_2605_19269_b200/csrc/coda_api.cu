@@ -275,9 +275,9 @@ using coda::F_SWIGLU_BWD;
 
 template <int FL, int CG>
 int launch_fast_fl(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mm, const CUtensorMap& mx,
-                   const coda::FastParams& P, cudaStream_t st) {
+                   const CUtensorMap& s0, const CUtensorMap& s1, const coda::FastParams& P, cudaStream_t st) {
     static bool configured = false;
-    const size_t smem = coda::fast_smem_bytes<CG>();
+    const size_t smem = coda::fast_smem_bytes<CG, FL>();
     auto kern = coda::coda_gemm_fast<__nv_bfloat16, FL, CG>;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -291,7 +291,7 @@ int launch_fast_fl(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorM
     const int units = num_sms() / CG;
     const int grid = (P.mp.ntiles < units ? P.mp.ntiles : units) * CG;
     return launch_pdl(kern, dim3((unsigned)grid), dim3(coda::FAST_THREADS), smem, st, CG, "coda_gemm_fast launch",
-                      ma, mb, mm, mx, P);
+                      ma, mb, mm, mx, s0, s1, P);
 }
 
 int fast_cg() { return opts().cg; }
@@ -304,11 +304,12 @@ bool fast_supported(int fl) {
 }
 
 int launch_fast(int fl, int cg, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mm,
-                const CUtensorMap& mx, const coda::FastParams& P, cudaStream_t st) {
+                const CUtensorMap& mx, const CUtensorMap& s0, const CUtensorMap& s1, const coda::FastParams& P,
+                cudaStream_t st) {
 #define CODA_FAST_CASE(F)                                                         \
     if (fl == (F))                                                                \
-        return cg == 2 ? launch_fast_fl<(F), 2>(ma, mb, mm, mx, P, st)            \
-                       : launch_fast_fl<(F), 1>(ma, mb, mm, mx, P, st);
+        return cg == 2 ? launch_fast_fl<(F), 2>(ma, mb, mm, mx, s0, s1, P, st)    \
+                       : launch_fast_fl<(F), 1>(ma, mb, mm, mx, s0, s1, P, st);
     CODA_FAST_SETS(CODA_FAST_CASE)
 #undef CODA_FAST_CASE
     return fail(CODA_E_CONFIG, "no specialised kernel for flags 0x%x", fl);
@@ -606,7 +607,26 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
             rc = make_map(&mb, b->ptr, (uint64_t)K, (uint64_t)N, (uint64_t)b->ld * 2, coda::BK, coda::BN / 2);
             if (rc) return rc;
         }
-        return launch_fast(fl, cg, ma, mb, mm, mx, F, st);
+        // side-operand maps: 32-row boxes of one 32-column chunk (preact: 64 columns)
+        CUtensorMap s0, s1;
+        memset(&s0, 0, sizeof(s0));
+        memset(&s1, 0, sizeof(s1));
+        auto side_map = [&](CUtensorMap* out, const void* ptr, int64_t ld, int64_t cols, int box_cols) {
+            return make_map(out, ptr, (uint64_t)cols, (uint64_t)M, (uint64_t)ld * 2, (uint32_t)box_cols, 32u,
+                            CODA_BF16, box_cols * 2);
+        };
+        if (fl & F_RESIDUAL) rc = side_map(&s0, F.residual, F.ld_res, N, 32);
+        if (!rc && (fl & F_ROPE)) {
+            rc = side_map(&s0, F.cosp, F.ld_cos, N, 32);
+            if (!rc) rc = side_map(&s1, F.sinp, F.ld_sin, N, 32);
+        }
+        if (!rc && (fl & F_SWIGLU_BWD)) rc = side_map(&s0, F.preact2, F.ld_pre2, 2 * N, 64);
+        if (!rc && (fl & F_RMSBWD)) {
+            rc = side_map(&s0, F.pre, F.ld_pre, N, 32);
+            if (!rc && (fl & F_RMSBWD_ACC)) rc = side_map(&s1, F.grad_in, F.ld_gin, N, 32);
+        }
+        if (rc) return rc;
+        return launch_fast(fl, cg, ma, mb, mm, mx, s0, s1, F, st);
     }
     if (sdt == CODA_BF16) return launch_gemm<__nv_bfloat16>(ma, mb, P, st);
     return launch_gemm<float>(ma, mb, P, st);

@@ -83,10 +83,47 @@ struct FastParams {
     float* target;
 };
 
-template <int CG>
+// Side operands (residual, cos/sin, preact, pre_norm/grad_in) are TMA-loaded per
+// epilogue warp into a 4 KiB swizzled buffer, one 32-row chunk ahead; kernels that
+// have them give up one ring stage for the buffers.
+constexpr int F_SIDE = F_RESIDUAL | F_ROPE | F_SWIGLU_BWD | F_RMSBWD;
+constexpr int SIDE_BYTES = 4096;
+
+template <int CG, int FL>
+struct FastGeom {
+    static constexpr bool SIDE = (FL & F_SIDE) != 0;
+    static constexpr int NS = Geom<CG>::NSTAGE - (SIDE ? 1 : 0);
+    static constexpr int RING = NS * Geom<CG>::STAGE;
+    static constexpr int SIDE_TOTAL = SIDE ? FAST_EPI_WARPS * SIDE_BYTES : 0;
+    // bytes one chunk's side loads deliver to a warp (32 rows)
+    static constexpr int CHUNK_BYTES = (FL & F_SWIGLU_BWD) ? 4096
+                                     : (FL & F_ROPE) ? 4096
+                                     : (FL & F_RMSBWD) ? ((FL & F_RMSBWD_ACC) ? 4096 : 2048)
+                                     : (FL & F_RESIDUAL) ? 2048 : 0;
+};
+
+template <int CG, int FL>
 constexpr size_t fast_smem_bytes() {
-    return (size_t)Geom<CG>::RING + (size_t)FAST_EPI_WARPS * STG_BYTES + COLRED_BYTES +
-           (2 * Geom<CG>::NSTAGE + 4) * 8 + 16;
+    using FG = FastGeom<CG, FL>;
+    return (size_t)FG::RING + (size_t)FAST_EPI_WARPS * STG_BYTES + FG::SIDE_TOTAL + COLRED_BYTES +
+           (2 * FG::NS + 4 + FAST_EPI_WARPS) * 8 + 16;
+}
+
+// One thread's row of a 32-row side box: RB bytes (64: SWIZZLE_64B, 128: SWIZZLE_128B) of bf16.
+template <int RB>
+__device__ __forceinline__ void side_row(uint32_t base, int r, float* out) {
+    constexpr uint32_t MASK = RB == 128 ? 0x70u : 0x30u;
+#pragma unroll
+    for (int c = 0; c < RB / 16; ++c) {
+        const uint32_t off = (uint32_t)(r * RB + c * 16);
+        uint32_t w[4];
+        ld_shared_v4(base + (off ^ ((off >> 3) & MASK)), w[0], w[1], w[2], w[3]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            out[c * 8 + 2 * i] = __uint_as_float(w[i] << 16);
+            out[c * 8 + 2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+        }
+    }
 }
 
 // -------------------------------------------------------------- row-segment loads
@@ -217,18 +254,23 @@ template <typename TS, int FL, int CG>
 __global__ void __launch_bounds__(FAST_THREADS, 1)
 coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                const __grid_constant__ CUtensorMap tma_main, const __grid_constant__ CUtensorMap tma_aux,
+               const __grid_constant__ CUtensorMap tma_s0, const __grid_constant__ CUtensorMap tma_s1,
                const __grid_constant__ FastParams P) {
     using G = Geom<CG>;
+    using FG = FastGeom<CG, FL>;
+    constexpr int NS = FG::NS;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sA = smem;
-    uint8_t* sB = smem + G::NSTAGE * G::A_BYTES;
-    uint8_t* stg = smem + G::RING;
-    float* colred = reinterpret_cast<float*>(stg + FAST_EPI_WARPS * STG_BYTES);
+    uint8_t* sB = smem + NS * G::A_BYTES;
+    uint8_t* stg = smem + FG::RING;
+    uint8_t* side = stg + FAST_EPI_WARPS * STG_BYTES;
+    float* colred = reinterpret_cast<float*>(side + FG::SIDE_TOTAL);
     uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(colred) + COLRED_BYTES);
-    uint64_t* empty = full + G::NSTAGE;
-    uint64_t* tfull = empty + G::NSTAGE;
+    uint64_t* empty = full + NS;
+    uint64_t* tfull = empty + NS;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* sidebar = tempty + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sidebar + FAST_EPI_WARPS);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -239,7 +281,7 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
 
     if (threadIdx.x == 0) {
         if (smem_u32(smem) & 1023u) __trap();   // swizzled TMA buffers need 1 KiB alignment
-        for (int s = 0; s < G::NSTAGE; ++s) {
+        for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -247,11 +289,16 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], FAST_EPI_WARPS * CG);   // one arrival per epilogue warp of the pair
         }
+        for (int s = 0; s < FAST_EPI_WARPS; ++s) mbar_init(&sidebar[s], 1);
         fence_mbar_init();
         tma_prefetch_desc(&tma_a);
         tma_prefetch_desc(&tma_b);
         if (FL & F_STORE_MAIN) tma_prefetch_desc(&tma_main);
         if (FL & (F_AUX | F_SWIGLU_BWD | F_RMSBWD)) tma_prefetch_desc(&tma_aux);
+        if (FG::SIDE) {
+            tma_prefetch_desc(&tma_s0);
+            if (FL & (F_ROPE | F_RMSBWD_ACC)) tma_prefetch_desc(&tma_s1);
+        }
     }
     if (warp == 1) {
         if constexpr (CG == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
@@ -268,9 +315,9 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     griddep_wait();
 
     if (warp == 0) {
-        if (lane == 0) producer_loop<CG>(mp, &tma_a, &tma_b, sA, sB, full, empty, rank, unit, nunits);
+        if (lane == 0) producer_loop<CG, NS>(mp, &tma_a, &tma_b, sA, sB, full, empty, rank, unit, nunits);
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) mma_loop<CG>(mp, tmem_base, sA, sB, full, empty, tfull, tempty, unit, nunits);
+        if (lane == 0 && rank == 0) mma_loop<CG, NS>(mp, tmem_base, sA, sB, full, empty, tfull, tempty, unit, nunits);
     } else {
         const int ew = warp - 2;            // 0..7
         const int q = warp & 3;             // TMEM lane quadrant
@@ -281,6 +328,24 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         int cbuf = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
+        const uint32_t sbase = smem_u32(side + ew * SIDE_BYTES);
+        uint32_t side_phase = 0;
+        // lane 0: TMA-load the side operands of chunk c of tile t into this warp's buffer
+        auto side_issue = [&](int t_, int c_) {
+            int tm_, tn_;
+            tile_coord(mp, t_, tm_, tn_);
+            const int y = tm_ * G::TILE_M + rank * BM + q * 32;
+            const int x = tn_ * BN + h * 128 + c_ * 32;
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&sidebar[ew], FG::CHUNK_BYTES);
+            if (FL & F_SWIGLU_BWD) {
+                tma_load_2d(sbase, &tma_s0, 2 * x, y, &sidebar[ew]);
+            } else {
+                tma_load_2d(sbase, &tma_s0, x, y, &sidebar[ew]);
+                if (FL & (F_ROPE | F_RMSBWD_ACC)) tma_load_2d(sbase + 2048, &tma_s1, x, y, &sidebar[ew]);
+            }
+        };
+        if (FG::SIDE && lane == 0 && unit < mp.ntiles) side_issue(unit, 0);
         for (int t = unit; t < mp.ntiles; t += nunits) {
             int tm, tn;
             tile_coord(mp, t, tm, tn);
@@ -318,6 +383,22 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         else mbar_arrive_leader(&tempty[acc]);
                     }
                 }
+                // side operands of this chunk: wait for the TMA load, pull this thread's row
+                // into registers, then reuse the buffer for the next chunk's load
+                float sd0[FG::SIDE ? ((FL & F_SWIGLU_BWD) ? 64 : 32) : 1];
+                float sd1[(FL & (F_ROPE | F_RMSBWD_ACC)) ? 32 : 1];
+                if constexpr (FG::SIDE) {
+                    mbar_wait(&sidebar[ew], side_phase);
+                    side_phase ^= 1;
+                    if constexpr ((FL & F_SWIGLU_BWD) != 0) side_row<128>(sbase, lane, sd0);
+                    else side_row<64>(sbase, lane, sd0);
+                    if constexpr ((FL & (F_ROPE | F_RMSBWD_ACC)) != 0) side_row<64>(sbase + 2048, lane, sd1);
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (c < 3) side_issue(t, c + 1);
+                        else if (t + nunits < mp.ntiles) side_issue(t + nunits, 0);
+                    }
+                }
                 const int gcol0 = n0 + h * 128 + c * 32;
                 if (gcol0 >= N) continue;   // uniform for the 4 warps of this half
                 const bool edge = gcol0 + 32 > N;
@@ -331,11 +412,9 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] *= rsc;
                 }
-                if (FL & F_RESIDUAL) {
-                    float x[32];
-                    fload<TS, 32>(static_cast<const TS*>(P.residual) + row * P.ld_res, gcol0, N, row_ok, x);
+                if constexpr ((FL & F_RESIDUAL) != 0) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] += x[i];
+                    for (int i = 0; i < 32; ++i) v[i] += sd0[i];
                 }
                 if (FL & F_AUX) staged_store<TS, 32>(sg, &tma_aux, gcol0, m0 + q * 32, v, lane);
                 if (FL & F_SUMSQ) {
@@ -356,10 +435,9 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] *= g[i];
                 }
-                if (FL & F_ROPE) {
-                    float cs[32], sn[32];
-                    fload<TS, 32>(static_cast<const TS*>(P.cosp) + row * P.ld_cos, gcol0, N, row_ok, cs);
-                    fload<TS, 32>(static_cast<const TS*>(P.sinp) + row * P.ld_sin, gcol0, N, row_ok, sn);
+                if constexpr ((FL & F_ROPE) != 0) {
+                    const float* cs = sd0;
+                    const float* sn = sd1;
 #pragma unroll
                     for (int k = 0; k < 16; ++k) {
                         const float x0 = v[2 * k], x1 = v[2 * k + 1];
@@ -410,9 +488,7 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     }
                     if (FL & F_STORE_MAIN) staged_store<TS, 16>(sg, &tma_main, gcol0 / 2, m0 + q * 32, v, lane);
                 } else if (FL & F_SWIGLU_BWD) {
-                    float z[64];
-                    fload<TS, 64>(static_cast<const TS*>(P.preact2) + row * P.ld_pre2, 2 * (int64_t)gcol0,
-                                  2 * (int64_t)N, row_ok, z);
+                    const float* z = sd0;
                     float rec[32];
                     float s = 0.0f;
                     float o[64];
@@ -439,8 +515,8 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     pacc += s;
                     if (FL & F_STORE_MAIN) staged_store<TS, 64>(sg, &tma_main, 2 * gcol0, m0 + q * 32, o, lane);
                 } else if (FL & F_RMSBWD) {
-                    float cp[32], g[32], tmp[32];
-                    fload<TS, 32>(static_cast<const TS*>(P.pre) + row * P.ld_pre, gcol0, N, row_ok, cp);
+                    float g[32], tmp[32];
+                    float* cp = sd0;
                     fload_vec<32>(P.gamma, gcol0, N, g);
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
@@ -478,11 +554,9 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     cbuf ^= 1;
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = (v[i] * g[i] - cp[i] * ss) * rr;
-                    if (FL & F_RMSBWD_ACC) {
-                        float x[32];
-                        fload<TS, 32>(static_cast<const TS*>(P.grad_in) + row * P.ld_gin, gcol0, N, row_ok, x);
+                    if constexpr ((FL & F_RMSBWD_ACC) != 0) {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) v[i] += x[i];
+                        for (int i = 0; i < 32; ++i) v[i] += sd1[i];
                     }
                     if (FL & F_STORE_MAIN) staged_store<TS, 32>(sg, &tma_main, gcol0, m0 + q * 32, v, lane);
                 } else if (FL & F_STORE_MAIN) {

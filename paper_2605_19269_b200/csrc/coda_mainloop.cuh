@@ -57,7 +57,7 @@ __device__ __forceinline__ void tile_coord(const MainParams& mp, int t, int& tm,
 }
 
 // TMA producer (one thread per CTA): fills this CTA's smem ring for every tile it owns.
-template <int CG>
+template <int CG, int NS = Geom<CG>::NSTAGE>
 __device__ __forceinline__ void producer_loop(const MainParams& mp, const CUtensorMap* tma_a,
                                               const CUtensorMap* tma_b, uint8_t* sA, uint8_t* sB,
                                               uint64_t* full, uint64_t* empty, int rank, int unit, int nunits) {
@@ -91,7 +91,7 @@ __device__ __forceinline__ void producer_loop(const MainParams& mp, const CUtens
 #pragma unroll
                 for (int b = 0; b < G::B_COLS / 64; ++b) load(sb + b * (BK * 128), tma_b, nb0 + 64 * b, k0);
             }
-            if (++stage == G::NSTAGE) { stage = 0; phase ^= 1; }
+            if (++stage == NS) { stage = 0; phase ^= 1; }
         }
     }
 }
@@ -99,7 +99,7 @@ __device__ __forceinline__ void producer_loop(const MainParams& mp, const CUtens
 // MMA issuer (one thread; for CG = 2 only in the leader CTA): 4 x tcgen05.mma
 // (K = 16 each) per k-block into the current TMEM accumulator; commits free smem
 // stages and publish finished accumulators.
-template <int CG>
+template <int CG, int NS = Geom<CG>::NSTAGE>
 __device__ __forceinline__ void mma_loop(const MainParams& mp, uint32_t tmem_base, uint8_t* sA, uint8_t* sB,
                                          uint64_t* full, uint64_t* empty, uint64_t* tfull, uint64_t* tempty,
                                          int unit, int nunits) {
@@ -135,7 +135,7 @@ __device__ __forceinline__ void mma_loop(const MainParams& mp, uint32_t tmem_bas
             }
             if constexpr (CG == 1) umma_commit(&empty[stage]);
             else umma_commit_pair(&empty[stage]);
-            if (++stage == G::NSTAGE) { stage = 0; phase ^= 1; }
+            if (++stage == NS) { stage = 0; phase ^= 1; }
         }
         if constexpr (CG == 1) umma_commit(&tfull[acc]);
         else umma_commit_pair(&tfull[acc]);
