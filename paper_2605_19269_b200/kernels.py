@@ -509,7 +509,9 @@ def layer_backward(grad_qkv: DenseMatrix, tape: LayerTape, weights: LayerWeights
     epilogues.  `wgrad_hook` (B200 extension for token-sharded data
     parallelism) receives each weight gradient as an unrounded float32
     tensor right after its GEMM is enqueued, in production order, and must
-    leave the reduced sum in place; rounding to storage happens once after.
+    leave the reduced sum in place; if the hook has a `wait()` (asynchronous
+    reduction on another stream) it is called before the single rounding to
+    storage at the end.
     """
     weights.check(config)
     tape.check(config)
@@ -554,6 +556,10 @@ def layer_backward(grad_qkv: DenseMatrix, tape: LayerTape, weights: LayerWeights
     g_wout = wgrad("w_out", tape.x, grad_h1a)
 
     if f32:
+        # the reduced sums must be complete before their single rounding to storage
+        wait = getattr(wgrad_hook, "wait", None)
+        if wait is not None:
+            wait()
         g_wqkv, g_wdown, g_wgu, g_wout = (to_storage(g, prec) for g in (g_wqkv, g_wdown, g_wgu, g_wout))
     return LayerGrads(x=grad_x, z=grad_h1a, w_out=g_wout, gamma_ffn=g_gffn, w_gate_up=g_wgu, w_down=g_wdown,
                       gamma_qkv=g_gqkv, w_qkv=g_wqkv, ledger=ledger)

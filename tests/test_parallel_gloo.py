@@ -96,3 +96,13 @@ def test_shard_bounds():
     assert [(s.start, s.stop) for s in (parallel.shard(10, r, 3) for r in range(3))] == [(0, 4), (4, 7), (7, 10)]
     assert parallel.shard(16384, 3, 8).rows == 2048
     assert parallel.shard(8192, 2, 8, "weak").start == 16384
+
+
+def test_layer_backward_waits_for_async_reduction_before_rounding():
+    """layer_backward must call hook.wait() before rounding the reduced f32 wgrads (no stream race)."""
+    import inspect
+
+    from paper_2605_19269_b200 import kernels
+
+    src = inspect.getsource(kernels.layer_backward)
+    assert src.index("wait()") < src.index("to_storage(g, prec)")
