@@ -150,7 +150,24 @@ def kat_case():
          layout=np.array([b.width for b in tf.row_block_layout(10, 4, 3)]))
 
 
+def codt_case():
+    """Containers written by the reference's codt.write_tensor, plus their values."""
+    from tilefuse.codt import write_tensor
+
+    rng = np.random.default_rng(9)
+    vals = {}
+    for tag, mode in MODES.items():
+        m = tf.DenseMatrix.from_array(rng.standard_normal((5, 9)), mode)
+        write_tensor(OUT / f"ref_{tag}_matrix.codt", m)
+        vals[f"{tag}_matrix"] = m.data
+        v = tf.Vector.from_array(np.linspace(-3, 3, 11), mode)
+        write_tensor(OUT / f"ref_{tag}_vector.codt", v)
+        vals[f"{tag}_vector"] = v.data
+    np.savez_compressed(OUT / "codt_values.npz", **vals)
+
+
 if __name__ == "__main__":
+    codt_case()
     kat_case()
     for mode in ("sim32", "simbf16", "exact64"):
         kernels_case("ragged", mode, m=37, k=45, n=50, tile=(16, 24), rtn=10, seed=11)
