@@ -85,6 +85,13 @@ typedef struct {
     int32_t out_dtype;     /* dtype of the main output */
     int32_t store_main;    /* engine.py:428-430 */
     int32_t _pad;
+    /* Optional caller-owned scratch for wave-tail splitting (split-K of the last,
+     * partial wave; deterministic fixed-order fold).  The first 64 KiB hold int32
+     * flags that must be zero before the first launch (the kernels leave them
+     * zero); the rest holds f32 partial tiles.  NULL / 0 disables splitting.
+     * Launches sharing one workspace must be stream-ordered. */
+    void*   workspace;
+    int64_t workspace_bytes;
 } coda_problem_t;
 
 /* One program step (EpilogueProgram.steps, epilogue.py:606-698).

@@ -83,6 +83,8 @@ class Problem(ctypes.Structure):
         ("out_dtype", ctypes.c_int32),
         ("store_main", ctypes.c_int32),
         ("_pad", ctypes.c_int32),
+        ("workspace", ctypes.c_void_p),
+        ("workspace_bytes", ctypes.c_int64),
     ]
 
 
@@ -206,6 +208,22 @@ def call(name: str, *args, tag: str | None = None, flops: float = 0.0) -> None:
 def set_option(name: str, value: int) -> None:
     """Process-wide engine option ("pdl", "cg", "generic", "raster"); see include/coda.h."""
     check(load().coda_set_option(name.encode(), int(value)))
+
+
+WORKSPACE_BYTES = 96 << 20
+_workspaces: dict = {}
+
+
+def workspace(device):
+    """Per-device zeroed scratch for wave-tail splitting (flags stay zero between launches)."""
+    import torch
+
+    key = str(device)
+    ws = _workspaces.get(key)
+    if ws is None:
+        ws = torch.zeros(WORKSPACE_BYTES // 4, dtype=torch.int32, device=device)
+        _workspaces[key] = ws
+    return ws
 
 
 def launch_count() -> int:

@@ -173,11 +173,13 @@ struct Options {
     int cg = 2;           // CTA-pair (2) or single-CTA (1) specialised kernels
     int generic = 0;      // force the generic epilogue interpreter
     int raster = 8;       // raster group (pair m-tiles)
+    int split = 1;        // split the partial last wave along K
     Options() {
         if (const char* e = getenv("CODA_PDL")) pdl = e[0] != '0';
         if (const char* e = getenv("CODA_CG")) cg = e[0] == '1' ? 1 : 2;
         if (const char* e = getenv("CODA_FORCE_GENERIC")) generic = e[0] && e[0] != '0';
         if (const char* e = getenv("CODA_RASTER_GROUP")) { const int g = atoi(e); if (g > 0) raster = g; }
+        if (const char* e = getenv("CODA_SPLIT")) split = e[0] != '0';
     }
 };
 Options& opts() {
@@ -289,7 +291,7 @@ int launch_fast_fl(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorM
         configured = true;
     }
     const int units = num_sms() / CG;
-    const int grid = (P.mp.ntiles < units ? P.mp.ntiles : units) * CG;
+    const int grid = (P.mp.nitems < units ? P.mp.nitems : units) * CG;
     return launch_pdl(kern, dim3((unsigned)grid), dim3(coda::FAST_THREADS), smem, st, CG, "coda_gemm_fast launch",
                       ma, mb, mm, mx, s0, s1, P);
 }
@@ -390,6 +392,7 @@ int coda_set_option(const char* name, int value) {
         if (value != 1 && value != 2) return fail(CODA_E_CONFIG, "cg must be 1 or 2");
         opts().cg = value;
     } else if (n == "generic") opts().generic = value != 0;
+    else if (n == "split") opts().split = value != 0;
     else if (n == "raster") {
         if (value < 1) return fail(CODA_E_CONFIG, "raster group must be >= 1");
         opts().raster = value;
@@ -541,8 +544,29 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         memset(&F, 0, sizeof(F));
         const int tile_m = coda::BM * cg;
         const int ntm = (int)((M + tile_m - 1) / tile_m);
-        F.mp = coda::MainParams{P.M, P.N, P.K, ntm, P.ntn, P.nk, ntm * P.ntn, P.a_mn, P.b_mn,
-                                raster_group(ntm, tile_m, K)};
+        const int ntiles = ntm * P.ntn;
+        F.mp = coda::MainParams{P.M, P.N, P.K, ntm, P.ntn, P.nk, ntiles, P.a_mn, P.b_mn,
+                                raster_group(ntm, tile_m, K), ntiles, 0, 1, ntiles};
+        // wave-tail split: the r tiles of the partial last wave run as s K-pieces each
+        const int units = num_sms() / cg;
+        const int r = units > 0 ? ntiles % units : 0;
+        if (opts().split && r > 0 && pr->workspace && pr->workspace_bytes > (64 << 10)) {
+            int sp = units / r;
+            if (sp > P.nk / 4) sp = P.nk / 4;
+            if (sp > 16) sp = 16;
+            const int64_t tile_bytes = (int64_t)cg * coda::BM * coda::BN * 4;
+            while (sp >= 2 && ((int64_t)r * (sp - 1) * tile_bytes > pr->workspace_bytes - (64 << 10) ||
+                               (int64_t)r * (sp - 1) * cg * coda::FAST_EPI_WARPS * 4 > (64 << 10)))
+                --sp;
+            if (sp >= 2) {
+                F.mp.full_tiles = ntiles - r;
+                F.mp.tail = r;
+                F.mp.split = sp;
+                F.mp.nitems = ntiles - r + r * sp;
+                F.flags = static_cast<int*>(pr->workspace);
+                F.ws = reinterpret_cast<float*>(static_cast<char*>(pr->workspace) + (64 << 10));
+            }
+        }
         F.acc_in = P.acc_in;
         F.ld_acc = P.ld_acc;
         F.rope_sign = 1.0f;

@@ -81,7 +81,23 @@ struct FastParams {
     const int32_t* colpart_map;
     const int64_t* labels;
     float* target;
+    // tail-split workspace: f32 partial accumulators [tail][piece < split-1][rank][128][256]
+    // and one flag per (tail, piece, rank, epilogue warp), zero between launches
+    float* ws;
+    int* flags;
 };
+
+__device__ __forceinline__ bool item_runs_program(const MainParams& mp, const Work& w) {
+    return w.piece < 0 || w.piece == mp.split - 1;
+}
+__device__ __forceinline__ void flag_release(int* f) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(f), "r"(1) : "memory");
+}
+__device__ __forceinline__ int flag_acquire(const int* f) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    return v;
+}
 
 // Side operands (residual, cos/sin, preact, pre_norm/grad_in) are TMA-loaded per
 // epilogue warp into a 4 KiB swizzled buffer, one 32-row chunk ahead; kernels that
@@ -331,9 +347,7 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         const uint32_t sbase = smem_u32(side + ew * SIDE_BYTES);
         uint32_t side_phase = 0;
         // lane 0: TMA-load the side operands of chunk c of tile t into this warp's buffer
-        auto side_issue = [&](int t_, int c_) {
-            int tm_, tn_;
-            tile_coord(mp, t_, tm_, tn_);
+        auto side_issue = [&](int tm_, int tn_, int c_) {
             const int y = tm_ * G::TILE_M + rank * BM + q * 32;
             const int x = tn_ * BN + h * 128 + c_ * 32;
             fence_proxy_async_smem();
@@ -345,12 +359,55 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 if (FL & (F_ROPE | F_RMSBWD_ACC)) tma_load_2d(sbase + 2048, &tma_s1, x, y, &sidebar[ew]);
             }
         };
-        if (FG::SIDE && lane == 0 && unit < mp.ntiles) side_issue(unit, 0);
-        for (int t = unit; t < mp.ntiles; t += nunits) {
-            int tm, tn;
-            tile_coord(mp, t, tm, tn);
+        if (FG::SIDE && lane == 0 && unit < mp.nitems) {
+            const Work w0 = work_item(mp, unit);
+            if (item_runs_program(mp, w0)) side_issue(w0.tm, w0.tn, 0);
+        }
+        const int nparts = mp.split - 1;   // partial pieces per split tile
+        for (int i = unit; i < mp.nitems; i += nunits) {
+            const Work w = work_item(mp, i);
+            const int tm = w.tm, tn = w.tn;
             const int m0 = tm * G::TILE_M + rank * BM;
             const int n0 = tn * BN;
+            if (w.piece >= 0 && w.piece < nparts) {
+                // an early K piece of a split tail tile: dump the raw f32 accumulator and signal
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+                const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + h * 128);
+                float* dst = P.ws + ((int64_t)(w.tail_idx * nparts + w.piece) * CG + rank) * (BM * BN) +
+                             (int64_t)(q * 32 + lane) * BN + h * 128;
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {
+                    float v[32];
+                    tmem_ld32(tb + c * 32, v);
+#pragma unroll
+                    for (int e = 0; e < 32; e += 4)
+                        *reinterpret_cast<float4*>(dst + c * 32 + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+                }
+                tc_fence_before();
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
+                    else mbar_arrive_leader(&tempty[acc]);
+                    flag_release(P.flags + ((w.tail_idx * nparts + w.piece) * CG + rank) * FAST_EPI_WARPS + ew);
+                }
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+                continue;
+            }
+            const bool last_piece = w.piece >= 0;
+            if (last_piece) {
+                // wait for every earlier piece of this tile (this warp's 32 x 128 region), reset flags
+                if (lane == 0) {
+                    for (int pc = 0; pc < nparts; ++pc) {
+                        int* f = P.flags + ((w.tail_idx * nparts + pc) * CG + rank) * FAST_EPI_WARPS + ew;
+                        while (flag_acquire(f) == 0) { }
+                        *f = 0;
+                    }
+                }
+                __syncwarp();
+            }
             const int64_t row = (int64_t)m0 + lrow;
             const bool row_ok = row < M;
             float rsc = 1.0f, rr = 0.0f, ss = 0.0f;
@@ -374,6 +431,21 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             for (int c = 0; c < 4; ++c) {
                 float v[32];
                 tmem_ld32(tbase + c * 32, v);
+                if (last_piece) {
+                    // fixed-order sum of the earlier K pieces (L2 loads, bypassing L1)
+                    for (int pc = 0; pc < nparts; ++pc) {
+                        const float* src = P.ws + ((int64_t)(w.tail_idx * nparts + pc) * CG + rank) * (BM * BN) +
+                                           (int64_t)(q * 32 + lane) * BN + h * 128 + c * 32;
+#pragma unroll
+                        for (int e = 0; e < 32; e += 4) {
+                            const float4 u = __ldcg(reinterpret_cast<const float4*>(src + e));
+                            v[e] += u.x;
+                            v[e + 1] += u.y;
+                            v[e + 2] += u.z;
+                            v[e + 3] += u.w;
+                        }
+                    }
+                }
                 if (c == 3) {
                     // this warp's share of the accumulator is in registers: release it
                     tc_fence_before();
@@ -395,8 +467,12 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     if constexpr ((FL & (F_ROPE | F_RMSBWD_ACC)) != 0) side_row<64>(sbase + 2048, lane, sd1);
                     __syncwarp();
                     if (lane == 0) {
-                        if (c < 3) side_issue(t, c + 1);
-                        else if (t + nunits < mp.ntiles) side_issue(t + nunits, 0);
+                        if (c < 3) {
+                            side_issue(tm, tn, c + 1);
+                        } else if (i + nunits < mp.nitems) {
+                            const Work wn = work_item(mp, i + nunits);
+                            if (item_runs_program(mp, wn)) side_issue(wn.tm, wn.tn, 0);
+                        }
                     }
                 }
                 const int gcol0 = n0 + h * 128 + c * 32;

@@ -44,7 +44,39 @@ struct MainParams {
     int ntm, ntn, nk, ntiles;   // ntm counts (pair) tiles of Geom<CG>::TILE_M rows
     int a_mn, b_mn;             // operand majorness: 1 = MN-major (transposed storage)
     int group;                  // raster group: m-tiles swept together across all n-tiles
+    // Tail splitting (wave quantization): the last `tail` tiles are split along K into
+    // `split` pieces that run concurrently in the final round; work items are the
+    // `full_tiles` whole tiles followed by tail x split pieces.
+    int full_tiles, tail, split, nitems;
 };
+
+// One unit of scheduled work: a whole tile (piece = -1) or piece `piece` of tail tile `tail_idx`.
+struct Work {
+    int tm, tn, kb0, kb1, piece, tail_idx;
+};
+
+__device__ __forceinline__ void tile_coord(const MainParams& mp, int t, int& tm, int& tn);
+
+__device__ __forceinline__ Work work_item(const MainParams& mp, int i) {
+    Work w;
+    int t;
+    if (i < mp.full_tiles) {
+        t = i;
+        w.piece = -1;
+        w.tail_idx = -1;
+        w.kb0 = 0;
+        w.kb1 = mp.nk;
+    } else {
+        const int j = i - mp.full_tiles;
+        w.tail_idx = j / mp.split;
+        w.piece = j - w.tail_idx * mp.split;
+        t = mp.full_tiles + w.tail_idx;
+        w.kb0 = (int)((int64_t)w.piece * mp.nk / mp.split);
+        w.kb1 = (int)((int64_t)(w.piece + 1) * mp.nk / mp.split);
+    }
+    tile_coord(mp, t, w.tm, w.tn);
+    return w;
+}
 
 __device__ __forceinline__ void tile_coord(const MainParams& mp, int t, int& tm, int& tn) {
     const int per_group = mp.group * mp.ntn;
@@ -64,12 +96,11 @@ __device__ __forceinline__ void producer_loop(const MainParams& mp, const CUtens
     using G = Geom<CG>;
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = unit; t < mp.ntiles; t += nunits) {
-        int tm, tn;
-        tile_coord(mp, t, tm, tn);
-        const int m0 = tm * G::TILE_M + rank * BM;
-        const int nb0 = tn * BN + rank * G::B_COLS;
-        for (int kb = 0; kb < mp.nk; ++kb) {
+    for (int i = unit; i < mp.nitems; i += nunits) {
+        const Work w = work_item(mp, i);
+        const int m0 = w.tm * G::TILE_M + rank * BM;
+        const int nb0 = w.tn * BN + rank * G::B_COLS;
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], G::STAGE * CG);
             const uint32_t sa = smem_u32(sA + stage * G::A_BYTES);
@@ -117,11 +148,12 @@ __device__ __forceinline__ void mma_loop(const MainParams& mp, uint32_t tmem_bas
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = unit; t < mp.ntiles; t += nunits) {
+    for (int i = unit; i < mp.nitems; i += nunits) {
+        const Work w = work_item(mp, i);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-        for (int kb = 0; kb < mp.nk; ++kb) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint32_t sa = smem_u32(sA + stage * G::A_BYTES);
@@ -130,8 +162,9 @@ __device__ __forceinline__ void mma_loop(const MainParams& mp, uint32_t tmem_bas
             for (int k = 0; k < BK / 16; ++k) {
                 const uint64_t ad = umma_desc_sw128(sa + k * a_step, a_lbo, 1024);
                 const uint64_t bd = umma_desc_sw128(sb + k * b_step, b_lbo, 1024);
-                if constexpr (CG == 1) umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
-                else umma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                const uint32_t accum = (kb != w.kb0 || k != 0) ? 1u : 0u;
+                if constexpr (CG == 1) umma_bf16(d_tmem, ad, bd, idesc, accum);
+                else umma_bf16_pair(d_tmem, ad, bd, idesc, accum);
             }
             if constexpr (CG == 1) umma_commit(&empty[stage]);
             else umma_commit_pair(&empty[stage]);
