@@ -1,0 +1,64 @@
+"""Single-GEMM micro-benchmark with engine options A/B'd in-process (CUDA-graph timed).
+
+    python tools/gemm_bench.py --shape 4096,4096,4096 --variant split=1 --variant split=0
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import statistics
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+import paper_2605_19269_b200 as cd  # noqa: E402
+from paper_2605_19269_b200 import _native  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--shape", action="append", required=True, help="m,n,k[,ta,tb]")
+    ap.add_argument("--variant", action="append", required=True)
+    ap.add_argument("--reps", type=int, default=20)
+    args = ap.parse_args()
+    P = cd.PrecisionMode.SIMBF16
+    for spec in args.shape:
+        parts = [int(x) for x in spec.split(",")]
+        m, n, k = parts[:3]
+        ta, tb = (bool(parts[3]), bool(parts[4])) if len(parts) == 5 else (False, False)
+        A = torch.randn((k, m) if ta else (m, k), device="cuda").to(torch.bfloat16)
+        B = torch.randn((n, k) if tb else (k, n), device="cuda").to(torch.bfloat16)
+        a, b = cd.DenseMatrix.from_tensor(A, P), cd.DenseMatrix.from_tensor(B, P)
+        prob = cd.GemmProblem(m=m, n=n, k=k, trans_a=ta, trans_b=tb, precision=P)
+        graphs = []
+        for v in args.variant:
+            opts = {kk: int(x) for kk, x in (kv.split("=") for kv in v.split(","))}
+            for kk, x in opts.items():
+                _native.set_option(kk, x)
+            for _ in range(3):
+                cd.run_gemm(prob, a, b)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _ in range(10):
+                    cd.run_gemm(prob, a, b)
+            graphs.append((v, g))
+        times = {v: [] for v, _ in graphs}
+        for _ in range(args.reps):
+            for v, g in graphs:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                g.replay()
+                e1.record()
+                torch.cuda.synchronize()
+                times[v].append(e0.elapsed_time(e1) / 10)
+        res = {v: statistics.median(t) for v, t in times.items()}
+        print(json.dumps({"shape": spec, **{v: {"ms": t, "tflops": 2 * m * n * k / t / 1e9} for v, t in res.items()}}),
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()
