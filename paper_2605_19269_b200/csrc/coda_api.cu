@@ -174,6 +174,7 @@ struct Options {
     int generic = 0;      // force the generic epilogue interpreter
     int raster = 8;       // raster group (pair m-tiles)
     int split = 1;        // split the partial last wave along K
+    int split_min_k = 8192;   // ... only for launches with at least this K
     Options() {
         if (const char* e = getenv("CODA_PDL")) pdl = e[0] != '0';
         if (const char* e = getenv("CODA_CG")) cg = e[0] == '1' ? 1 : 2;
@@ -393,6 +394,7 @@ int coda_set_option(const char* name, int value) {
         opts().cg = value;
     } else if (n == "generic") opts().generic = value != 0;
     else if (n == "split") opts().split = value != 0;
+    else if (n == "split_min_k") opts().split_min_k = value;
     else if (n == "raster") {
         if (value < 1) return fail(CODA_E_CONFIG, "raster group must be >= 1");
         opts().raster = value;
@@ -550,7 +552,10 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         // wave-tail split: the r tiles of the partial last wave run as s K-pieces each
         const int units = num_sms() / cg;
         const int r = units > 0 ? ntiles % units : 0;
-        if (opts().split && r > 0 && pr->workspace && pr->workspace_bytes > (64 << 10)) {
+        // only long-K launches: the dump / fixed-order fold costs ~10-20 us, which a split of a
+        // short mainloop cannot repay (tools/gemm_bench.py: +9 % at K=16384, -8 % at K=4096)
+        if (opts().split && r > 0 && K >= opts().split_min_k && pr->workspace &&
+            pr->workspace_bytes > (64 << 10)) {
             int sp = units / r;
             if (sp > P.nk / 4) sp = P.nk / 4;
             if (sp > 16) sp = 16;

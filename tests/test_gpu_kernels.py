@@ -256,6 +256,7 @@ def test_tail_split_matches_unsplit(cuda_ready):
         return outs
 
     try:
+        _native.set_option("split_min_k", 0)     # split every eligible launch of this test
         _native.set_option("split", 0)
         ref = run()
         _native.set_option("split", 1)
@@ -263,6 +264,7 @@ def test_tail_split_matches_unsplit(cuda_ready):
         got2 = run()
     finally:
         _native.set_option("split", 1)
+        _native.set_option("split_min_k", 8192)
     for i, (x, y, y2) in enumerate(zip(ref, got, got2)):
         assert np.array_equal(y, y2), f"output {i}: split launch not deterministic"
         assert O.rel_error(y, x) < 5e-3, (i, O.rel_error(y, x))
