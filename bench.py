@@ -40,6 +40,7 @@ CONFIGS = {
     "c5": (4096, 14336, 8192, "LLaMA-3-8B 4-block stack bf16 fwd+bwd, 8192 tokens/GPU/block (65536 over 8 GPUs)"),
 }
 BLOCKS = {"c5": 4}
+FP32 = {"c1"}          # BASELINE config 0 is the fp32 (SIM32) path
 
 
 def flops_per_token(d: int, inter: int) -> float:
@@ -163,7 +164,7 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- workload
 
 
-def make_workload(cd, d, inter, m, start, device, seed=0, blocks=1):
+def make_workload(cd, d, inter, m, start, device, seed=0, blocks=1, fp32=False):
     """Synthetic bf16 inputs and random-init weights (N(0, 0.02^2), gains 1 + 0.1 N).
 
     Weights are identical on every rank (same seed); activations differ per
@@ -171,12 +172,12 @@ def make_workload(cd, d, inter, m, start, device, seed=0, blocks=1):
     """
     import torch
 
-    P = cd.PrecisionMode.SIMBF16
+    P = cd.PrecisionMode.SIM32 if fp32 else cd.PrecisionMode.SIMBF16
     g = torch.Generator(device=device).manual_seed(seed)
     gr = torch.Generator(device=device).manual_seed(seed * 1000 + 17 + start)
 
     def w(*shape, scale=0.02, gen=g):
-        t = cd.tensors.alloc_matrix(shape[0], shape[1], torch.bfloat16, device)
+        t = cd.tensors.alloc_matrix(shape[0], shape[1], P.torch_dtype, device)
         t.copy_(torch.randn(shape, generator=gen, device=device) * scale)
         return cd.DenseMatrix.from_tensor(t, P)
 
@@ -306,7 +307,11 @@ def coda_arm(args, rank, world, local_rank):
     P = cd.PrecisionMode.SIMBF16
     cfg = cd.PipelineConfig(hidden=d, ffn=2 * inter, precision=P)
     nblocks = BLOCKS.get(args.config, 1)
-    weights, acts, cos, sin = make_workload(cd, d, inter, m, sh.start, device, blocks=nblocks)
+    fp32 = args.config in FP32
+    if fp32:
+        P = cd.PrecisionMode.SIM32
+        cfg = cd.PipelineConfig(hidden=d, ffn=2 * inter, precision=P)
+    weights, acts, cos, sin = make_workload(cd, d, inter, m, sh.start, device, blocks=nblocks, fp32=fp32)
     hook = parallel.WgradAllReduce(dist, device) if dist is not None else None
 
     def step():
@@ -380,9 +385,9 @@ def coda_arm(args, rank, world, local_rank):
             for j in range(2)]
     dev_in = [{k: torch.empty_like(v.tensor) for k, v in acts.items()} for _ in range(2)]
     h2d = sum(t.numel() * t.element_size() for t in host[0].values())
-    out_host = [torch.empty((m, d), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+    out_host = [torch.empty((m, d), dtype=P.torch_dtype).pin_memory() for _ in range(2)]
     gam_host = [torch.empty((2, d), dtype=torch.float32).pin_memory() for _ in range(2)]
-    d2h = out_host[0].numel() * 2 + gam_host[0].numel() * 4
+    d2h = out_host[0].numel() * out_host[0].element_size() + gam_host[0].numel() * 4
     h2d_stream, d2h_stream = torch.cuda.Stream(device), torch.cuda.Stream(device)
 
     def e2e_run(nsteps):
@@ -466,7 +471,8 @@ def coda_arm(args, rank, world, local_rank):
             "metric": "block fwd+bwd tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if args.scaling == "strong" and world > 1 else "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, N(0,1) activations)",
+            "vs_baseline": None, "dtype": "f32" if fp32 else "bf16",
+            "data": "synthetic (random-init weights, N(0,1) activations)",
             "config": {"workload": label, "blocks": nblocks, "tokens_per_gpu": m, "global_tokens": world * m,
                        "hidden": d,
                        "intermediate": inter, "ffn_interleaved": 2 * inter, "qkv": 3 * d,

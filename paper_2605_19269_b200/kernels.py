@@ -110,12 +110,24 @@ def _problem(a: DenseMatrix, b: DenseMatrix, *, trans_a=False, trans_b=False, ti
                        reduction_tile_n=reduction_tile_n, precision=precision)
 
 
+_programs: dict = {}
+
+
+def _program(prims) -> EpilogueProgram:
+    """Validated programs are immutable: build each distinct primitive sequence once."""
+    key = tuple(repr(p) for p in prims)
+    prog = _programs.get(key)
+    if prog is None:
+        prog = _programs[key] = EpilogueProgram(prims)
+    return prog
+
+
 def _launch(name, a, b, prims, bindings, *, trans_a=False, trans_b=False, tile_shape=TileShape(128, 128),
             reduction_tile_n=128, precision=PrecisionMode.EXACT64, ledger=None, tile_order=None,
             store_main=True, out_f32=False) -> KernelResult:
     prob = _problem(a, b, trans_a=trans_a, trans_b=trans_b, tile_shape=tile_shape,
                     reduction_tile_n=reduction_tile_n, precision=precision)
-    return run_gemm(prob, a, b, EpilogueProgram(prims), bindings, kernel_name=name, ledger=ledger,
+    return run_gemm(prob, a, b, _program(prims), bindings, kernel_name=name, ledger=ledger,
                     tile_order=tile_order, store_main=store_main, out_f32=out_f32)
 
 
