@@ -216,14 +216,14 @@ class CpuOracle:
     """The reference algorithm on the host cores: the fused-order SIMBF16 oracle
     (oracle/coda_oracle.py, numpy/OpenBLAS using every core) on a token sample."""
 
-    def __init__(self, d, inter, sample_tokens, seed=0):
+    def __init__(self, d, inter, sample_tokens, seed=0, fp32=False):
         import numpy as np
 
         from oracle import coda_oracle as O
 
         self.O = O
         rng = np.random.default_rng(seed)
-        self.mode = O.SIMBF16
+        self.mode = O.SIM32 if fp32 else O.SIMBF16
         self.w = O.random_layer(rng, d, 2 * inter, self.mode, scale=0.02)
         self.m = sample_tokens
         self.x, self.z = (O.q(rng.standard_normal((self.m, d)), self.mode) for _ in range(2))
@@ -239,8 +239,8 @@ class CpuOracle:
         return time.perf_counter() - t0
 
 
-def cpu_oracle_tokens_per_s(d, inter, sample_tokens, seconds_budget=20.0, max_reps=5):
-    runner = CpuOracle(d, inter, sample_tokens)
+def cpu_oracle_tokens_per_s(d, inter, sample_tokens, seconds_budget=20.0, max_reps=5, fp32=False):
+    runner = CpuOracle(d, inter, sample_tokens, fp32=fp32)
     times = []
     t_start = time.perf_counter()
     while True:
@@ -266,8 +266,8 @@ def reference_arm(args, rank, world):
     d, inter, tokens, label = CONFIGS[args.config]
     if rank != 0:
         return
-    sample = args.cpu_sample
-    runner = CpuOracle(d, inter, sample)
+    sample = min(args.cpu_sample, tokens)
+    runner = CpuOracle(d, inter, sample, fp32=args.config in FP32)
     for _ in range(max(1, args.warmup)):
         runner.step()
     per_step = [runner.step() for _ in range(args.steps)]
@@ -461,9 +461,11 @@ def coda_arm(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        tps, secs, reps = cpu_oracle_tokens_per_s(d, inter, args.cpu_sample, seconds_budget=20.0, max_reps=3)
+        sample = min(args.cpu_sample, m)
+        tps, secs, reps = cpu_oracle_tokens_per_s(d, inter, sample, seconds_budget=20.0, max_reps=3, fp32=fp32)
         cpu = {"value": tps, "unit": "tokens/s", "cores": host_cores(), "kind": "port",
-               "sample": f"{args.cpu_sample} tokens of the {args.config} block, fused-order SIMBF16 oracle, "
+               "sample": f"{sample} tokens of the {args.config} block, fused-order "
+                         f"{'SIM32' if fp32 else 'SIMBF16'} oracle, "
                          f"best of {reps} ({secs:.2f} s each)"}
 
     if rank == 0:
