@@ -106,6 +106,11 @@ def kernels_case(tag, mode_name, m, k, n, tile, rtn, seed):
     out["at"] = at.data
     out["wgrad"] = tf.run_gemm(tf.GemmProblem(m=m, n=n, k=k, trans_a=True, precision=mode, tile_shape=ts,
                                               reduction_tile_n=rtn), at, b).main.data
+    # reference traffic ledger records (read, write bytes) of each launch above
+    out["records"] = np.array([[r.read_bytes, r.write_bytes] for r in (
+        tf.gemm_rope(a, b, cos, sin, **kw).record, k2.record, k3.record, k4.record,
+        tf.gemm_row_scale(a, b, r, **kw).record, k6.record, tf.gemm_rms_rope(a, b, r, cos, sin, **kw).record,
+        k8.record, k9.record, k10.record)], dtype=np.int64)
     save(f"kernels_{tag}_{mode_name}", **out)
 
 
