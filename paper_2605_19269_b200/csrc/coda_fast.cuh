@@ -331,9 +331,9 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     griddep_wait();
 
     if (warp == 0) {
-        if (lane == 0) producer_loop<CG, NS>(mp, &tma_a, &tma_b, sA, sB, full, empty, rank, unit, nunits);
+        producer_loop<CG, NS>(mp, &tma_a, &tma_b, sA, sB, full, empty, rank, unit, nunits);
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) mma_loop<CG, NS>(mp, tmem_base, sA, sB, full, empty, tfull, tempty, unit, nunits);
+        if (rank == 0) mma_loop<CG, NS>(mp, tmem_base, sA, sB, full, empty, tfull, tempty, unit, nunits);
     } else {
         const int ew = warp - 2;            // 0..7
         const int q = warp & 3;             // TMEM lane quadrant

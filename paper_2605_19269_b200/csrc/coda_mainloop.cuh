@@ -88,7 +88,8 @@ __device__ __forceinline__ void tile_coord(const MainParams& mp, int t, int& tm,
     tn = r / gs;
 }
 
-// TMA producer (one thread per CTA): fills this CTA's smem ring for every tile it owns.
+// TMA producer (one warp per CTA, warp-uniform control flow; one elected lane
+// issues): fills this CTA's smem ring for every tile it owns.
 template <int CG, int NS = Geom<CG>::NSTAGE>
 __device__ __forceinline__ void producer_loop(const MainParams& mp, const CUtensorMap* tma_a,
                                               const CUtensorMap* tma_b, uint8_t* sA, uint8_t* sB,
@@ -96,40 +97,46 @@ __device__ __forceinline__ void producer_loop(const MainParams& mp, const CUtens
     using G = Geom<CG>;
     int stage = 0;
     uint32_t phase = 0;
+    const uint32_t sa0 = smem_u32(sA), sb0 = smem_u32(sB);
     for (int i = unit; i < mp.nitems; i += nunits) {
         const Work w = work_item(mp, i);
         const int m0 = w.tm * G::TILE_M + rank * BM;
         const int nb0 = w.tn * BN + rank * G::B_COLS;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
-            if (rank == 0) mbar_arrive_expect_tx(&full[stage], G::STAGE * CG);
-            const uint32_t sa = smem_u32(sA + stage * G::A_BYTES);
-            const uint32_t sb = smem_u32(sB + stage * G::B_BYTES);
-            const int k0 = kb * BK;
-            auto load = [&](uint32_t dst, const CUtensorMap* map, int c0, int c1) {
-                if constexpr (CG == 1) tma_load_2d(dst, map, c0, c1, &full[stage]);
-                else tma_load_2d_pair(dst, map, c0, c1, &full[stage]);
-            };
-            if (!mp.a_mn) {
-                load(sa, tma_a, k0, m0);
-            } else {
+            if (elect_one()) {
+                if (rank == 0) mbar_arrive_expect_tx(&full[stage], G::STAGE * CG);
+                const uint32_t sa = sa0 + stage * G::A_BYTES;
+                const uint32_t sb = sb0 + stage * G::B_BYTES;
+                const int k0 = kb * BK;
+                auto load = [&](uint32_t dst, const CUtensorMap* map, int c0, int c1) {
+                    if constexpr (CG == 1) tma_load_2d(dst, map, c0, c1, &full[stage]);
+                    else tma_load_2d_pair(dst, map, c0, c1, &full[stage]);
+                };
+                if (!mp.a_mn) {
+                    load(sa, tma_a, k0, m0);
+                } else {
 #pragma unroll
-                for (int b = 0; b < BM / 64; ++b) load(sa + b * (BK * 128), tma_a, m0 + 64 * b, k0);
-            }
-            if (!mp.b_mn) {
-                load(sb, tma_b, k0, nb0);
-            } else {
+                    for (int b = 0; b < BM / 64; ++b) load(sa + b * (BK * 128), tma_a, m0 + 64 * b, k0);
+                }
+                if (!mp.b_mn) {
+                    load(sb, tma_b, k0, nb0);
+                } else {
 #pragma unroll
-                for (int b = 0; b < G::B_COLS / 64; ++b) load(sb + b * (BK * 128), tma_b, nb0 + 64 * b, k0);
+                    for (int b = 0; b < G::B_COLS / 64; ++b) load(sb + b * (BK * 128), tma_b, nb0 + 64 * b, k0);
+                }
             }
+            __syncwarp();
             if (++stage == NS) { stage = 0; phase ^= 1; }
         }
     }
 }
 
-// MMA issuer (one thread; for CG = 2 only in the leader CTA): 4 x tcgen05.mma
-// (K = 16 each) per k-block into the current TMEM accumulator; commits free smem
-// stages and publish finished accumulators.
+// MMA issuer (one warp; for CG = 2 only in the leader CTA; one elected lane issues):
+// 4 x tcgen05.mma (K = 16 each) per k-block into the current TMEM accumulator;
+// commits free smem stages and publish finished accumulators.  Descriptors are a
+// per-launch base plus compile-time/stage offsets in the 14-bit address field
+// (smem addresses < 256 KiB, so the field never carries).
 template <int CG, int NS = Geom<CG>::NSTAGE>
 __device__ __forceinline__ void mma_loop(const MainParams& mp, uint32_t tmem_base, uint8_t* sA, uint8_t* sB,
                                          uint64_t* full, uint64_t* empty, uint64_t* tfull, uint64_t* tempty,
@@ -143,7 +150,9 @@ __device__ __forceinline__ void mma_loop(const MainParams& mp, uint32_t tmem_bas
     // MN-major: LBO = next 64-wide MN atom column (BK * 128 B), SBO = 8 K-rows * 128 B;
     //           advance 2 x 1024 B per UMMA_K = 16.
     const uint32_t a_lbo = mp.a_mn ? BK * 128 : 16, b_lbo = mp.b_mn ? BK * 128 : 16;
-    const uint32_t a_step = mp.a_mn ? 2048 : 32, b_step = mp.b_mn ? 2048 : 32;
+    const uint64_t a_step = mp.a_mn ? (2048 >> 4) : (32 >> 4), b_step = mp.b_mn ? (2048 >> 4) : (32 >> 4);
+    const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA), a_lbo, 1024);
+    const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB), b_lbo, 1024);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -156,22 +165,26 @@ __device__ __forceinline__ void mma_loop(const MainParams& mp, uint32_t tmem_bas
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            const uint32_t sa = smem_u32(sA + stage * G::A_BYTES);
-            const uint32_t sb = smem_u32(sB + stage * G::B_BYTES);
+            if (elect_one()) {
+                const uint64_t ad = a_desc0 + (uint64_t)((stage * G::A_BYTES) >> 4);
+                const uint64_t bd = b_desc0 + (uint64_t)((stage * G::B_BYTES) >> 4);
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k) {
-                const uint64_t ad = umma_desc_sw128(sa + k * a_step, a_lbo, 1024);
-                const uint64_t bd = umma_desc_sw128(sb + k * b_step, b_lbo, 1024);
-                const uint32_t accum = (kb != w.kb0 || k != 0) ? 1u : 0u;
-                if constexpr (CG == 1) umma_bf16(d_tmem, ad, bd, idesc, accum);
-                else umma_bf16_pair(d_tmem, ad, bd, idesc, accum);
+                for (int k = 0; k < BK / 16; ++k) {
+                    const uint32_t accum = (kb != w.kb0 || k != 0) ? 1u : 0u;
+                    if constexpr (CG == 1) umma_bf16(d_tmem, ad + k * a_step, bd + k * b_step, idesc, accum);
+                    else umma_bf16_pair(d_tmem, ad + k * a_step, bd + k * b_step, idesc, accum);
+                }
+                if constexpr (CG == 1) umma_commit(&empty[stage]);
+                else umma_commit_pair(&empty[stage]);
             }
-            if constexpr (CG == 1) umma_commit(&empty[stage]);
-            else umma_commit_pair(&empty[stage]);
+            __syncwarp();
             if (++stage == NS) { stage = 0; phase ^= 1; }
         }
-        if constexpr (CG == 1) umma_commit(&tfull[acc]);
-        else umma_commit_pair(&tfull[acc]);
+        if (elect_one()) {
+            if constexpr (CG == 1) umma_commit(&tfull[acc]);
+            else umma_commit_pair(&tfull[acc]);
+        }
+        __syncwarp();
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
     }
