@@ -197,16 +197,23 @@ def make_workload(cd, d, inter, m, start, device, seed=0, blocks=1, fp32=False):
     return weights, acts, cos, sin
 
 
-def run_step(cd, cfg, weights, acts, cos, sin, hook=None):
-    """One fwd+bwd step: a single block, or a stack when `weights` is a list of blocks."""
+def run_step(cd, cfg, weights, acts, cos, sin, hook=None, before_backward=None):
+    """One fwd+bwd step: a single block, or a stack when `weights` is a list of blocks.
+
+    `before_backward` (optional) runs after the forward is enqueued — the e2e loop
+    uses it to make the backward wait for its own inputs' host-to-device copy."""
     if isinstance(weights, (list, tuple)):
         from paper_2605_19269_b200 import stack
 
         fwd = stack.stack_forward(acts["x"], acts["z"], weights, cos, sin, config=cfg)
+        if before_backward is not None:
+            before_backward()
         grads = stack.stack_backward(acts["grad_qkv"], acts["grad_residual"], fwd, weights, config=cfg,
                                      wgrad_hook=hook)
         return fwd, grads[0]
     fwd = cd.layer_forward(acts["x"], acts["z"], weights, cos, sin, config=cfg)
+    if before_backward is not None:
+        before_backward()
     bwd = cd.layer_backward(acts["grad_qkv"], fwd.tape, weights, grad_residual=acts["grad_residual"], config=cfg,
                             wgrad_hook=hook)
     return fwd, bwd
@@ -390,19 +397,31 @@ def coda_arm(args, rank, world, local_rank):
     d2h = out_host[0].numel() * out_host[0].element_size() + gam_host[0].numel() * 4
     h2d_stream, d2h_stream = torch.cuda.Stream(device), torch.cuda.Stream(device)
 
+    # Forward inputs (x, z) are copied first with their own event, so a step's forward
+    # starts after 268 MB rather than all 805 MB; the backward waits for grad_qkv /
+    # grad_residual.  Results of step s are kept referenced until their D2H copy is
+    # done (no record_stream: the allocator then reuses the same blocks every step).
+    fwd_keys = ("x", "z")
+
     def e2e_run(nsteps):
-        copied = [torch.cuda.Event() for _ in range(2)]
+        copied_f = [torch.cuda.Event() for _ in range(2)]
+        copied_b = [torch.cuda.Event() for _ in range(2)]
         consumed = [torch.cuda.Event() for _ in range(2)]
         done = [torch.cuda.Event() for _ in range(2)]
+        pending = [None, None]
 
         def issue_copy(s):
             b = s % 2
             with torch.cuda.stream(h2d_stream):
                 if s >= 2:
                     h2d_stream.wait_event(consumed[b])
-                for k in host[b]:
+                for k in fwd_keys:
                     dev_in[b][k].copy_(host[b][k], non_blocking=True)
-                copied[b].record(h2d_stream)
+                copied_f[b].record(h2d_stream)
+                for k in host[b]:
+                    if k not in fwd_keys:
+                        dev_in[b][k].copy_(host[b][k], non_blocking=True)
+                copied_b[b].record(h2d_stream)
 
         h2d_stream.wait_stream(stream)
         issue_copy(0)
@@ -410,9 +429,13 @@ def coda_arm(args, rank, world, local_rank):
             b = s % 2
             if s + 1 < nsteps:
                 issue_copy(s + 1)
-            stream.wait_event(copied[b])
+            if pending[b] is not None:   # step s-2's results: D2H finished before their blocks are reused
+                stream.wait_event(done[b])
+                pending[b] = None
+            stream.wait_event(copied_f[b])
             a = {k: cd.DenseMatrix.from_tensor(dev_in[b][k], P) for k in dev_in[b]}
-            _, bwd = run_step(cd, cfg, weights, a, cos, sin, hook)
+            _, bwd = run_step(cd, cfg, weights, a, cos, sin, hook,
+                              before_backward=lambda: stream.wait_event(copied_b[b]))
             if hook is not None:
                 hook.wait()
             consumed[b].record(stream)
@@ -422,12 +445,12 @@ def coda_arm(args, rank, world, local_rank):
                 gam_host[b][0].copy_(bwd.gamma_ffn.tensor, non_blocking=True)
                 gam_host[b][1].copy_(bwd.gamma_qkv.tensor, non_blocking=True)
                 done[b].record(d2h_stream)
-                for t in (bwd.x.tensor, bwd.gamma_ffn.tensor, bwd.gamma_qkv.tensor):
-                    t.record_stream(d2h_stream)
+            pending[b] = bwd
         stream.wait_stream(d2h_stream)
         stream.wait_stream(h2d_stream)
+        pending[0] = pending[1] = None   # later allocations on `stream` are ordered after the D2H
 
-    e2e_run(max(2, args.warmup // 2))
+    e2e_run(max(4, args.warmup))
     barrier()
     e0.record(stream)
     e2e_run(args.steps)
