@@ -403,7 +403,17 @@ def coda_arm(args, rank, world, local_rank):
     # done (no record_stream: the allocator then reuses the same blocks every step).
     fwd_keys = ("x", "z")
 
+    timeline = os.environ.get("CODA_E2E_TIMELINE") == "1"
+
+    def mark(marks, what, st):
+        if timeline:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(st)
+            marks.append((what, e))
+
     def e2e_run(nsteps):
+        marks = []
+        mark(marks, "begin", stream)
         copied_f = [torch.cuda.Event() for _ in range(2)]
         copied_b = [torch.cuda.Event() for _ in range(2)]
         consumed = [torch.cuda.Event() for _ in range(2)]
@@ -415,6 +425,7 @@ def coda_arm(args, rank, world, local_rank):
             with torch.cuda.stream(h2d_stream):
                 if s >= 2:
                     h2d_stream.wait_event(consumed[b])
+                mark(marks, f"copy{s} start", h2d_stream)
                 for k in fwd_keys:
                     dev_in[b][k].copy_(host[b][k], non_blocking=True)
                 copied_f[b].record(h2d_stream)
@@ -422,6 +433,7 @@ def coda_arm(args, rank, world, local_rank):
                     if k not in fwd_keys:
                         dev_in[b][k].copy_(host[b][k], non_blocking=True)
                 copied_b[b].record(h2d_stream)
+                mark(marks, f"copy{s} end", h2d_stream)
 
         h2d_stream.wait_stream(stream)
         issue_copy(0)
@@ -433,12 +445,14 @@ def coda_arm(args, rank, world, local_rank):
                 stream.wait_event(done[b])
                 pending[b] = None
             stream.wait_event(copied_f[b])
+            mark(marks, f"step{s} start", stream)
             a = {k: cd.DenseMatrix.from_tensor(dev_in[b][k], P) for k in dev_in[b]}
             _, bwd = run_step(cd, cfg, weights, a, cos, sin, hook,
                               before_backward=lambda: stream.wait_event(copied_b[b]))
             if hook is not None:
                 hook.wait()
             consumed[b].record(stream)
+            mark(marks, f"step{s} end", stream)
             with torch.cuda.stream(d2h_stream):
                 d2h_stream.wait_event(consumed[b])
                 out_host[b].copy_(bwd.x.tensor, non_blocking=True)
@@ -449,6 +463,11 @@ def coda_arm(args, rank, world, local_rank):
         stream.wait_stream(d2h_stream)
         stream.wait_stream(h2d_stream)
         pending[0] = pending[1] = None   # later allocations on `stream` are ordered after the D2H
+        if timeline:
+            torch.cuda.synchronize()
+            t0 = marks[0][1]
+            for what, e in sorted(marks[1:], key=lambda x: t0.elapsed_time(x[1])):
+                print(f"  e2e {what:14s} {t0.elapsed_time(e):9.2f} ms", file=sys.stderr)
 
     e2e_run(max(4, args.warmup))
     barrier()

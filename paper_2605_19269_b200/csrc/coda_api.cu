@@ -175,7 +175,11 @@ struct Options {
     int raster = 8;       // raster group (pair m-tiles)
     int split = 1;        // split the partial last wave along K
     int split_min_k = 8192;   // ... only for launches with at least this K
+    int prefetch = 0;     // L2 prefetch distance (k-blocks beyond the smem ring)
+    int ablate = 0;       // measurement-only epilogue ablations (results invalid)
+    int ring = 0;         // operand ring stages in use (0 = the compiled depth)
     Options() {
+        if (const char* e = getenv("CODA_PREFETCH")) prefetch = atoi(e);
         if (const char* e = getenv("CODA_PDL")) pdl = e[0] != '0';
         if (const char* e = getenv("CODA_CG")) cg = e[0] == '1' ? 1 : 2;
         if (const char* e = getenv("CODA_FORCE_GENERIC")) generic = e[0] && e[0] != '0';
@@ -395,6 +399,12 @@ int coda_set_option(const char* name, int value) {
     } else if (n == "generic") opts().generic = value != 0;
     else if (n == "split") opts().split = value != 0;
     else if (n == "split_min_k") opts().split_min_k = value;
+    else if (n == "ablate") opts().ablate = value;
+    else if (n == "ring") opts().ring = value;
+    else if (n == "prefetch") {
+        if (value < 0 || value > 64) return fail(CODA_E_CONFIG, "prefetch distance must be in [0, 64]");
+        opts().prefetch = value;
+    }
     else if (n == "raster") {
         if (value < 1) return fail(CODA_E_CONFIG, "raster group must be >= 1");
         opts().raster = value;
@@ -548,7 +558,7 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         const int ntm = (int)((M + tile_m - 1) / tile_m);
         const int ntiles = ntm * P.ntn;
         F.mp = coda::MainParams{P.M, P.N, P.K, ntm, P.ntn, P.nk, ntiles, P.a_mn, P.b_mn,
-                                raster_group(ntm, tile_m, K), ntiles, 0, 1, ntiles};
+                                raster_group(ntm, tile_m, K), ntiles, 0, 1, ntiles, opts().prefetch, opts().ring};
         // wave-tail split: the r tiles of the partial last wave run as s K-pieces each
         const int units = num_sms() / cg;
         const int r = units > 0 ? ntiles % units : 0;
@@ -574,6 +584,7 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         }
         F.acc_in = P.acc_in;
         F.ld_acc = P.ld_acc;
+        F.ablate = opts().ablate;
         F.rope_sign = 1.0f;
         int aux_slot = -1;
         for (int s = 0; s < nsteps; ++s) {

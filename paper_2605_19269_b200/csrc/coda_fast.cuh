@@ -85,6 +85,7 @@ struct FastParams {
     // and one flag per (tail, piece, rank, epilogue warp), zero between launches
     float* ws;
     int* flags;
+    int ablate;   // measurement-only ablations (results invalid): 1 = no side loads, 2 = no TMA stores
 };
 
 __device__ __forceinline__ bool item_runs_program(const MainParams& mp, const Work& w) {
@@ -188,6 +189,7 @@ struct Stager {
     uint32_t base;      // smem address of this warp's 4 KiB buffer (1024-aligned)
     int region;
     bool wide_pending;
+    bool skip;          // ablation: stage into smem but issue no TMA store
 };
 
 template <typename TO, int W>
@@ -233,7 +235,7 @@ __device__ __forceinline__ void staged_store(Stager& sg, const CUtensorMap* tm, 
     fence_proxy_async_smem();
     __syncwarp();
     // 3. one lane hands the box to the TMA engine
-    if (lane == 0) {
+    if (lane == 0 && !sg.skip) {
         if (RB == 128) {
             tma_store_2d(tm, sg.base, x, y);
             tma_store_2d(tm, sg.base + 2048, x, y + 16);
@@ -340,14 +342,16 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         const int h = ew >> 2;              // column half of the 256-wide tile
         const int lrow = q * 32 + lane;
         const int M = mp.M, N = mp.N;
-        Stager sg{smem_u32(stg + ew * STG_BYTES), 0, false};
+        Stager sg{smem_u32(stg + ew * STG_BYTES), 0, false, (P.ablate & 2) != 0};
         int cbuf = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
         const uint32_t sbase = smem_u32(side + ew * SIDE_BYTES);
         uint32_t side_phase = 0;
         // lane 0: TMA-load the side operands of chunk c of tile t into this warp's buffer
+        const bool no_side = (P.ablate & 1) != 0;
         auto side_issue = [&](int tm_, int tn_, int c_) {
+            if (no_side) return;
             const int y = tm_ * G::TILE_M + rank * BM + q * 32;
             const int x = tn_ * BN + h * 128 + c_ * 32;
             fence_proxy_async_smem();
@@ -460,8 +464,10 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 float sd0[FG::SIDE ? ((FL & F_SWIGLU_BWD) ? 64 : 32) : 1];
                 float sd1[(FL & (F_ROPE | F_RMSBWD_ACC)) ? 32 : 1];
                 if constexpr (FG::SIDE) {
-                    mbar_wait(&sidebar[ew], side_phase);
-                    side_phase ^= 1;
+                    if (!no_side) {
+                        mbar_wait(&sidebar[ew], side_phase);
+                        side_phase ^= 1;
+                    }
                     if constexpr ((FL & F_SWIGLU_BWD) != 0) side_row<128>(sbase, lane, sd0);
                     else side_row<64>(sbase, lane, sd0);
                     if constexpr ((FL & (F_ROPE | F_RMSBWD_ACC)) != 0) side_row<64>(sbase + 2048, lane, sd1);

@@ -324,7 +324,7 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
     griddep_wait();
 
     const MainParams mp{P.M, P.N, P.K, P.ntm, P.ntn, P.nk, P.ntiles, P.a_mn, P.b_mn, 16,
-                        P.ntiles, 0, 1, P.ntiles};
+                        P.ntiles, 0, 1, P.ntiles, 0, 0};
     auto tile_mn = [&](int t, int& tm, int& tn) { tile_coord(mp, t, tm, tn); };
 
     if (warp == 0) {

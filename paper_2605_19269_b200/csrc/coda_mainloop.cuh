@@ -48,6 +48,8 @@ struct MainParams {
     // `split` pieces that run concurrently in the final round; work items are the
     // `full_tiles` whole tiles followed by tail x split pieces.
     int full_tiles, tail, split, nitems;
+    int prefetch;               // L2 prefetch distance in k-blocks beyond the load (0 = off)
+    int ns;                     // ring stages in use (<= the compiled ring depth; 0 = all)
 };
 
 // One unit of scheduled work: a whole tile (piece = -1) or piece `piece` of tail tile `tail_idx`.
@@ -98,36 +100,62 @@ __device__ __forceinline__ void producer_loop(const MainParams& mp, const CUtens
     int stage = 0;
     uint32_t phase = 0;
     const uint32_t sa0 = smem_u32(sA), sb0 = smem_u32(sB);
+    const int nst = (mp.ns > 0 && mp.ns < NS) ? mp.ns : NS;
+    auto boxes = [&](auto&& op, int m0, int nb0, int kb) {
+        const int k0 = kb * BK;
+        if (!mp.a_mn) {
+            op(0, tma_a, k0, m0);
+        } else {
+#pragma unroll
+            for (int b = 0; b < BM / 64; ++b) op(b * (BK * 128), tma_a, m0 + 64 * b, k0);
+        }
+        if (!mp.b_mn) {
+            op(-1, tma_b, k0, nb0);
+        } else {
+#pragma unroll
+            for (int b = 0; b < G::B_COLS / 64; ++b) op(-1 - b * (BK * 128), tma_b, nb0 + 64 * b, k0);
+        }
+    };
+    auto prefetch = [&](int, const CUtensorMap* map, int c0, int c1) { tma_prefetch_2d(map, c0, c1); };
+    const int pf = mp.prefetch;
+    if (pf > 0 && unit < mp.nitems && elect_one()) {
+        // warm L2 for the first k-blocks this unit will load beyond the ring
+        const Work w = work_item(mp, unit);
+        const int m0 = w.tm * G::TILE_M + rank * BM, nb0 = w.tn * BN + rank * G::B_COLS;
+        for (int kb = w.kb0 + nst; kb < w.kb1 && kb < w.kb0 + nst + pf; ++kb) boxes(prefetch, m0, nb0, kb);
+    }
+    __syncwarp();
     for (int i = unit; i < mp.nitems; i += nunits) {
         const Work w = work_item(mp, i);
         const int m0 = w.tm * G::TILE_M + rank * BM;
         const int nb0 = w.tn * BN + rank * G::B_COLS;
+        // the item after this one (prefetch target once this item's k-blocks run out)
+        const bool has_next = i + nunits < mp.nitems;
+        Work wn = w;
+        if (pf > 0 && has_next) wn = work_item(mp, i + nunits);
+        const int m0n = wn.tm * G::TILE_M + rank * BM, nb0n = wn.tn * BN + rank * G::B_COLS;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
             if (elect_one()) {
                 if (rank == 0) mbar_arrive_expect_tx(&full[stage], G::STAGE * CG);
                 const uint32_t sa = sa0 + stage * G::A_BYTES;
                 const uint32_t sb = sb0 + stage * G::B_BYTES;
-                const int k0 = kb * BK;
-                auto load = [&](uint32_t dst, const CUtensorMap* map, int c0, int c1) {
-                    if constexpr (CG == 1) tma_load_2d(dst, map, c0, c1, &full[stage]);
-                    else tma_load_2d_pair(dst, map, c0, c1, &full[stage]);
+                uint64_t* bar = &full[stage];
+                auto load = [&](int off, const CUtensorMap* map, int c0, int c1) {
+                    const uint32_t dst = off >= 0 ? sa + (uint32_t)off : sb + (uint32_t)(-1 - off);
+                    if constexpr (CG == 1) tma_load_2d(dst, map, c0, c1, bar);
+                    else tma_load_2d_pair(dst, map, c0, c1, bar);
                 };
-                if (!mp.a_mn) {
-                    load(sa, tma_a, k0, m0);
-                } else {
-#pragma unroll
-                    for (int b = 0; b < BM / 64; ++b) load(sa + b * (BK * 128), tma_a, m0 + 64 * b, k0);
-                }
-                if (!mp.b_mn) {
-                    load(sb, tma_b, k0, nb0);
-                } else {
-#pragma unroll
-                    for (int b = 0; b < G::B_COLS / 64; ++b) load(sb + b * (BK * 128), tma_b, nb0 + 64 * b, k0);
+                boxes(load, m0, nb0, kb);
+                if (pf > 0) {
+                    // keep L2 `pf` k-blocks ahead of the ring: this item, then the next one
+                    const int kp = kb + nst + pf;
+                    if (kp < w.kb1) boxes(prefetch, m0, nb0, kp);
+                    else if (has_next && kp - w.kb1 + wn.kb0 < wn.kb1) boxes(prefetch, m0n, nb0n, kp - w.kb1 + wn.kb0);
                 }
             }
             __syncwarp();
-            if (++stage == NS) { stage = 0; phase ^= 1; }
+            if (++stage == nst) { stage = 0; phase ^= 1; }
         }
     }
 }
@@ -153,6 +181,7 @@ __device__ __forceinline__ void mma_loop(const MainParams& mp, uint32_t tmem_bas
     const uint64_t a_step = mp.a_mn ? (2048 >> 4) : (32 >> 4), b_step = mp.b_mn ? (2048 >> 4) : (32 >> 4);
     const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA), a_lbo, 1024);
     const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB), b_lbo, 1024);
+    const int nst = (mp.ns > 0 && mp.ns < NS) ? mp.ns : NS;
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -178,7 +207,7 @@ __device__ __forceinline__ void mma_loop(const MainParams& mp, uint32_t tmem_bas
                 else umma_commit_pair(&empty[stage]);
             }
             __syncwarp();
-            if (++stage == NS) { stage = 0; phase ^= 1; }
+            if (++stage == nst) { stage = 0; phase ^= 1; }
         }
         if (elect_one()) {
             if constexpr (CG == 1) umma_commit(&tfull[acc]);

@@ -54,6 +54,12 @@ __device__ __forceinline__ void tma_load_2d(uint32_t smem_dst, const void* desc,
         : "memory");
 }
 
+// L2 prefetch of a TMA box (no smem, no barrier): warms L2 ahead of the real load.
+__device__ __forceinline__ void tma_prefetch_2d(const void* desc, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];"
+                 :: "l"(reinterpret_cast<uint64_t>(desc)), "r"(c0), "r"(c1) : "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05
 template <int COLS>
 __device__ __forceinline__ void tmem_alloc(uint32_t* slot_smem) {
