@@ -38,14 +38,18 @@ CONFIGS = {
     "c3": (2048, 8192, 8192, "LLaMA-3-1B block shapes (d=2048, ffn=8192, 8192 tokens) bf16 fwd+bwd"),
     "c4": (4096, 14336, 16384, "LLaMA-3-8B block shapes (d=4096, ffn=14336, 16384 tokens) bf16 fwd+bwd"),
     "c5": (4096, 14336, 8192, "LLaMA-3-8B 4-block stack bf16 fwd+bwd, 8192 tokens/GPU/block (65536 over 8 GPUs)"),
+    # GQA extension (not a BASELINE config): the real LLaMA-3-8B projection, 8 KV heads of 128
+    "c4gqa": (4096, 14336, 16384, "LLaMA-3-8B block shapes with GQA q 4096 + k 1024 + v 1024 "
+                                  "(d=4096, ffn=14336, 16384 tokens) bf16 fwd+bwd"),
 }
+KV = {"c4gqa": 1024}   # k / v span width (default: d, the reference's packed 3d)
 BLOCKS = {"c5": 4}
 FP32 = {"c1"}          # BASELINE config 0 is the fp32 (SIM32) path
 
 
-def flops_per_token(d: int, inter: int) -> float:
-    """fwd+bwd = 3 x 2(d^2 + d*F + I*d + d*Q), F = 2I, Q = 3d."""
-    f, q = 2 * inter, 3 * d
+def flops_per_token(d: int, inter: int, kv: int | None = None) -> float:
+    """fwd+bwd = 3 x 2(d^2 + d*F + I*d + d*Q), F = 2I, Q = 3d; Q = d + 2kv with GQA."""
+    f, q = 2 * inter, d + 2 * (d if kv is None else kv)
     return 3 * 2.0 * (d * d + d * f + inter * d + d * q)
 
 
@@ -164,7 +168,7 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- workload
 
 
-def make_workload(cd, d, inter, m, start, device, seed=0, blocks=1, fp32=False):
+def make_workload(cd, d, inter, m, start, device, seed=0, blocks=1, fp32=False, kv=None):
     """Synthetic bf16 inputs and random-init weights (N(0, 0.02^2), gains 1 + 0.1 N).
 
     Weights are identical on every rank (same seed); activations differ per
@@ -185,15 +189,16 @@ def make_workload(cd, d, inter, m, start, device, seed=0, blocks=1, fp32=False):
         return cd.Vector.from_tensor(1.0 + 0.1 * torch.randn(n, generator=g, device=device), P)
 
     f = 2 * inter
+    qw = d + 2 * (d if kv is None else kv)
 
     def block():
         return cd.LayerWeights(w_out=w(d, d), gamma_ffn=gain(d), w_gate_up=w(d, f), w_down=w(inter, d),
-                               gamma_qkv=gain(d), w_qkv=w(d, 3 * d))
+                               gamma_qkv=gain(d), w_qkv=w(d, qw))
 
     weights = block() if blocks == 1 else [block() for _ in range(blocks)]
     acts = {name: w(m, width, scale=1.0, gen=gr) for name, width in
-            (("x", d), ("z", d), ("grad_qkv", 3 * d), ("grad_residual", d))}
-    cos, sin = cd.qkv_rope_tables(m, d, start=start, precision=P)
+            (("x", d), ("z", d), ("grad_qkv", qw), ("grad_residual", d))}
+    cos, sin = cd.qkv_rope_tables(m, d, start=start, precision=P, kv_width=kv)
     return weights, acts, cos, sin
 
 
@@ -223,7 +228,7 @@ class CpuOracle:
     """The reference algorithm on the host cores: the fused-order SIMBF16 oracle
     (oracle/coda_oracle.py, numpy/OpenBLAS using every core) on a token sample."""
 
-    def __init__(self, d, inter, sample_tokens, seed=0, fp32=False):
+    def __init__(self, d, inter, sample_tokens, seed=0, fp32=False, kv=None):
         import numpy as np
 
         from oracle import coda_oracle as O
@@ -231,11 +236,11 @@ class CpuOracle:
         self.O = O
         rng = np.random.default_rng(seed)
         self.mode = O.SIM32 if fp32 else O.SIMBF16
-        self.w = O.random_layer(rng, d, 2 * inter, self.mode, scale=0.02)
+        self.w = O.random_layer(rng, d, 2 * inter, self.mode, scale=0.02, kv_width=kv)
         self.m = sample_tokens
         self.x, self.z = (O.q(rng.standard_normal((self.m, d)), self.mode) for _ in range(2))
-        self.cos, self.sin = O.qkv_rope_tables(self.m, d, self.mode)
-        self.gq = O.q(rng.standard_normal((self.m, 3 * d)), self.mode)
+        self.cos, self.sin = O.qkv_rope_tables(self.m, d, self.mode, kv_width=kv)
+        self.gq = O.q(rng.standard_normal((self.m, d + 2 * (d if kv is None else kv))), self.mode)
         self.gres = O.q(rng.standard_normal((self.m, d)), self.mode)
 
     def step(self) -> float:
@@ -246,8 +251,8 @@ class CpuOracle:
         return time.perf_counter() - t0
 
 
-def cpu_oracle_tokens_per_s(d, inter, sample_tokens, seconds_budget=20.0, max_reps=5, fp32=False):
-    runner = CpuOracle(d, inter, sample_tokens, fp32=fp32)
+def cpu_oracle_tokens_per_s(d, inter, sample_tokens, seconds_budget=20.0, max_reps=5, fp32=False, kv=None):
+    runner = CpuOracle(d, inter, sample_tokens, fp32=fp32, kv=kv)
     times = []
     t_start = time.perf_counter()
     while True:
@@ -274,7 +279,7 @@ def reference_arm(args, rank, world):
     if rank != 0:
         return
     sample = min(args.cpu_sample, tokens)
-    runner = CpuOracle(d, inter, sample, fp32=args.config in FP32)
+    runner = CpuOracle(d, inter, sample, fp32=args.config in FP32, kv=KV.get(args.config))
     for _ in range(max(1, args.warmup)):
         runner.step()
     per_step = [runner.step() for _ in range(args.steps)]
@@ -312,13 +317,14 @@ def coda_arm(args, rank, world, local_rank):
     sh = parallel.shard(tokens, rank, world, args.scaling)
     m = sh.rows
     P = cd.PrecisionMode.SIMBF16
-    cfg = cd.PipelineConfig(hidden=d, ffn=2 * inter, precision=P)
+    kv = KV.get(args.config)
+    cfg = cd.PipelineConfig(hidden=d, ffn=2 * inter, precision=P, kv_width=kv)
     nblocks = BLOCKS.get(args.config, 1)
     fp32 = args.config in FP32
     if fp32:
         P = cd.PrecisionMode.SIM32
         cfg = cd.PipelineConfig(hidden=d, ffn=2 * inter, precision=P)
-    weights, acts, cos, sin = make_workload(cd, d, inter, m, sh.start, device, blocks=nblocks, fp32=fp32)
+    weights, acts, cos, sin = make_workload(cd, d, inter, m, sh.start, device, blocks=nblocks, fp32=fp32, kv=kv)
     hook = parallel.WgradAllReduce(dist, device) if dist is not None else None
 
     def step():
@@ -342,6 +348,15 @@ def coda_arm(args, rank, world, local_rank):
             step()
         torch.cuda.synchronize()
         torch.cuda.nvtx.range_pop()
+        # launch tags of one step, in order (tools/traffic_json.py maps ncu rows onto them)
+        rows = []
+        _native.record_tags(rows)
+        step()
+        _native.record_tags(None)
+        if rank == 0:
+            out = ROOT / "gpurun_out"
+            out.mkdir(exist_ok=True)
+            (out / f"launch_tags_{args.config}.json").write_text(json.dumps(rows))
         if dist is not None:
             dist.destroy_process_group()
         return
@@ -498,13 +513,14 @@ def coda_arm(args, rank, world, local_rank):
                     "frac": achieved / peak, "traffic": traffic, "kernel": top["name"],
                     "peak_kind": "measured sustained bf16 (MEASURED_PEAKS.json)",
                     "share_of_step": top["total_ms"] / sum(r["total_ms"] for r in prof.values())}
-    total_flops = flops_per_token(d, inter) * m * nblocks
+    total_flops = flops_per_token(d, inter, kv) * m * nblocks
     block_tflops = total_flops / (ms_step / 1e3) / 1e12
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         sample = min(args.cpu_sample, m)
-        tps, secs, reps = cpu_oracle_tokens_per_s(d, inter, sample, seconds_budget=20.0, max_reps=3, fp32=fp32)
+        tps, secs, reps = cpu_oracle_tokens_per_s(d, inter, sample, seconds_budget=20.0, max_reps=3, fp32=fp32,
+                                                  kv=kv)
         cpu = {"value": tps, "unit": "tokens/s", "cores": host_cores(), "kind": "port",
                "sample": f"{sample} tokens of the {args.config} block, fused-order "
                          f"{'SIM32' if fp32 else 'SIMBF16'} oracle, "
@@ -519,7 +535,7 @@ def coda_arm(args, rank, world, local_rank):
             "data": "synthetic (random-init weights, N(0,1) activations)",
             "config": {"workload": label, "blocks": nblocks, "tokens_per_gpu": m, "global_tokens": world * m,
                        "hidden": d,
-                       "intermediate": inter, "ffn_interleaved": 2 * inter, "qkv": 3 * d,
+                       "intermediate": inter, "ffn_interleaved": 2 * inter, "qkv": d + 2 * (d if kv is None else kv),
                        "parallelism": f"token-sharded dp{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (>=100 MB activations per launch)"},
             "block_tflops": block_tflops,

@@ -306,19 +306,30 @@ def combine_lse(partials, mode: str) -> np.ndarray:
 # ----------------------------------------------------------------------------- pipelines
 
 
-def qkv_rope_tables(m: int, hidden: int, mode: str, base: float = 10000.0, start: int = 0):
-    """(m, 3h) cos/sin: q and k share angles, v identity (kernels.py:156-206)."""
-    inv = base ** (-2.0 * np.arange(hidden // 2, dtype=np.float64) / hidden)
-    ang = (start + np.arange(m, dtype=np.float64))[:, None] * inv[None, :]
-    c = np.repeat(np.cos(ang), 2, axis=1)
-    s = np.repeat(np.sin(ang), 2, axis=1)
-    cos = np.concatenate([c, c, np.ones((m, hidden))], axis=1)
-    sin = np.concatenate([s, s, np.zeros((m, hidden))], axis=1)
+def qkv_rope_tables(m: int, hidden: int, mode: str, base: float = 10000.0, start: int = 0, kv_width=None):
+    """(m, h + 2kv) cos/sin: q and k rotate, v identity (kernels.py:156-206).
+
+    kv_width None (= hidden) is the reference's packed 3h layout, where q and k share
+    angles.  The GQA extension (no reference counterpart) rotates the k span with the
+    reference's rule applied to its own width (pair p of a width-w span turns by
+    t * base^(-2p/w)).
+    """
+    kv = hidden if kv_width is None else kv_width
+
+    def span(w):
+        inv = base ** (-2.0 * np.arange(w // 2, dtype=np.float64) / w)
+        ang = (start + np.arange(m, dtype=np.float64))[:, None] * inv[None, :]
+        return np.repeat(np.cos(ang), 2, axis=1), np.repeat(np.sin(ang), 2, axis=1)
+
+    cq, sq = span(hidden)
+    ck, sk = span(kv)
+    cos = np.concatenate([cq, ck, np.ones((m, kv))], axis=1)
+    sin = np.concatenate([sq, sk, np.zeros((m, kv))], axis=1)
     return q(cos, mode), q(sin, mode)
 
 
-def random_layer(rng: np.random.Generator, d: int, ffn: int, mode: str, scale: float = 0.2) -> dict:
-    """Weights in the reference draw order (kernels.py:750-767)."""
+def random_layer(rng: np.random.Generator, d: int, ffn: int, mode: str, scale: float = 0.2, kv_width=None) -> dict:
+    """Weights in the reference draw order (kernels.py:750-767); w_qkv is (d, d + 2 kv)."""
     mk = lambda *s: q(rng.standard_normal(s) * scale, mode)  # noqa: E731
     w = {}
     w["w_out"] = mk(d, d)
@@ -326,7 +337,7 @@ def random_layer(rng: np.random.Generator, d: int, ffn: int, mode: str, scale: f
     w["w_gate_up"] = mk(d, ffn)
     w["w_down"] = mk(ffn // 2, d)
     w["gamma_qkv"] = q(1.0 + 0.1 * rng.standard_normal(d), mode)
-    w["w_qkv"] = mk(d, 3 * d)
+    w["w_qkv"] = mk(d, d + 2 * (d if kv_width is None else kv_width))
     return w
 
 

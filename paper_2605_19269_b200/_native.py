@@ -186,12 +186,21 @@ def check(rc: int) -> None:
 
 _launches = 0
 _profile = None   # list of (tag, flops, start_event, end_event) while profiling
+_tags = None      # list of launch tags while recording (no events)
+
+
+def record_tags(rows) -> None:
+    """Start (rows = a list) or stop (None) recording the tag of every launch."""
+    global _tags
+    _tags = rows
 
 
 def call(name: str, *args, tag: str | None = None, flops: float = 0.0) -> None:
     """Invoke one C-ABI entry point; every call enqueues exactly one kernel."""
     global _launches
     lib = load()
+    if _tags is not None:
+        _tags.append(tag or name)
     if _profile is not None:
         import torch
 

@@ -74,6 +74,9 @@ class PipelineConfig:
     precision: PrecisionMode = PrecisionMode.EXACT64
     eps: float = 1e-6
     rope_base: float = 10000.0
+    # GQA extension (no reference counterpart): width of each of the k and v spans of the
+    # packed projection.  None = hidden, the reference's packed (q, k, v) of width 3*hidden.
+    kv_width: Optional[int] = None
 
     def __post_init__(self):
         if self.hidden <= 0:
@@ -86,10 +89,21 @@ class PipelineConfig:
             raise ConfigError("tile parameters must be positive")
         if self.eps <= 0:
             raise ConfigError("eps must be positive")
+        if self.kv_width is not None and (self.kv_width <= 0 or self.kv_width % 2):
+            raise ConfigError(f"kv width must be positive and even, got {self.kv_width}")
 
     @property
     def ffn_resolved(self) -> int:
         return self.ffn if self.ffn is not None else ffn_width(self.hidden)
+
+    @property
+    def kv_resolved(self) -> int:
+        return self.hidden if self.kv_width is None else self.kv_width
+
+    @property
+    def qkv_width(self) -> int:
+        """Packed projection width: q (hidden) + k + v (kv each); 3*hidden by default."""
+        return self.hidden + 2 * self.kv_resolved
 
     @property
     def tile_shape(self) -> TileShape:
@@ -162,16 +176,23 @@ def rope_tables(m: int, width: int, *, base: float = 10000.0, start: int = 0,
 
 
 def qkv_rope_tables(m: int, hidden: int, *, base: float = 10000.0, start: int = 0,
-                    precision: PrecisionMode = PrecisionMode.EXACT64) -> tuple[DenseMatrix, DenseMatrix]:
-    """Tables for packed (q, k, v): q and k share angles, v is identity (kernels.py:184-206)."""
+                    precision: PrecisionMode = PrecisionMode.EXACT64,
+                    kv_width: Optional[int] = None) -> tuple[DenseMatrix, DenseMatrix]:
+    """Tables for packed (q, k, v): q and k rotate, v is identity (kernels.py:184-206).
+
+    kv_width None (= hidden) is the reference layout, q and k sharing angles.  With a GQA
+    kv_width the k span rotates by the reference rule applied to its own width.
+    """
+    kv = hidden if kv_width is None else kv_width
     c_h, s_h = rope_tables(m, hidden, base=base, start=start, precision=precision)
+    c_k, s_k = (c_h, s_h) if kv == hidden else rope_tables(m, kv, base=base, start=start, precision=precision)
     dev = c_h.tensor.device
     out = []
-    for src, fill in ((c_h, 1.0), (s_h, 0.0)):
-        full = alloc_matrix(m, 3 * hidden, precision.torch_dtype, dev)
+    for src, srck, fill in ((c_h, c_k, 1.0), (s_h, s_k, 0.0)):
+        full = alloc_matrix(m, hidden + 2 * kv, precision.torch_dtype, dev)
         full[:, :hidden] = src.tensor
-        full[:, hidden:2 * hidden] = src.tensor
-        full[:, 2 * hidden:] = fill
+        full[:, hidden:hidden + kv] = srck.tensor
+        full[:, hidden + kv:] = fill
         out.append(DenseMatrix._wrap(full, precision))
     return out[0], out[1]
 
@@ -405,17 +426,17 @@ class LayerWeights:
     w_gate_up: DenseMatrix    # (d, ffn) interleaved gate/up
     w_down: DenseMatrix       # (ffn/2, d)
     gamma_qkv: Vector         # (d,)
-    w_qkv: DenseMatrix        # (d, 3d)
+    w_qkv: DenseMatrix        # (d, d + 2 kv) = (d, 3d) for the reference layout
 
     def check(self, config: PipelineConfig) -> None:
-        d, f = config.hidden, config.ffn_resolved
+        d, f, qw = config.hidden, config.ffn_resolved, config.qkv_width
         for name, got, want in (
             ("w_out", self.w_out.shape, (d, d)),
             ("gamma_ffn", (len(self.gamma_ffn),), (d,)),
             ("w_gate_up", self.w_gate_up.shape, (d, f)),
             ("w_down", self.w_down.shape, (f // 2, d)),
             ("gamma_qkv", (len(self.gamma_qkv),), (d,)),
-            ("w_qkv", self.w_qkv.shape, (d, 3 * d)),
+            ("w_qkv", self.w_qkv.shape, (d, qw)),
         ):
             if got != want:
                 raise DimensionError(f"{name} has shape {got}, expected {want}")
@@ -433,7 +454,7 @@ class LayerWeights:
         w_gu = mk(d, f)
         w_down = mk(f // 2, d)
         g_qkv = Vector.from_array(1.0 + 0.1 * rng.standard_normal(d), p)
-        w_qkv = mk(d, 3 * d)
+        w_qkv = mk(d, config.qkv_width)
         return cls(w_out=w_out, gamma_ffn=g_ffn, w_gate_up=w_gu, w_down=w_down, gamma_qkv=g_qkv, w_qkv=w_qkv)
 
 
@@ -453,14 +474,14 @@ class LayerTape:
 
     def check(self, config: PipelineConfig) -> None:
         m, d = self.x.shape
-        f = config.ffn_resolved
+        f, qw = config.ffn_resolved, config.qkv_width
         for name, got, want in (
             ("pre_norm_a", self.pre_norm_a.shape, (m, d)),
             ("preact", self.preact.shape, (m, f)),
             ("pre_norm_b", self.pre_norm_b.shape, (m, d)),
-            ("qkv", self.qkv.shape, (m, 3 * d)),
-            ("cos", self.cos.shape, (m, 3 * d)),
-            ("sin", self.sin.shape, (m, 3 * d)),
+            ("qkv", self.qkv.shape, (m, qw)),
+            ("cos", self.cos.shape, (m, qw)),
+            ("sin", self.sin.shape, (m, qw)),
         ):
             if got != want:
                 raise TapeError(f"tape entry {name} has shape {got}, expected {want}")

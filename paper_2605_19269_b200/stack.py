@@ -17,6 +17,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
+from .errors import ConfigError
 from .kernels import LayerGrads, LayerTape, LayerWeights, PipelineConfig, layer_backward, layer_forward
 from .tensors import DenseMatrix, alloc_matrix
 
@@ -33,8 +34,14 @@ def v_span(qkv: DenseMatrix, d: int) -> DenseMatrix:
     return DenseMatrix._wrap(qkv.tensor[:, 2 * d:3 * d], qkv.precision)
 
 
+def _check_glue(config: PipelineConfig) -> None:
+    if config.kv_resolved != config.hidden:
+        raise ConfigError("the identity-attention stack glue needs a V span of hidden width (kv_width=None)")
+
+
 def stack_forward(x: DenseMatrix, z: DenseMatrix, weights: Sequence[LayerWeights], cos: DenseMatrix,
                   sin: DenseMatrix, *, config: PipelineConfig) -> StackForwardResult:
+    _check_glue(config)
     d = config.hidden
     tapes: list[LayerTape] = []
     fwd = None
@@ -48,6 +55,7 @@ def stack_forward(x: DenseMatrix, z: DenseMatrix, weights: Sequence[LayerWeights
 def stack_backward(grad_qkv: DenseMatrix, grad_residual: Optional[DenseMatrix], result: StackForwardResult,
                    weights: Sequence[LayerWeights], *, config: PipelineConfig, wgrad_hook=None) -> list[LayerGrads]:
     """Gradients of every block, returned in block order (index 0 = first block)."""
+    _check_glue(config)
     d = config.hidden
     grads: list[LayerGrads] = [None] * len(weights)
     gq, gr = grad_qkv, grad_residual

@@ -224,3 +224,41 @@ def test_quantize_matches_oracle_rounding():
     x = np.random.default_rng(0).standard_normal(10000) * 100
     assert np.array_equal(cd.quantize(x, cd.PrecisionMode.SIMBF16), O.q(x, O.SIMBF16))
     assert cd.ffn_width(4096) == 11008
+
+
+def test_gqa_config_and_tables():
+    """GQA extension: kv_width validation, projection width, table spans (oracle, host-only)."""
+    import paper_2605_19269_b200 as cd
+    from oracle import coda_oracle as O
+
+    cfg = cd.PipelineConfig(hidden=256, ffn=1024)
+    assert cfg.qkv_width == 768 and cfg.kv_resolved == 256
+    g = cd.PipelineConfig(hidden=256, ffn=1024, kv_width=64)
+    assert g.qkv_width == 384
+    for bad in (0, -2, 63):
+        with pytest.raises(cd.ConfigError):
+            cd.PipelineConfig(hidden=256, kv_width=bad)
+    m, d, kv = 5, 16, 4
+    c, s = O.qkv_rope_tables(m, d, O.EXACT64, kv_width=kv)
+    c0, s0 = O.qkv_rope_tables(m, d, O.EXACT64)
+    assert c.shape == (m, d + 2 * kv)
+    np.testing.assert_array_equal(c[:, :d], c0[:, :d])          # q span unchanged
+    ck, sk = O.qkv_rope_tables(m, kv, O.EXACT64)                 # k span: the rule at its own width
+    np.testing.assert_array_equal(c[:, d:d + kv], ck[:, :kv])
+    np.testing.assert_array_equal(s[:, d:d + kv], sk[:, :kv])
+    assert np.all(c[:, d + kv:] == 1.0) and np.all(s[:, d + kv:] == 0.0)   # v identity
+    # the fused-order oracle and the float64 canonical chain agree at a GQA width
+    rng = np.random.default_rng(3)
+    mode = O.SIM32
+    m, d, ffn, kv = 32, 32, 96, 8
+    w = O.random_layer(rng, d, ffn, mode, kv_width=kv)
+    x, z = (O.q(rng.standard_normal((m, d)), mode) for _ in range(2))
+    cos, sin = O.qkv_rope_tables(m, d, mode, kv_width=kv)
+    gq, gr = O.q(rng.standard_normal((m, d + 2 * kv)), mode), O.q(rng.standard_normal((m, d)), mode)
+    of = O.layer_forward(x, z, w, cos, sin, mode)
+    ob = O.layer_backward(gq, of, w, mode, grad_residual=gr)
+    ref = O.layer_ref_forward(x, z, w, cos, sin)
+    refb = O.layer_ref_backward(gq, gr, ref, x, w, cos, sin)
+    assert O.rel_error(of["qkv"], ref["qkv"]) < 1e-5
+    for k in O.GRAD_KEYS:
+        assert O.rel_error(ob[k], refb[k]) < 1e-5, k
