@@ -201,7 +201,10 @@ int coda_convert_f32_bf16(const coda_tensor_t* src, coda_tensor_t* dst, void* st
 /* Engine options (defaults from the environment): "pdl" 0/1 programmatic
  * dependent launch, "cg" 1/2 CTA-pair mainloop, "generic" 0/1 force the generic
  * epilogue interpreter, "raster" >= 1 raster group, "split" 0/1 wave-tail split-K,
- * "split_min_k" smallest K that is split.  Process-wide. */
+ * "split_min_k" smallest K that is split, "ring" operand-ring stages in use
+ * (0 = compiled depth), "prefetch" 0..64 L2 prefetch distance in k-blocks (0 = off,
+ * measured slower), "ablate" measurement-only epilogue ablations (1 = skip side
+ * loads, 2 = skip TMA stores; results are invalid).  Process-wide. */
 int coda_set_option(const char* name, int value);
 
 /* Number of SMs the persistent kernel sizes its grid for (0 if no device). */

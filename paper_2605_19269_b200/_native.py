@@ -215,7 +215,8 @@ def call(name: str, *args, tag: str | None = None, flops: float = 0.0) -> None:
 
 
 def set_option(name: str, value: int) -> None:
-    """Process-wide engine option ("pdl", "cg", "generic", "raster"); see include/coda.h."""
+    """Process-wide engine option ("pdl", "cg", "generic", "raster", "split", "split_min_k",
+    "ring", "prefetch", "ablate"); see include/coda.h."""
     check(load().coda_set_option(name.encode(), int(value)))
 
 

@@ -262,3 +262,12 @@ def test_gqa_config_and_tables():
     assert O.rel_error(of["qkv"], ref["qkv"]) < 1e-5
     for k in O.GRAD_KEYS:
         assert O.rel_error(ob[k], refb[k]) < 1e-5, k
+
+
+def test_engine_options_validated():
+    """coda_set_option rejects unknown names and out-of-range values (no GPU needed)."""
+    for name, bad in (("cg", 3), ("raster", 0), ("prefetch", -1), ("prefetch", 65), ("no_such_option", 1)):
+        with pytest.raises(cd.TileFuseError):
+            nat.set_option(name, bad)
+    for name, ok in (("ring", 0), ("prefetch", 0), ("ablate", 0), ("raster", 8), ("cg", 2)):
+        nat.set_option(name, ok)

@@ -23,14 +23,19 @@ def main():
     ap.add_argument("--shape", action="append", required=True, help="m,n,k[,ta,tb]")
     ap.add_argument("--variant", action="append", required=True)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--pad", type=int, default=0, help="extra elements per row of A and B (row-pitch experiment)")
     args = ap.parse_args()
     P = cd.PrecisionMode.SIMBF16
     for spec in args.shape:
         parts = [int(x) for x in spec.split(",")]
         m, n, k = parts[:3]
         ta, tb = (bool(parts[3]), bool(parts[4])) if len(parts) == 5 else (False, False)
-        A = torch.randn((k, m) if ta else (m, k), device="cuda").to(torch.bfloat16)
-        B = torch.randn((n, k) if tb else (k, n), device="cuda").to(torch.bfloat16)
+        def mk(r, c):
+            t = torch.randn((r, c + args.pad), device="cuda").to(torch.bfloat16)
+            return t[:, :c] if args.pad else t
+
+        A = mk(*((k, m) if ta else (m, k)))
+        B = mk(*((n, k) if tb else (k, n)))
         a, b = cd.DenseMatrix.from_tensor(A, P), cd.DenseMatrix.from_tensor(B, P)
         prob = cd.GemmProblem(m=m, n=n, k=k, trans_a=ta, trans_b=tb, precision=P)
         graphs = []
