@@ -204,9 +204,7 @@ int coda_convert_f32_bf16(const coda_tensor_t* src, coda_tensor_t* dst, void* st
  * "split_min_k" smallest K that is split, "ring" operand-ring stages in use
  * (0 = compiled depth), "prefetch" 0..64 L2 prefetch distance in k-blocks (0 = off,
  * measured slower), "ablate" measurement-only epilogue ablations (1 = skip side
- * loads, 2 = skip TMA stores; results are invalid), "epi_sleep" ns back-off of the
- * epilogue's accumulator wait, "sched" 1 = dynamic atomic-claim tile scheduler
- * (bit-identical results; 0 = static round-robin, the default).  Process-wide. */
+ * loads, 2 = skip TMA stores; results are invalid).  Process-wide. */
 int coda_set_option(const char* name, int value);
 
 /* Number of SMs the persistent kernel sizes its grid for (0 if no device). */

@@ -216,7 +216,7 @@ def call(name: str, *args, tag: str | None = None, flops: float = 0.0) -> None:
 
 def set_option(name: str, value: int) -> None:
     """Process-wide engine option ("pdl", "cg", "generic", "raster", "split", "split_min_k",
-    "ring", "prefetch", "ablate", "epi_sleep", "sched"); see include/coda.h."""
+    "ring", "prefetch", "ablate"); see include/coda.h."""
     check(load().coda_set_option(name.encode(), int(value)))
 
 

@@ -178,11 +178,8 @@ struct Options {
     int prefetch = 0;     // L2 prefetch distance (k-blocks beyond the smem ring)
     int ablate = 0;       // measurement-only epilogue ablations (results invalid)
     int ring = 0;         // operand ring stages in use (0 = the compiled depth)
-    int epi_sleep = 0;    // epilogue accumulator-wait back-off in ns (0 = spin)
-    int sched = 0;        // 1 = dynamic (atomic-claim) tile scheduler, 0 = static round-robin
     Options() {
         if (const char* e = getenv("CODA_PREFETCH")) prefetch = atoi(e);
-        if (const char* e = getenv("CODA_SCHED")) sched = atoi(e) != 0;
         if (const char* e = getenv("CODA_PDL")) pdl = e[0] != '0';
         if (const char* e = getenv("CODA_CG")) cg = e[0] == '1' ? 1 : 2;
         if (const char* e = getenv("CODA_FORCE_GENERIC")) generic = e[0] && e[0] != '0';
@@ -328,10 +325,6 @@ int launch_fast(int fl, int cg, const CUtensorMap& ma, const CUtensorMap& mb, co
 // Raster group: m-tiles swept together across all n-tiles.  8 (pair) m-tiles was
 // measured best on the C4 block (sweep 4/8/16/32/64, profiles/r01_raster_sweep.md);
 // CODA_RASTER_GROUP overrides it for experiments.
-// Workspace layout: [0, kSchedOffset) split-K flags, [kSchedOffset, 64 KiB) scheduler
-// counters, [64 KiB, ...) split-K partial accumulators.  All zero between launches.
-constexpr int kSchedOffset = (64 << 10) - 256;
-
 int raster_group(int ntm, int tile_m, int64_t k) {
     (void)tile_m;
     (void)k;
@@ -408,11 +401,6 @@ int coda_set_option(const char* name, int value) {
     else if (n == "split_min_k") opts().split_min_k = value;
     else if (n == "ablate") opts().ablate = value;
     else if (n == "ring") opts().ring = value;
-    else if (n == "sched") opts().sched = value != 0;
-    else if (n == "epi_sleep") {
-        if (value < 0 || value > 100000) return fail(CODA_E_CONFIG, "epi_sleep must be in [0, 100000] ns");
-        opts().epi_sleep = value;
-    }
     else if (n == "prefetch") {
         if (value < 0 || value > 64) return fail(CODA_E_CONFIG, "prefetch distance must be in [0, 64]");
         opts().prefetch = value;
@@ -583,7 +571,7 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
             if (sp > 16) sp = 16;
             const int64_t tile_bytes = (int64_t)cg * coda::BM * coda::BN * 4;
             while (sp >= 2 && ((int64_t)r * (sp - 1) * tile_bytes > pr->workspace_bytes - (64 << 10) ||
-                               (int64_t)r * (sp - 1) * cg * coda::FAST_EPI_WARPS * 4 > kSchedOffset))
+                               (int64_t)r * (sp - 1) * cg * coda::FAST_EPI_WARPS * 4 > (64 << 10)))
                 --sp;
             if (sp >= 2) {
                 F.mp.full_tiles = ntiles - r;
@@ -597,10 +585,6 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         F.acc_in = P.acc_in;
         F.ld_acc = P.ld_acc;
         F.ablate = opts().ablate;
-        // dynamic scheduler counters live at the end of the 64 KiB flag region of the workspace
-        if (opts().sched && pr->workspace && pr->workspace_bytes >= (64 << 10))
-            F.sched = reinterpret_cast<int*>(static_cast<char*>(pr->workspace) + kSchedOffset);
-        F.epi_sleep_ns = opts().epi_sleep;
         F.rope_sign = 1.0f;
         int aux_slot = -1;
         for (int s = 0; s < nsteps; ++s) {

@@ -86,10 +86,6 @@ struct FastParams {
     float* ws;
     int* flags;
     int ablate;   // measurement-only ablations (results invalid): 1 = no side loads, 2 = no TMA stores
-    int epi_sleep_ns;   // epilogue back-off while waiting for an accumulator (0 = spin)
-    // dynamic tile scheduler: [0] claim counter, [1] finished-CTA counter; both zero
-    // between launches (the last CTA to finish resets them).  nullptr = static.
-    int* sched;
 };
 
 __device__ __forceinline__ bool item_runs_program(const MainParams& mp, const Work& w) {
@@ -127,7 +123,7 @@ template <int CG, int FL>
 constexpr size_t fast_smem_bytes() {
     using FG = FastGeom<CG, FL>;
     return (size_t)FG::RING + (size_t)FAST_EPI_WARPS * STG_BYTES + FG::SIDE_TOTAL + COLRED_BYTES +
-           (2 * FG::NS + 4 + FAST_EPI_WARPS + 2 * SCHED_SLOTS) * 8 + SCHED_SLOTS * 4 + 16;
+           (2 * FG::NS + 4 + FAST_EPI_WARPS) * 8 + 16;
 }
 
 // One thread's row of a 32-row side box: RB bytes (64: SWIZZLE_64B, 128: SWIZZLE_128B) of bf16.
@@ -292,10 +288,7 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     uint64_t* tfull = empty + NS;
     uint64_t* tempty = tfull + 2;
     uint64_t* sidebar = tempty + 2;
-    uint64_t* sfull = sidebar + FAST_EPI_WARPS;
-    uint64_t* sempty = sfull + SCHED_SLOTS;
-    int* sring = reinterpret_cast<int*>(sempty + SCHED_SLOTS);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sring + SCHED_SLOTS);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sidebar + FAST_EPI_WARPS);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -315,11 +308,6 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             mbar_init(&tempty[s], FAST_EPI_WARPS * CG);   // one arrival per epilogue warp of the pair
         }
         for (int s = 0; s < FAST_EPI_WARPS; ++s) mbar_init(&sidebar[s], 1);
-        for (int s = 0; s < SCHED_SLOTS; ++s) {
-            mbar_init(&sfull[s], 1);
-            // readers: leader MMA warp + epilogue warps (+ peer producer + peer epilogue warps)
-            mbar_init(&sempty[s], CG == 1 ? 1 + FAST_EPI_WARPS : 2 * (1 + FAST_EPI_WARPS));
-        }
         fence_mbar_init();
         tma_prefetch_desc(&tma_a);
         tma_prefetch_desc(&tma_b);
@@ -344,27 +332,10 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     griddep_launch_dependents();
     griddep_wait();
 
-    auto make_sched = [&](int role) {
-        Sched sc = sched_static(unit, nunits);
-        if (P.sched != nullptr) {
-            sc.ctr = P.sched;
-            sc.ring = sring;
-            sc.sfull = sfull;
-            sc.sempty = sempty;
-            sc.slot = 0;
-            sc.phase = 0;
-            sc.role = role;
-            sc.cg = CG;
-            sc.nitems = mp.nitems;
-            sc.started = false;
-            sc.done = false;
-        }
-        return sc;
-    };
     if (warp == 0) {
-        producer_loop<CG, NS>(mp, &tma_a, &tma_b, sA, sB, full, empty, rank, make_sched(rank == 0 ? 0 : 2));
+        producer_loop<CG, NS>(mp, &tma_a, &tma_b, sA, sB, full, empty, rank, unit, nunits);
     } else if (warp == 1) {
-        if (rank == 0) mma_loop<CG, NS>(mp, tmem_base, sA, sB, full, empty, tfull, tempty, make_sched(1));
+        if (rank == 0) mma_loop<CG, NS>(mp, tmem_base, sA, sB, full, empty, tfull, tempty, unit, nunits);
     } else {
         const int ew = warp - 2;            // 0..7
         const int q = warp & 3;             // TMEM lane quadrant
@@ -392,17 +363,12 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 if (FL & (F_ROPE | F_RMSBWD_ACC)) tma_load_2d(sbase + 2048, &tma_s1, x, y, &sidebar[ew]);
             }
         };
-        Sched sc = make_sched(rank == 0 ? 1 : 2);
-        int cur = sched_next(sc);
-        if (FG::SIDE && lane == 0 && cur < mp.nitems) {
-            const Work w0 = work_item(mp, cur);
+        if (FG::SIDE && lane == 0 && unit < mp.nitems) {
+            const Work w0 = work_item(mp, unit);
             if (item_runs_program(mp, w0)) side_issue(w0.tm, w0.tn, 0);
         }
         const int nparts = mp.split - 1;   // partial pieces per split tile
-        while (cur < mp.nitems) {
-            const int i = cur;
-            const int nxt = sched_next(sc);   // one-item lookahead (side-operand prefetch)
-            cur = nxt;
+        for (int i = unit; i < mp.nitems; i += nunits) {
             const Work w = work_item(mp, i);
             const int tm = w.tm, tn = w.tn;
             const int m0 = tm * G::TILE_M + rank * BM;
@@ -429,13 +395,6 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
                     else mbar_arrive_leader(&tempty[acc]);
                     flag_release(P.flags + ((w.tail_idx * nparts + w.piece) * CG + rank) * FAST_EPI_WARPS + ew);
-                    // this item loaded no side operands, so chunk 0 of the next program item
-                    // must be requested here (the dynamic scheduler can follow a K piece with
-                    // a whole tile; the static order never does)
-                    if (FG::SIDE && nxt < mp.nitems) {
-                        const Work wn = work_item(mp, nxt);
-                        if (item_runs_program(mp, wn)) side_issue(wn.tm, wn.tn, 0);
-                    }
                 }
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
@@ -468,7 +427,7 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
 
             // CTA-scope wait: the accumulator is read through tcgen05.ld after the fence below;
             // a cluster-scope acquire would emit an L1 invalidate (CCTL.IVALL) on every poll.
-            mbar_wait_backoff(&tfull[acc], acc_phase, (uint32_t)P.epi_sleep_ns);
+            mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + h * 128);
 
@@ -516,8 +475,8 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     if (lane == 0) {
                         if (c < 3) {
                             side_issue(tm, tn, c + 1);
-                        } else if (nxt < mp.nitems) {
-                            const Work wn = work_item(mp, nxt);
+                        } else if (i + nunits < mp.nitems) {
+                            const Work wn = work_item(mp, i + nunits);
                             if (item_runs_program(mp, wn)) side_issue(wn.tm, wn.tn, 0);
                         }
                     }
@@ -703,15 +662,6 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     tc_fence_before();
     __syncthreads();
     if constexpr (CG == 2) cluster_sync_all();   // both CTAs done with the paired TMEM
-    if (P.sched != nullptr && threadIdx.x == 0) {
-        // every claim of this CTA is done; the last CTA of the launch re-arms the counters
-        __threadfence();
-        if (atomicAdd(P.sched + 1, 1) == (int)gridDim.x - 1) {
-            atomicExch(P.sched, 0);
-            atomicExch(P.sched + 1, 0);
-            __threadfence();
-        }
-    }
     if (warp == 1) {
         tc_fence_after();
         if constexpr (CG == 1) tmem_dealloc<TMEM_COLS>(tmem_base);

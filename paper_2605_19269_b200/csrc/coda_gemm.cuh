@@ -328,9 +328,9 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
     auto tile_mn = [&](int t, int& tm, int& tn) { tile_coord(mp, t, tm, tn); };
 
     if (warp == 0) {
-        producer_loop<1>(mp, &tma_a, &tma_b, sA, sB, full, empty, 0, sched_static(blockIdx.x, gridDim.x));
+        producer_loop<1>(mp, &tma_a, &tma_b, sA, sB, full, empty, 0, blockIdx.x, gridDim.x);
     } else if (warp == 1) {
-        mma_loop<1>(mp, tmem_base, sA, sB, full, empty, tfull, tempty, sched_static(blockIdx.x, gridDim.x));
+        mma_loop<1>(mp, tmem_base, sA, sB, full, empty, tfull, tempty, blockIdx.x, gridDim.x);
     } else {
         // ------------------------------------------------ epilogue
         const int q = warp & 3;                 // TMEM lane quadrant this warp may read

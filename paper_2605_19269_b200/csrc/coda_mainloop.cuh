@@ -90,130 +90,12 @@ __device__ __forceinline__ void tile_coord(const MainParams& mp, int t, int& tm,
     tn = r / gs;
 }
 
-// ------------------------------------------------------------------ work scheduling
-// Static: unit u takes items u, u + nunits, ...  Dynamic: the leader CTA's producer
-// warp claims items from a global counter (atomicAdd) and publishes each claim
-// through a SCHED_SLOTS-deep smem ring (and, for CTA pairs, into the peer CTA's ring
-// with a remote store + remote mbarrier arrive); every other role of both CTAs reads
-// the ring in order and releases the slot on the leader's `sempty` barrier.  A CTA
-// that starts late (its SM still busy with another kernel, e.g. a collective on a
-// side stream) simply claims fewer items instead of delaying the whole launch.
-constexpr int SCHED_SLOTS = 4;
-// readers per slot: the leader's MMA warp + FAST epilogue warps (+ the peer's producer
-// and epilogue warps for CTA pairs); set by the kernel that owns the ring
-struct Sched {
-    int unit, nunits, last;     // static mode
-    int* ctr;                   // global claim counter; nullptr = static mode
-    int* ring;                  // this CTA's smem ring
-    uint64_t* sfull;            // this CTA's "slot published" barriers
-    uint64_t* sempty;           // this CTA's "slot consumed" barriers (used by the claimer)
-    int slot;
-    uint32_t phase;
-    int role;                   // 0 = claimer (leader producer), 1 = reader in the leader, 2 = reader in the peer
-    int cg;
-    // claimer: items are published one ahead of the caller (claim latency hidden behind
-    // a whole tile); `ahead` = published but not yet returned, `fut` = claim in flight
-    int ahead, fut, nitems;
-    bool started, done;
-};
-
-__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
-    asm volatile("st.shared::cluster.u32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(addr) : "memory");
-}
-
-__device__ __forceinline__ Sched sched_static(int unit, int nunits) {
-    Sched s{};
-    s.unit = unit;
-    s.nunits = nunits;
-    s.last = unit - nunits;
-    s.ctr = nullptr;
-    return s;
-}
-
-// claimer: publish item t in the next ring slot (this CTA and, for pairs, the peer)
-__device__ __forceinline__ void sched_publish(Sched& s, int t) {
-    mbar_wait_cluster(&s.sempty[s.slot], s.phase ^ 1);   // every reader is done with this slot
-    if ((threadIdx.x & 31) == 0) {
-        s.ring[s.slot] = t;
-        mbar_arrive(&s.sfull[s.slot]);
-        if (s.cg == 2) {
-            st_cluster_u32(mapa_rank(smem_u32(&s.ring[s.slot]), 1), (uint32_t)t);
-            mbar_arrive_remote(mapa_rank(smem_u32(&s.sfull[s.slot]), 1));
-        }
-    }
-    __syncwarp();
-    if (++s.slot == SCHED_SLOTS) { s.slot = 0; s.phase ^= 1; }
-}
-
-// claimer: lane 0 claims, every lane gets the value
-__device__ __forceinline__ int sched_claim(Sched& s) {
-    int t = 0;
-    if ((threadIdx.x & 31) == 0) t = atomicAdd(s.ctr, 1);
-    return __shfl_sync(0xffffffffu, t, 0);
-}
-
-// Next item index for this warp (warp-uniform; call with the whole warp converged).
-// Returns a value >= nitems once the work is exhausted.
-__device__ __forceinline__ int sched_next(Sched& s) {
-    if (s.ctr == nullptr) {
-        s.last += s.nunits;
-        return s.last;
-    }
-    const int lane = threadIdx.x & 31;
-    int t;
-    if (s.role == 0) {
-        if (!s.started) {
-            s.started = true;
-            t = sched_claim(s);
-            sched_publish(s, t);
-            s.done = t >= s.nitems;
-            s.ahead = t;
-            if (!s.done) {
-                s.ahead = sched_claim(s);
-                sched_publish(s, s.ahead);
-                s.done = s.ahead >= s.nitems;
-                if (!s.done && lane == 0) s.fut = atomicAdd(s.ctr, 1);   // next claim in flight
-            }
-            return t;
-        }
-        t = s.ahead;
-        if (!s.done) {
-            // the claim issued one call ago has long returned: publish it, start the next
-            const int f = __shfl_sync(0xffffffffu, s.fut, 0);
-            sched_publish(s, f);
-            s.ahead = f;
-            s.done = f >= s.nitems;
-            if (!s.done && lane == 0) s.fut = atomicAdd(s.ctr, 1);
-        }
-        return t;
-    }
-    if (s.role == 2) mbar_wait_cluster(&s.sfull[s.slot], s.phase);
-    else mbar_wait(&s.sfull[s.slot], s.phase);
-    t = *reinterpret_cast<volatile int*>(&s.ring[s.slot]);
-    __syncwarp();
-    if (lane == 0) {
-        if (s.role == 2) mbar_arrive_remote(mapa_rank(smem_u32(&s.sempty[s.slot]), 0));
-        else mbar_arrive(&s.sempty[s.slot]);
-    }
-    __syncwarp();
-    if (++s.slot == SCHED_SLOTS) { s.slot = 0; s.phase ^= 1; }
-    return t;
-}
-
 // TMA producer (one warp per CTA, warp-uniform control flow; one elected lane
 // issues): fills this CTA's smem ring for every tile it owns.
 template <int CG, int NS = Geom<CG>::NSTAGE>
 __device__ __forceinline__ void producer_loop(const MainParams& mp, const CUtensorMap* tma_a,
                                               const CUtensorMap* tma_b, uint8_t* sA, uint8_t* sB,
-                                              uint64_t* full, uint64_t* empty, int rank, Sched sc) {
+                                              uint64_t* full, uint64_t* empty, int rank, int unit, int nunits) {
     using G = Geom<CG>;
     int stage = 0;
     uint32_t phase = 0;
@@ -235,8 +117,7 @@ __device__ __forceinline__ void producer_loop(const MainParams& mp, const CUtens
         }
     };
     auto prefetch = [&](int, const CUtensorMap* map, int c0, int c1) { tma_prefetch_2d(map, c0, c1); };
-    const int pf = sc.ctr == nullptr ? mp.prefetch : 0;   // prefetch needs the static item order
-    const int unit = sc.unit, nunits = sc.nunits;
+    const int pf = mp.prefetch;
     if (pf > 0 && unit < mp.nitems && elect_one()) {
         // warm L2 for the first k-blocks this unit will load beyond the ring
         const Work w = work_item(mp, unit);
@@ -244,7 +125,7 @@ __device__ __forceinline__ void producer_loop(const MainParams& mp, const CUtens
         for (int kb = w.kb0 + nst; kb < w.kb1 && kb < w.kb0 + nst + pf; ++kb) boxes(prefetch, m0, nb0, kb);
     }
     __syncwarp();
-    for (int i = sched_next(sc); i < mp.nitems; i = sched_next(sc)) {
+    for (int i = unit; i < mp.nitems; i += nunits) {
         const Work w = work_item(mp, i);
         const int m0 = w.tm * G::TILE_M + rank * BM;
         const int nb0 = w.tn * BN + rank * G::B_COLS;
@@ -287,7 +168,7 @@ __device__ __forceinline__ void producer_loop(const MainParams& mp, const CUtens
 template <int CG, int NS = Geom<CG>::NSTAGE>
 __device__ __forceinline__ void mma_loop(const MainParams& mp, uint32_t tmem_base, uint8_t* sA, uint8_t* sB,
                                          uint64_t* full, uint64_t* empty, uint64_t* tfull, uint64_t* tempty,
-                                         Sched sc) {
+                                         int unit, int nunits) {
     using G = Geom<CG>;
     // kind::f16 instruction descriptor: D f32, A/B bf16, majorness, N>>3, M>>4.
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)mp.a_mn << 15) |
@@ -305,7 +186,7 @@ __device__ __forceinline__ void mma_loop(const MainParams& mp, uint32_t tmem_bas
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int i = sched_next(sc); i < mp.nitems; i = sched_next(sc)) {
+    for (int i = unit; i < mp.nitems; i += nunits) {
         const Work w = work_item(mp, i);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();

@@ -32,14 +32,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     while (!mbar_try_wait(a, parity)) { }
 }
-// Wait with a nanosleep back-off between polls (for waits expected to be long,
-// e.g. the epilogue waiting out a whole mainloop); ns = 0 polls like mbar_wait.
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
-    const uint32_t a = smem_u32(bar);
-    while (!mbar_try_wait(a, parity)) {
-        if (ns) __nanosleep(ns);
-    }
-}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
 }

@@ -269,48 +269,3 @@ def test_tail_split_matches_unsplit(cuda_ready):
         assert np.array_equal(y, y2), f"output {i}: split launch not deterministic"
         assert O.rel_error(y, x) < 5e-3, (i, O.rel_error(y, x))
 
-
-def test_dynamic_scheduler_bit_identical(cuda_ready):
-    """The dynamic (atomic-claim) tile scheduler computes exactly the same bits as the static
-    round-robin one, including wave-tail K pieces followed by whole tiles on one CTA pair."""
-    import torch
-
-    cd = _mods()
-    from paper_2605_19269_b200 import _native
-
-    rng = np.random.default_rng(21)
-    P = cd.PrecisionMode.SIMBF16
-    M = lambda a: cd.DenseMatrix.from_array(a, P)  # noqa: E731
-    m, k, n = 2304, 4096, 2560           # 9 x 10 = 90 pair tiles: one full wave + a split tail
-    a, b = M(rng.standard_normal((m, k)) / 64), M(rng.standard_normal((k, n)) / 64)
-    bt = M(rng.standard_normal((n, k)) / 64)
-    z, pre, gin = M(rng.standard_normal((m, n))), M(rng.standard_normal((m, n))), M(rng.standard_normal((m, n)))
-    pre2 = M(rng.standard_normal((m, 2 * n)))
-    r = cd.Vector.from_array(0.5 + rng.random(m), cd.PrecisionMode.SIM32)
-    s = cd.Vector.from_array(0.1 * rng.standard_normal(m), cd.PrecisionMode.SIM32)
-    gamma = cd.Vector.from_array(1 + 0.1 * rng.standard_normal(n), P)
-
-    def run():
-        outs = []
-        k4 = cd.gemm_residual_partial_rms(a, b, z, gamma, precision=P)
-        outs += [k4.main.data, k4.aux["sumsq"].data]
-        outs.append(cd.gemm_rms_swiglu(a, b, r, precision=P).main.data)
-        k9 = cd.gemm_rmsnorm_backward(a, bt, pre, r, gamma, s, grad_in=gin, trans_b=True, precision=P)
-        outs += [k9.main.data, k9.aux["gamma_grad"].data]
-        k10 = cd.gemm_swiglu_backward(a, bt, pre2, trans_b=True, precision=P)
-        outs += [k10.main.data, k10.aux["rowdot"].data]
-        torch.cuda.synchronize()
-        return outs
-
-    try:
-        _native.set_option("split_min_k", 0)
-        _native.set_option("sched", 0)
-        ref = run()
-        _native.set_option("sched", 1)
-        got = run()
-        got2 = run()
-    finally:
-        _native.set_option("sched", 0)
-        _native.set_option("split_min_k", 8192)
-    for i, (x, y, y2) in enumerate(zip(ref, got, got2)):
-        assert np.array_equal(x, y) and np.array_equal(y, y2), f"output {i} differs under the dynamic scheduler"

@@ -26,6 +26,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--config", default="c4")
+    ap.add_argument("--option", action="append", default=[], help="engine option name=value for the fused runs")
     args = ap.parse_args()
     d, inter, m, _ = bench.CONFIGS[args.config]
     dev = torch.device("cuda", 0)
@@ -53,6 +54,9 @@ def main():
         for t, (pr, a, b) in plains.items():
             cd.run_gemm(pr, a, b, kernel_name="plain:" + t)
 
+    opts = [(kv.split("=")[0], int(kv.split("=")[1])) for kv in args.option]
+    for kk, vv in opts:
+        _native.set_option(kk, vv)
     for _ in range(args.rounds):
         step()
         pf = _native.profile_launches(step, reps=1)
