@@ -225,11 +225,19 @@ _workspaces: dict = {}
 
 
 def workspace(device):
-    """Per-device zeroed scratch for wave-tail splitting (flags stay zero between launches)."""
+    """Zeroed scratch for wave-tail splitting, one per (device, current stream).
+
+    The split-K flags are reset by the launch that consumes them, so consecutive
+    launches on one stream can share the buffer; launches on different streams may
+    run concurrently and therefore get their own."""
     import torch
 
-    key = str(device)
+    key = (str(device), torch.cuda.current_stream(device).cuda_stream)
     ws = _workspaces.get(key)
+    if ws is None and torch.cuda.is_current_stream_capturing():
+        # CUDA-graph capture runs on a side stream: reuse this device's workspace (the
+        # captured launches replay in stream order) rather than capturing a 96 MB memset
+        ws = next((w for (d, _), w in _workspaces.items() if d == str(device)), None)
     if ws is None:
         ws = torch.zeros(WORKSPACE_BYTES // 4, dtype=torch.int32, device=device)
         _workspaces[key] = ws
