@@ -105,7 +105,9 @@ typedef struct {
  *   PARTIAL_COLSUM arg0 = store (col-sum pieces)
  *   ONLINE_LSE     arg0 = store (row-pair pieces)
  *   TARGET_GATHER  arg0 = operand (labels, int64), arg1 = store (gather, f32)
- *   ROPE           arg0 = cos operand, arg1 = sin operand, arg2 = backward flag
+ *   ROPE           arg0 = cos operand, arg1 = sin operand, arg2 = backward flag,
+ *                  arg3/arg4 = 1 + slot of compact (m, h/2) bf16 cos/sin tables or 0,
+ *                  arg5 = h (q-span width; columns >= 2h are the identity)
  *   SWIGLU         —
  *   SWIGLU_BWD     arg0 = preact operand (factor 2), arg1 = recompute store,
  *                  arg2 = row-sum pieces store (factor 2)
@@ -176,6 +178,16 @@ int coda_rope_backward_stat(const coda_tensor_t* grad, const coda_tensor_t* rota
                             const int32_t* block_start, int64_t nb,
                             coda_tensor_t* grad_z, float* rowdot, int64_t ld_rowdot,
                             void* stream);
+
+/* rope_backward_stat with compact tables (bf16, default 128-column row blocks):
+ * cos_c / sin_c are (m, h/2), one angle per pair; grad columns [0, 2h) rotate by
+ * pair (col mod h)/2 (the q and k spans of the packed projection share angles,
+ * kernels.py:184-206) and columns >= 2h are the identity (the v span).  Same
+ * results as coda_rope_backward_stat on the expanded (m, n) tables, with 2*m*h
+ * instead of 4*m*n bytes of table reads.  h % 32 == 0, 2h <= n. */
+int coda_rope_backward_stat_compact(const coda_tensor_t* grad, const coda_tensor_t* rotated,
+                                    const coda_tensor_t* cos_c, const coda_tensor_t* sin_c, int64_t h,
+                                    coda_tensor_t* grad_z, float* rowdot, int64_t ld_rowdot, void* stream);
 
 /* Fold piece partials into reference blocks in ascending piece order.
  * block_ptr (nb+1, host-built CSR) lists the piece range of each block. */

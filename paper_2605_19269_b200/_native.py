@@ -50,6 +50,7 @@ EXPORTS = (
     "coda_combine_lse",
     "coda_cross_entropy_finalize",
     "coda_rope_backward_stat",
+    "coda_rope_backward_stat_compact",
     "coda_combine_row_pieces",
     "coda_combine_col_pieces",
     "coda_split_operand",
@@ -136,6 +137,8 @@ def _declare(lib) -> None:
     lib.coda_cross_entropy_finalize.argtypes = [vp, vp, i64, vp, vp]
     lib.coda_rope_backward_stat.argtypes = [P(Tensor), P(Tensor), P(Tensor), P(Tensor), vp, i64, P(Tensor),
                                             vp, i64, vp]
+    lib.coda_rope_backward_stat_compact.argtypes = [P(Tensor), P(Tensor), P(Tensor), P(Tensor), i64, P(Tensor),
+                                                    vp, i64, vp]
     lib.coda_combine_row_pieces.argtypes = [vp, i64, i64, i64, vp, i64, i32, vp, i64, vp]
     lib.coda_combine_col_pieces.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, vp]
     lib.coda_split_operand.argtypes = [P(Tensor), i32, i64, P(ctypes.c_int32), P(Tensor), vp]

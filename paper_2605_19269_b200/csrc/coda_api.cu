@@ -473,7 +473,18 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         case CODA_OP_PARTIAL_ROWDOT:
             ok = opnd_ok(cs.arg[0]) && store_ok(cs.arg[1]) && w == 32 && (cs.arg[6] == 0 || cs.arg[6] == 1); break;
         case CODA_OP_TARGET_GATHER: ok = opnd_ok(cs.arg[0]) && store_ok(cs.arg[1]) && w == 32; break;
-        case CODA_OP_ROPE: ok = opnd_ok(cs.arg[0]) && opnd_ok(cs.arg[1]); break;
+        case CODA_OP_ROPE:
+            ok = opnd_ok(cs.arg[0]) && opnd_ok(cs.arg[1]);
+            if (ok && cs.arg[3] > 0) {   // compact tables: arg3/arg4 = 1 + operand slot, arg5 = q-span width h
+                const int h = cs.arg[5];
+                ok = opnd_ok(cs.arg[3] - 1) && opnd_ok(cs.arg[4] - 1) && h > 0 && h % 32 == 0 && 2 * (int64_t)h <= N;
+                for (int j = 3; ok && j <= 4; ++j) {
+                    const coda_tensor_t& t = operands[cs.arg[j] - 1];
+                    ok = t.dtype == CODA_BF16 && t.rows == M && t.cols == h / 2;
+                }
+                if (!ok) return fail(CODA_E_BINDING, "step %d: compact RoPE tables must be bf16 (m, h/2), h %% 32 == 0", s);
+            }
+            break;
         case CODA_OP_SWIGLU:
             if (w == 16) return fail(CODA_E_CONFIG, "GPU epilogue supports running width factors 1/2, 1, 2");
             w /= 2; break;
@@ -586,6 +597,9 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         F.ld_acc = P.ld_acc;
         F.ablate = opts().ablate;
         F.rope_sign = 1.0f;
+        const void* rope_c = nullptr;
+        const void* rope_s = nullptr;
+        int64_t ld_rope_c = 0, ld_rope_s = 0;
         int aux_slot = -1;
         for (int s = 0; s < nsteps; ++s) {
             const coda_step_t& cs = steps[s];
@@ -607,7 +621,13 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
             case CODA_OP_ROPE:
                 F.cosp = o[cs.arg[0]].ptr; F.ld_cos = o[cs.arg[0]].ld;
                 F.sinp = o[cs.arg[1]].ptr; F.ld_sin = o[cs.arg[1]].ld;
-                F.rope_sign = cs.arg[2] ? -1.0f : 1.0f; break;
+                F.rope_sign = cs.arg[2] ? -1.0f : 1.0f;
+                if (cs.arg[3] > 0) {
+                    rope_c = o[cs.arg[3] - 1].ptr; ld_rope_c = o[cs.arg[3] - 1].ld;
+                    rope_s = o[cs.arg[4] - 1].ptr; ld_rope_s = o[cs.arg[4] - 1].ld;
+                    F.rope_h = cs.arg[5];
+                }
+                break;
             case CODA_OP_SWIGLU_BWD:
                 F.preact2 = o[cs.arg[0]].ptr; F.ld_pre2 = o[cs.arg[0]].ld;
                 aux_slot = cs.arg[1];
@@ -657,8 +677,13 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         };
         if (fl & F_RESIDUAL) rc = side_map(&s0, F.residual, F.ld_res, N, 32);
         if (!rc && (fl & F_ROPE)) {
-            rc = side_map(&s0, F.cosp, F.ld_cos, N, 32);
-            if (!rc) rc = side_map(&s1, F.sinp, F.ld_sin, N, 32);
+            if (F.rope_h > 0) {   // compact: 32 rows x 16 angles (32 B, SWIZZLE_32B)
+                rc = side_map(&s0, rope_c, ld_rope_c, F.rope_h / 2, 16);
+                if (!rc) rc = side_map(&s1, rope_s, ld_rope_s, F.rope_h / 2, 16);
+            } else {
+                rc = side_map(&s0, F.cosp, F.ld_cos, N, 32);
+                if (!rc) rc = side_map(&s1, F.sinp, F.ld_sin, N, 32);
+            }
         }
         if (!rc && (fl & F_SWIGLU_BWD)) rc = side_map(&s0, F.preact2, F.ld_pre2, 2 * N, 64);
         if (!rc && (fl & F_RMSBWD)) {
@@ -734,6 +759,40 @@ int coda_cross_entropy_finalize(const float* target, const float* lse, int64_t m
     if ((rc = bind_device(lse))) return rc;
     return launch_pdl(coda::coda_ce_finalize_kernel, dim3(grid1d(m, 256)), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_ce_finalize_kernel",
         target, lse, m, losses);
+}
+
+int coda_rope_backward_stat_compact(const coda_tensor_t* grad, const coda_tensor_t* rotated,
+                                    const coda_tensor_t* cos_c, const coda_tensor_t* sin_c, int64_t h,
+                                    coda_tensor_t* grad_z, float* rowdot, int64_t ld_rowdot, void* stream) {
+    if (!grad || !rotated || !cos_c || !sin_c || !grad_z || !rowdot)
+        return fail(CODA_E_BINDING, "rope_backward_stat_compact: null argument");
+    int rc;
+    const coda_tensor_t* ts[3] = {grad, rotated, grad_z};
+    const char* nm[3] = {"grad", "rotated", "grad_z"};
+    for (int i = 0; i < 3; ++i) {
+        if ((rc = check_tensor2d(ts[i], nm[i], CODA_BF16))) return rc;
+        if (ts[i]->rows != grad->rows || ts[i]->cols != grad->cols)
+            return fail(CODA_E_DIMENSION, "%s has shape (%lld,%lld), expected (%lld,%lld)", nm[i],
+                        (long long)ts[i]->rows, (long long)ts[i]->cols, (long long)grad->rows,
+                        (long long)grad->cols);
+    }
+    if (h <= 0 || h % 32 || 2 * h > grad->cols)
+        return fail(CODA_E_DIMENSION, "compact RoPE width h=%lld must be a positive multiple of 32 with 2h <= n",
+                    (long long)h);
+    const coda_tensor_t* tb[2] = {cos_c, sin_c};
+    for (int i = 0; i < 2; ++i) {
+        if ((rc = check_tensor2d(tb[i], i ? "sin_c" : "cos_c", CODA_BF16))) return rc;
+        if (tb[i]->rows != grad->rows || tb[i]->cols != h / 2)
+            return fail(CODA_E_DIMENSION, "compact table must be (%lld, %lld)", (long long)grad->rows,
+                        (long long)(h / 2));
+    }
+    if ((rc = bind_device(grad->ptr))) return rc;
+    const unsigned grid = (unsigned)(grad->rows < 148 * 8 ? grad->rows : 148 * 8);
+    return launch_pdl(coda::coda_rope_backward_stat128_compact_kernel, dim3(grid), dim3(256), 0,
+                      (cudaStream_t)stream, 1, "coda::coda_rope_backward_stat128_compact_kernel",
+                      (const __nv_bfloat16*)grad->ptr, grad->ld, (const __nv_bfloat16*)rotated->ptr, rotated->ld,
+                      (const __nv_bfloat16*)cos_c->ptr, cos_c->ld, (const __nv_bfloat16*)sin_c->ptr, sin_c->ld, h,
+                      grad->rows, grad->cols, (__nv_bfloat16*)grad_z->ptr, grad_z->ld, rowdot, ld_rowdot);
 }
 
 int coda_rope_backward_stat(const coda_tensor_t* grad, const coda_tensor_t* rotated, const coda_tensor_t* cos,

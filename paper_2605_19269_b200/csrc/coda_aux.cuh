@@ -260,6 +260,92 @@ coda_rope_backward_stat128_kernel(const TS* __restrict__ g, int64_t ldg, const T
     }
 }
 
+// Compact-table variant (bf16): cs/sn are (m, h/2) with one angle per pair; columns
+// [0, 2h) rotate by pair (col mod h)/2 (q and k spans share angles), columns >= 2h are the
+// identity.  Reads 2 x m x h bytes of tables instead of 4 x m x n; arithmetic identical.
+__global__ void __launch_bounds__(256)
+coda_rope_backward_stat128_compact_kernel(const __nv_bfloat16* __restrict__ g, int64_t ldg,
+                                          const __nv_bfloat16* __restrict__ rot, int64_t ldr,
+                                          const __nv_bfloat16* __restrict__ cs, int64_t ldc,
+                                          const __nv_bfloat16* __restrict__ sn, int64_t lds, int64_t h,
+                                          int64_t m, int64_t n, __nv_bfloat16* __restrict__ gz, int64_t ldz,
+                                          float* __restrict__ rowdot, int64_t ldd) {
+    griddep_wait();
+    using TS = __nv_bfloat16;
+    constexpr int V = Io<TS>::V;                       // 8
+    constexpr int LPB = 128 / V;
+    constexpr int U = 1;                               // sweeps per iteration (2 measured slower: registers)
+    const int lane = threadIdx.x & 31;
+    const int64_t sweep = (int64_t)blockDim.x * V;
+    for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
+        const TS* gr = g + i * ldg;
+        const TS* rr = rot + i * ldr;
+        const TS* cr = cs + i * ldc;
+        const TS* sr = sn + i * lds;
+        TS* zr = gz + i * ldz;
+        for (int64_t base = 0; base < n; base += U * sweep) {
+            float gv[U][V], rv[U][V], cv[U][V], sv[U][V];
+            int64_t c0[U];
+            bool ok[U];
+            // issue every load of U sweeps before any arithmetic
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                c0[u] = base + u * sweep + (int64_t)threadIdx.x * V;
+                ok[u] = c0[u] < n;
+                if (ok[u] && c0[u] + V <= n) {
+                    Io<TS>::load(gr + c0[u], gv[u]);
+                    Io<TS>::load(rr + c0[u], rv[u]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        const bool in = ok[u] && c0[u] + e < n;
+                        gv[u][e] = in ? Io<TS>::load1(gr + c0[u] + e) : 0.f;
+                        rv[u][e] = in ? Io<TS>::load1(rr + c0[u] + e) : 0.f;
+                    }
+                }
+                if (ok[u] && c0[u] < 2 * h) {
+                    const int64_t p0 = (c0[u] % h) / 2;     // multiple of 4: h % 32 == 0, c0 % 8 == 0
+                    const uint2 uc = __ldg(reinterpret_cast<const uint2*>(cr + p0));
+                    const uint2 us = __ldg(reinterpret_cast<const uint2*>(sr + p0));
+                    const uint32_t wc[2] = {uc.x, uc.y}, ws[2] = {us.x, us.y};
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const float c_lo = __uint_as_float(wc[j] << 16), c_hi = __uint_as_float(wc[j] & 0xFFFF0000u);
+                        const float s_lo = __uint_as_float(ws[j] << 16), s_hi = __uint_as_float(ws[j] & 0xFFFF0000u);
+                        cv[u][4 * j] = cv[u][4 * j + 1] = c_lo;
+                        cv[u][4 * j + 2] = cv[u][4 * j + 3] = c_hi;
+                        sv[u][4 * j] = sv[u][4 * j + 1] = s_lo;
+                        sv[u][4 * j + 2] = sv[u][4 * j + 3] = s_hi;
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        cv[u][e] = 1.0f;
+                        sv[u][e] = 0.0f;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                float zv[V];
+                float p = 0.0f;
+#pragma unroll
+                for (int k = 0; k < V / 2; ++k) {
+                    const float g0 = gv[u][2 * k], g1 = gv[u][2 * k + 1];
+                    zv[2 * k] = g0 * cv[u][2 * k] + g1 * sv[u][2 * k];
+                    zv[2 * k + 1] = -g0 * sv[u][2 * k + 1] + g1 * cv[u][2 * k + 1];
+                }
+#pragma unroll
+                for (int e = 0; e < V; ++e) p += gv[u][e] * rv[u][e];
+                if (ok[u]) store_seg<TS, V>(zr, c0[u], n, zv);
+#pragma unroll
+                for (int off = LPB / 2; off >= 1; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+                if (ok[u] && (lane % LPB) == 0) rowdot[i * ldd + c0[u] / 128] = p;
+            }
+        }
+    }
+}
+
 // SIM32 split: x = x0 + x1 + x2 with x0 = bf16(x), x1 = bf16(x - x0), x2 = bf16(x - x0 - x1)
 // (each difference is exact in f32).  dst holds 6 K-blocks of kp, block j = term pattern[j].
 struct SplitPattern { int t[6]; };

@@ -86,6 +86,11 @@ struct FastParams {
     float* ws;
     int* flags;
     int ablate;   // measurement-only ablations (results invalid): 1 = no side loads, 2 = no TMA stores
+    // compact RoPE tables (F_ROPE): 0 = full (M, N) cos/sin tables.  h > 0: tma_s0/s1 map
+    // (M, h/2) tables of one angle per pair; columns [0, 2h) rotate by pair (col mod h)/2
+    // (the q and k spans of the packed projection share angles), columns >= 2h are the
+    // identity (cos 1, sin 0) and load nothing.
+    int rope_h;
 };
 
 __device__ __forceinline__ bool item_runs_program(const MainParams& mp, const Work& w) {
@@ -139,6 +144,25 @@ __device__ __forceinline__ void side_row(uint32_t base, int r, float* out) {
         for (int i = 0; i < 4; ++i) {
             out[c * 8 + 2 * i] = __uint_as_float(w[i] << 16);
             out[c * 8 + 2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+        }
+    }
+}
+
+// One thread's row of a compact RoPE box (32 rows x 16 bf16, SWIZZLE_32B): 16 angles,
+// each duplicated for the two columns of its pair -> 32 values.
+__device__ __forceinline__ void side_row_pairs(uint32_t base, int r, float* out) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const uint32_t off = (uint32_t)(r * 32 + c * 16);
+        uint32_t w[4];
+        ld_shared_v4(base + (off ^ ((off >> 3) & 0x10u)), w[0], w[1], w[2], w[3]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xFFFF0000u);
+            out[c * 16 + 4 * i] = lo;
+            out[c * 16 + 4 * i + 1] = lo;
+            out[c * 16 + 4 * i + 2] = hi;
+            out[c * 16 + 4 * i + 3] = hi;
         }
     }
 }
@@ -350,11 +374,23 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         uint32_t side_phase = 0;
         // lane 0: TMA-load the side operands of chunk c of tile t into this warp's buffer
         const bool no_side = (P.ablate & 1) != 0;
+        const int rope_h = (FL & F_ROPE) ? P.rope_h : 0;
+        // does the chunk starting at global column x load side operands?  (issue and wait
+        // sides evaluate the same predicate)
+        auto side_needed = [&](int x) { return !no_side && !(rope_h > 0 && x >= 2 * rope_h); };
         auto side_issue = [&](int tm_, int tn_, int c_) {
-            if (no_side) return;
             const int y = tm_ * G::TILE_M + rank * BM + q * 32;
             const int x = tn_ * BN + h * 128 + c_ * 32;
+            if (!side_needed(x)) return;
             fence_proxy_async_smem();
+            if ((FL & F_ROPE) && rope_h > 0) {
+                // one angle per pair: 16 columns (32 B) of each compact table
+                const int pc = (x % rope_h) / 2;
+                mbar_arrive_expect_tx(&sidebar[ew], 2048);
+                tma_load_2d(sbase, &tma_s0, pc, y, &sidebar[ew]);
+                tma_load_2d(sbase + 2048, &tma_s1, pc, y, &sidebar[ew]);
+                return;
+            }
             mbar_arrive_expect_tx(&sidebar[ew], FG::CHUNK_BYTES);
             if (FL & F_SWIGLU_BWD) {
                 tma_load_2d(sbase, &tma_s0, 2 * x, y, &sidebar[ew]);
@@ -464,13 +500,33 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 float sd0[FG::SIDE ? ((FL & F_SWIGLU_BWD) ? 64 : 32) : 1];
                 float sd1[(FL & (F_ROPE | F_RMSBWD_ACC)) ? 32 : 1];
                 if constexpr (FG::SIDE) {
-                    if (!no_side) {
+                    const int xcol = n0 + h * 128 + c * 32;
+                    const bool loaded = side_needed(xcol);
+                    if (loaded) {
                         mbar_wait(&sidebar[ew], side_phase);
                         side_phase ^= 1;
                     }
-                    if constexpr ((FL & F_SWIGLU_BWD) != 0) side_row<128>(sbase, lane, sd0);
-                    else side_row<64>(sbase, lane, sd0);
-                    if constexpr ((FL & (F_ROPE | F_RMSBWD_ACC)) != 0) side_row<64>(sbase + 2048, lane, sd1);
+                    if constexpr ((FL & F_ROPE) != 0) {
+                        if (rope_h > 0) {
+                            if (loaded) {
+                                side_row_pairs(sbase, lane, sd0);
+                                side_row_pairs(sbase + 2048, lane, sd1);
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 32; ++e) {
+                                    sd0[e] = 1.0f;
+                                    sd1[e] = 0.0f;
+                                }
+                            }
+                        } else {
+                            side_row<64>(sbase, lane, sd0);
+                            side_row<64>(sbase + 2048, lane, sd1);
+                        }
+                    } else {
+                        if constexpr ((FL & F_SWIGLU_BWD) != 0) side_row<128>(sbase, lane, sd0);
+                        else side_row<64>(sbase, lane, sd0);
+                        if constexpr ((FL & F_RMSBWD_ACC) != 0) side_row<64>(sbase + 2048, lane, sd1);
+                    }
                     __syncwarp();
                     if (lane == 0) {
                         if (c < 3) {

@@ -323,6 +323,28 @@ def run_gemm(
         keep.append(t)
         op_descs[i] = nat.tensor_desc(t)
 
+    # ---- compact RoPE tables (qkv_rope_tables pairs): extra operands the specialised
+    # kernel loads instead of the full (m, n) tables; the generic interpreter ignores them
+    nops = len(onames)
+    steps = list(steps)   # the lowering is memoized on the program: never edit it in place
+    if prec is PrecisionMode.SIMBF16:
+        from .kernels import rope_compact_of
+
+        for si, (op, w2, args) in enumerate(steps):
+            if op != nat.OP_ROPE or len(onames) + 2 > nat.MAX_OPERANDS:
+                continue
+            spec = rope_compact_of(bindings[onames[args[0]]], bindings[onames[args[1]]])
+            if spec is None or 2 * spec.hidden > p.n or spec.cos.shape[0] != p.m:
+                continue
+            grown = (nat.Tensor * (nops + 2))()
+            for j in range(nops):
+                grown[j] = op_descs[j]
+            grown[nops], grown[nops + 1] = nat.tensor_desc(spec.cos), nat.tensor_desc(spec.sin)
+            keep.extend((spec.cos, spec.sin))
+            op_descs = grown
+            steps[si] = (op, w2, list(args[:3]) + [nops + 1, nops + 2, spec.hidden, 0])
+            nops += 2
+
     # ---- stores
     st_descs = (nat.Store * max(1, len(snames)))()
     outputs = {}
@@ -382,7 +404,7 @@ def run_gemm(
         acc_desc = nat.tensor_desc(acc_t) if acc_t is not None else None
         nat.call("coda_gemm_epilogue", ctypes.byref(prob), ctypes.byref(nat.tensor_desc(ta)),
                  ctypes.byref(nat.tensor_desc(tb)), step_arr, len(steps) if program_on else 0, op_descs,
-                 len(onames), st_descs, len(snames) if program_on else 0,
+                 nops, st_descs, len(snames) if program_on else 0,
                  ctypes.byref(mdesc) if mdesc is not None else None,
                  ctypes.byref(acc_desc) if acc_desc is not None else None, _stream(dev),
                  tag=f"{kernel_name} {p.m}x{p.n}x{p.k}{' TN' if p.trans_a else ''}{' NT' if p.trans_b else ''}",

@@ -194,7 +194,36 @@ def qkv_rope_tables(m: int, hidden: int, *, base: float = 10000.0, start: int = 
         full[:, hidden:hidden + kv] = srck.tensor
         full[:, hidden + kv:] = fill
         out.append(DenseMatrix._wrap(full, precision))
+    if precision is PrecisionMode.SIMBF16 and kv == hidden and hidden % 32 == 0:
+        # compact form for the kernels: one angle per pair of the q span (the k span
+        # repeats it, the v span is the identity) -- the same bf16 values, 1/6 the bytes
+        spec = RopeCompact(cos=c_h.tensor[:, 0::2].contiguous(), sin=s_h.tensor[:, 0::2].contiguous(),
+                           hidden=hidden)
+        out[0]._rope = spec
+        out[1]._rope = spec
     return out[0], out[1]
+
+
+@dataclass(frozen=True)
+class RopeCompact:
+    """Compact packed-qkv RoPE tables: (m, hidden/2) bf16 cos/sin, one value per pair.
+
+    Columns [0, 2*hidden) of the full table hold cos[:, (col % hidden) // 2] (q and k
+    spans share angles, kernels.py:184-206); columns >= 2*hidden are cos 1 / sin 0."""
+
+    cos: object
+    sin: object
+    hidden: int
+
+
+def rope_compact_of(cos: DenseMatrix, sin: DenseMatrix) -> Optional[RopeCompact]:
+    """The compact form shared by a (cos, sin) pair built together by qkv_rope_tables."""
+    spec = getattr(cos, "_rope", None)
+    if spec is None or getattr(sin, "_rope", None) is not spec:
+        return None
+    if cos.precision is not PrecisionMode.SIMBF16 or cos.rows != spec.cos.shape[0]:
+        return None
+    return spec
 
 
 def interleave_gate_up(gate: DenseMatrix, up: DenseMatrix) -> DenseMatrix:
@@ -353,9 +382,17 @@ def rope_backward_stat(grad: DenseMatrix, rotated: DenseMatrix, cos: DenseMatrix
     descs = [nat.tensor_desc(t) for t in ts]
     gzd = nat.tensor_desc(gz)
     uniform128 = all(int(w) == 128 for w in counts[:-1]) and int(counts[-1]) <= 128
-    nat.call("coda_rope_backward_stat", *[ctypes.byref(d) for d in descs], None if uniform128 else bst.data_ptr(),
-             nb, ctypes.byref(gzd), rowdot.data_ptr(), rowdot.stride(0), torch.cuda.current_stream(dev).cuda_stream,
-             tag="rope_backward_stat", flops=0.0)
+    spec = rope_compact_of(cos, sin) if precision is PrecisionMode.SIMBF16 else None
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    if spec is not None and uniform128 and 2 * spec.hidden <= n:
+        cd_, sd_ = nat.tensor_desc(spec.cos), nat.tensor_desc(spec.sin)
+        nat.call("coda_rope_backward_stat_compact", ctypes.byref(descs[0]), ctypes.byref(descs[1]),
+                 ctypes.byref(cd_), ctypes.byref(sd_), spec.hidden, ctypes.byref(gzd), rowdot.data_ptr(),
+                 rowdot.stride(0), stream, tag="rope_backward_stat", flops=0.0)
+    else:
+        nat.call("coda_rope_backward_stat", *[ctypes.byref(d) for d in descs],
+                 None if uniform128 else bst.data_ptr(), nb, ctypes.byref(gzd), rowdot.data_ptr(), rowdot.stride(0),
+                 stream, tag="rope_backward_stat", flops=0.0)
     slot = PartialSlot(StoreKind.ROW_SUM, rowdot, counts, precision).freeze()
     w, pw = precision.storage_bytes, precision.partial_bytes
     rec = LaunchRecord(traffic.K_ROPE_BWD_STAT, 4 * m * n * w, m * n * w + m * nb * pw)

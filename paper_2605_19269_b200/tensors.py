@@ -181,15 +181,18 @@ class DenseMatrix:
     """Row-major 2-D device tensor tagged with its storage precision.
 
     Treated as immutable by the engine: launches always write fresh outputs.
+    `_rope` optionally carries a compact form of a RoPE table (set only by
+    `qkv_rope_tables`, which builds both forms from the same values).
     """
 
-    __slots__ = ("_t", "precision", "_host")
+    __slots__ = ("_t", "precision", "_host", "_rope")
 
     def __init__(self, data, precision: PrecisionMode = PrecisionMode.EXACT64):
         import torch
 
         self.precision = precision
         self._host = None
+        self._rope = None
         if isinstance(data, np.ndarray):
             if data.ndim != 2:
                 raise DimensionError(f"DenseMatrix needs a 2-D array, got ndim={data.ndim}")
@@ -229,6 +232,7 @@ class DenseMatrix:
         obj._t = tensor
         obj.precision = precision
         obj._host = None
+        obj._rope = None
         return obj
 
     @property

@@ -208,3 +208,34 @@ def test_gqa_kv_width_layer(cuda_ready, mode_name):
         e64 = {k: O.rel_error(getattr(bwd, k).data, refb[k]) for k in O.GRAD_KEYS}
         e64["qkv"] = O.rel_error(fwd.qkv.data, ref["qkv"])
         assert max(e64.values()) <= 1e-5, e64
+
+
+def test_compact_rope_tables_bit_identical(cuda_ready):
+    """qkv_rope_tables attaches a compact (m, d/2) form that K7 and rope_backward_stat load
+    instead of the full (m, 3d) tables; results must be bit-identical to the full tables."""
+    cd = _cd()
+    P = cd.PrecisionMode.SIMBF16
+    m, d, ffn = 640, 256, 1024
+    cfg = cd.PipelineConfig(hidden=d, ffn=ffn, precision=P)
+    rng = np.random.default_rng(13)
+    w = cd.LayerWeights.random(rng, cfg, scale=0.05)
+    M = lambda a: cd.DenseMatrix.from_array(a, P)  # noqa: E731
+    x, z = M(rng.standard_normal((m, d))), M(rng.standard_normal((m, d)))
+    gq, gr = M(rng.standard_normal((m, 3 * d))), M(rng.standard_normal((m, d)))
+    cos_c, sin_c = cd.qkv_rope_tables(m, d, start=7, precision=P)
+    assert cos_c._rope is not None and cos_c._rope is sin_c._rope
+    assert cos_c._rope.cos.shape == (m, d // 2)
+    # the same values without the compact form (full-table path)
+    cos_f, sin_f = cd.DenseMatrix.from_tensor(cos_c.tensor, P), cd.DenseMatrix.from_tensor(sin_c.tensor, P)
+    assert cos_f._rope is None
+    outs = []
+    for c, s in ((cos_c, sin_c), (cos_f, sin_f)):
+        fwd = cd.layer_forward(x, z, w, c, s, config=cfg)
+        bwd = cd.layer_backward(gq, fwd.tape, w, grad_residual=gr, config=cfg)
+        gz, rd = cd.rope_backward_stat(gq, fwd.qkv, c, s, precision=P)
+        outs.append([fwd.qkv.data, gz.data, rd.data] + [getattr(bwd, k).data for k in O.GRAD_KEYS])
+    for i, (a, b) in enumerate(zip(*outs)):
+        assert np.array_equal(a, b), f"output {i} differs between compact and full RoPE tables"
+    # and the compact path agrees with the fused-order oracle
+    of = O.layer_forward(x.data, z.data, {k: getattr(w, k).data for k in WKEYS}, cos_f.data, sin_f.data, O.SIMBF16)
+    assert O.rel_error(outs[0][0], of["qkv"]) <= 2e-2
