@@ -307,10 +307,15 @@ def coda_arm(args, rank, world, local_rank):
     device = torch.device("cuda", local_rank)
     torch.cuda.set_device(device)
     dist = None
-    if world > 1:
+    if world > 1 or args.force_dist:
         import torch.distributed as dist  # noqa: F811
 
-        dist.init_process_group("nccl", device_id=device)
+        if world == 1:   # --force-dist: a 1-rank NCCL group, to exercise the collective path on one GPU
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29511")
+            dist.init_process_group("nccl", device_id=device, rank=0, world_size=1)
+        else:
+            dist.init_process_group("nccl", device_id=device)
     from paper_2605_19269_b200 import parallel
 
     d, inter, tokens, label = CONFIGS[args.config]
@@ -567,6 +572,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="profiling pass only (no timing / JSON line)")
     ap.add_argument("--graph", action="store_true", help="replay the step as one captured CUDA graph")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the NCCL wgrad all-reduce path even at world size 1 (collective overlap check)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", 0))

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -896,8 +897,13 @@ int coda_convert_f32_bf16(const coda_tensor_t* src, coda_tensor_t* dst, void* st
     if (src->rows != dst->rows || src->cols != dst->cols) return fail(CODA_E_DIMENSION, "convert: shapes differ");
     int rc;
     if ((rc = bind_device(src->ptr))) return rc;
-    return launch_pdl(coda::coda_convert_f32_bf16_kernel, dim3(grid1d(src->rows * src->cols, 256)), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_convert_f32_bf16_kernel",
-        (const float*)src->ptr, src->rows, src->cols, src->ld, (__nv_bfloat16*)dst->ptr, dst->ld);
+    const int vec = src->ld % 4 == 0 && dst->ld % 8 == 0 && reinterpret_cast<uintptr_t>(src->ptr) % 16 == 0 &&
+                    reinterpret_cast<uintptr_t>(dst->ptr) % 16 == 0;
+    const int64_t work = vec ? src->rows * (src->cols / 8) : src->rows;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 148 * 8));
+    return launch_pdl(coda::coda_convert_f32_bf16_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, 1,
+                      "coda::coda_convert_f32_bf16_kernel", (const float*)src->ptr, src->rows, src->cols, src->ld,
+                      (__nv_bfloat16*)dst->ptr, dst->ld, vec);
 }
 
 }  // extern "C"

@@ -379,13 +379,31 @@ __global__ void coda_split_operand_kernel(const float* __restrict__ src, int64_t
     dst[r * ldd + c] = __float2bfloat16_rn(val);
 }
 
-__global__ void coda_convert_f32_bf16_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
-                                        __nv_bfloat16* __restrict__ dst, int64_t ldd) {
+__global__ void __launch_bounds__(256)
+coda_convert_f32_bf16_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
+                             __nv_bfloat16* __restrict__ dst, int64_t ldd, int vec) {
     griddep_wait();
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= rows * cols) return;
-    const int64_t r = idx / cols, c = idx % cols;
-    dst[r * ldd + c] = __float2bfloat16_rn(src[r * lds + c]);
+    // 8 elements per thread step: two 16-B streaming loads, one 16-B store (when rows are
+    // 16-B aligned: vec = 1); HBM-bound, 6 B per element.  Unaligned rows go scalar.
+    const int64_t vpr = vec ? cols / 8 : 0;
+    const int64_t total = rows * vpr;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < total; v += stride) {
+        const int64_t r = v / vpr, c = (v - r * vpr) * 8;
+        const float4 a = __ldcs(reinterpret_cast<const float4*>(src + r * lds + c));
+        const float4 b = __ldcs(reinterpret_cast<const float4*>(src + r * lds + c + 4));
+        uint4 o;
+        o.x = pack_bf16x2(a.x, a.y);
+        o.y = pack_bf16x2(a.z, a.w);
+        o.z = pack_bf16x2(b.x, b.y);
+        o.w = pack_bf16x2(b.z, b.w);
+        __stcs(reinterpret_cast<uint4*>(dst + r * ldd + c), o);
+    }
+    const int64_t c0 = vpr * 8;
+    if (c0 < cols) {
+        for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride)
+            for (int64_t c = c0; c < cols; ++c) dst[r * ldd + c] = __float2bfloat16_rn(src[r * lds + c]);
+    }
 }
 
 }  // namespace coda
