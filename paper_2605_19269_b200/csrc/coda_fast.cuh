@@ -587,11 +587,20 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 if (FL & F_GATHER) {
                     const int64_t local = label - gcol0;
                     if (local >= 0 && local < 32 && label < N) {
-                        float val = 0.0f;
+                        // select v[local] with a 5-level select tree over the bits of local:
+                        // static register indices only (a dynamic v[local] would put the
+                        // whole chunk in local memory every chunk)
+                        const int l = (int)local;
+                        float t16[16], t8[8], t4[4], t2[2];
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (i == (int)local) val = v[i];
-                        P.target[row] = val;
+                        for (int i = 0; i < 16; ++i) t16[i] = (l & 16) ? v[i + 16] : v[i];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) t8[i] = (l & 8) ? t16[i + 8] : t16[i];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) t4[i] = (l & 4) ? t8[i + 4] : t8[i];
+#pragma unroll
+                        for (int i = 0; i < 2; ++i) t2[i] = (l & 2) ? t4[i + 2] : t4[i];
+                        P.target[row] = (l & 1) ? t2[1] : t2[0];
                     }
                 }
                 if (FL & F_LSE) {
