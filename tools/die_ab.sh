@@ -1,4 +1,6 @@
 #!/bin/bash
+# NOTE: historical.  The "die" option (die-local rasters) was measured with this script and
+# removed again because it did not reduce DRAM bytes (profiles/r01b_summary.md §5).
 # Die-local rasters on vs off: DRAM bytes + duration of single launches (ncu), then
 # interleaved timing of the same GEMMs and of the C4 step.
 mkdir -p gpurun_out
