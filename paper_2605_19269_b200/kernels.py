@@ -673,7 +673,8 @@ def lm_head_forward(a, b, z, gamma, w_vocab, labels, *, config: PipelineConfig,
     k4 = gemm_residual_partial_rms(a, b, z, gamma, **kw)
     r = finalize_rms(k4.aux["sumsq"], config.eps, ledger=ledger)
     k8 = gemm_rms_partial_xent(k4.main, w_vocab, r, labels, store_logits=store_logits, **kw)
-    lse = combine_lse(k8.aux["lse"], ledger=ledger)
-    losses, mean = cross_entropy_finalize(k8.aux["target"], lse, ledger=ledger)
+    # one device->host read for the LSE / target checks and the mean (same errors, same order)
+    lse = combine_lse(k8.aux["lse"], ledger=ledger, check=False)
+    losses, mean = cross_entropy_finalize(k8.aux["target"], lse, ledger=ledger, check_lse=True)
     return LmHeadResult(losses=losses, mean_loss=mean, lse=lse, target=k8.aux["target"],
                         pre_norm=k4.aux["pre_norm"], inv_rms=r, logits=k8.main, ledger=ledger)

@@ -146,3 +146,27 @@ def test_uniform_logits_give_ln_vocab(cuda_ready):
     res = cd.lm_head_forward(a, b, z, gamma, wv, labels, config=cd.PipelineConfig(hidden=d, precision=P))
     assert abs(res.mean_loss - math.log(v)) / math.log(v) < 1e-6
     assert np.allclose(res.lse.data, np.float32(math.log(v)), rtol=1e-6)
+
+
+def test_xent_error_paths(cuda_ready):
+    """The reference's CE errors survive the single host read: a NaN (unvisited) target
+    raises MissingGatherError, a row with no LSE values raises DegenerateError, in the
+    reference's order (reductions.py:101-168)."""
+    import torch
+
+    cd = _cd()
+    P = cd.PrecisionMode.SIMBF16
+    S = cd.stat_mode(P)
+    m = 6
+    lse = cd.Vector.from_tensor(torch.zeros(m, device="cuda"), S)
+    tgt = torch.zeros(m, device="cuda")
+    tgt[3] = float("nan")
+    with pytest.raises(cd.MissingGatherError):
+        cd.cross_entropy_finalize(cd.Vector.from_tensor(tgt, S), lse)
+    bad_lse = torch.zeros(m, device="cuda")
+    bad_lse[1] = float("nan")
+    with pytest.raises(cd.DegenerateError):
+        cd.cross_entropy_finalize(cd.Vector.from_tensor(tgt, S), cd.Vector.from_tensor(bad_lse, S), check_lse=True)
+    losses, mean = cd.cross_entropy_finalize(cd.Vector.from_tensor(torch.full((m,), 0.5, device="cuda"), S),
+                                             cd.Vector.from_tensor(torch.full((m,), 2.0, device="cuda"), S))
+    assert mean == pytest.approx(1.5) and np.allclose(losses.data, 1.5)
