@@ -247,8 +247,36 @@ class CpuOracle:
         O = self.O
         t0 = time.perf_counter()
         f = O.layer_forward(self.x, self.z, self.w, self.cos, self.sin, self.mode)
-        O.layer_backward(self.gq, f, self.w, self.mode, grad_residual=self.gres)
-        return time.perf_counter() - t0
+        b = O.layer_backward(self.gq, f, self.w, self.mode, grad_residual=self.gres)
+        dt = time.perf_counter() - t0
+        self.last = (f, b)
+        return dt
+
+    def gpu_parity(self, cd, kv=None) -> dict:
+        """The same sample through the CUDA path: worst relative (Frobenius) and max
+        absolute error over qkv and the eight gradients vs this oracle's outputs."""
+        import numpy as np
+
+        O = self.O
+        P = cd.PrecisionMode.SIM32 if self.mode == O.SIM32 else cd.PrecisionMode.SIMBF16
+        d = self.x.shape[1]
+        M = lambda a: cd.DenseMatrix.from_array(a, P)  # noqa: E731
+        V = lambda a: cd.Vector.from_array(a, P)  # noqa: E731
+        w = self.w
+        weights = cd.LayerWeights(w_out=M(w["w_out"]), gamma_ffn=V(w["gamma_ffn"]), w_gate_up=M(w["w_gate_up"]),
+                                  w_down=M(w["w_down"]), gamma_qkv=V(w["gamma_qkv"]), w_qkv=M(w["w_qkv"]))
+        cfg = cd.PipelineConfig(hidden=d, ffn=w["w_gate_up"].shape[1], precision=P, kv_width=kv)
+        fwd = cd.layer_forward(M(self.x), M(self.z), weights, M(self.cos), M(self.sin), config=cfg)
+        bwd = cd.layer_backward(M(self.gq), fwd.tape, weights, grad_residual=M(self.gres), config=cfg)
+        f, b = self.last
+        pairs = [("qkv", fwd.qkv.data, f["qkv"])] + [(k, getattr(bwd, k).data, b[k]) for k in O.GRAD_KEYS]
+        rel = {k: O.rel_error(g, r) for k, g, r in pairs}
+        mx = max(float(np.max(np.abs(g - r))) for _, g, r in pairs)
+        mref = max(float(np.max(np.abs(r))) for _, _, r in pairs)
+        worst = max(rel, key=rel.get)
+        return {"rel_err_max": rel[worst], "worst_output": worst, "max_abs_err": mx, "max_abs_ref": mref,
+                "tol": 1e-5 if P is cd.PrecisionMode.SIM32 else 2e-2, "vs": "fused-order CPU oracle, same inputs",
+                "sample_tokens": self.m}
 
 
 def cpu_oracle_tokens_per_s(d, inter, sample_tokens, seconds_budget=20.0, max_reps=5, fp32=False, kv=None):
@@ -260,7 +288,7 @@ def cpu_oracle_tokens_per_s(d, inter, sample_tokens, seconds_budget=20.0, max_re
         if time.perf_counter() - t_start > seconds_budget or len(times) >= max_reps:
             break
     best = min(times)
-    return sample_tokens / best, best, len(times)
+    return sample_tokens / best, best, len(times), runner
 
 
 def host_cores() -> int:
@@ -522,10 +550,12 @@ def coda_arm(args, rank, world, local_rank):
     block_tflops = total_flops / (ms_step / 1e3) / 1e12
 
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
         sample = min(args.cpu_sample, m)
-        tps, secs, reps = cpu_oracle_tokens_per_s(d, inter, sample, seconds_budget=20.0, max_reps=3, fp32=fp32,
-                                                  kv=kv)
+        tps, secs, reps, runner = cpu_oracle_tokens_per_s(d, inter, sample, seconds_budget=20.0, max_reps=3,
+                                                          fp32=fp32, kv=kv)
+        parity = runner.gpu_parity(cd, kv=kv)
         cpu = {"value": tps, "unit": "tokens/s", "cores": host_cores(), "kind": "port",
                "sample": f"{sample} tokens of the {args.config} block, fused-order "
                          f"{'SIM32' if fp32 else 'SIMBF16'} oracle, "
@@ -553,6 +583,7 @@ def coda_arm(args, rank, world, local_rank):
             "cuda_graph": bool(args.graph),
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "parity": parity,
             "launch_breakdown_ms": {k: round(v["avg_ms"], 4) for k, v in (prof or {}).items()},
         }
         print(json.dumps(line), flush=True)
