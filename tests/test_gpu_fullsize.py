@@ -130,3 +130,22 @@ def bwd_grad_h1b(r):
     k9b = cd.gemm_rmsnorm_backward(gz, w.w_qkv, tape.pre_norm_b, tape.inv_rms_b, w.gamma_qkv, s_b,
                                    grad_in=r["gr"], trans_b=True, precision=cd.PrecisionMode.SIMBF16)
     return k9b.main
+
+
+def test_c4_compact_rope_tables_bit_identical(c4_run):
+    """At full C4 size the compact RoPE path (K7 + rope_backward_stat) gives exactly the
+    bits of the full-table path."""
+    import torch
+
+    r = c4_run
+    cd = r["cd"]
+    P = cd.PrecisionMode.SIMBF16
+    assert r["cos"]._rope is not None
+    cos_f = cd.DenseMatrix.from_tensor(r["cos"].tensor, P)
+    sin_f = cd.DenseMatrix.from_tensor(r["sin"].tensor, P)
+    fwd = cd.layer_forward(r["x"], r["z"], r["w"], cos_f, sin_f, config=r["cfg"])
+    bwd = cd.layer_backward(r["gq"], fwd.tape, r["w"], grad_residual=r["gr"], config=r["cfg"])
+    torch.cuda.synchronize()
+    assert torch.equal(fwd.qkv.tensor, r["fwd"].qkv.tensor)
+    for k in O.GRAD_KEYS:
+        assert torch.equal(getattr(bwd, k).tensor, getattr(r["bwd"], k).tensor), k
