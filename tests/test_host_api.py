@@ -271,3 +271,13 @@ def test_engine_options_validated():
             nat.set_option(name, bad)
     for name, ok in (("ring", 0), ("prefetch", 0), ("ablate", 0), ("raster", 8), ("cg", 2)):
         nat.set_option(name, ok)
+
+
+def test_problem_validation():
+    """GemmProblem validation (reference tests/test_engine.py:198-210), host only."""
+    with pytest.raises(cd.DimensionError):
+        cd.GemmProblem(m=0, n=4, k=4)
+    with pytest.raises(cd.ConfigError):
+        cd.GemmProblem(m=4, n=4, k=4, tile_shape=cd.TileShape(0, 4))
+    with pytest.raises(cd.ConfigError):
+        cd.GemmProblem(m=4, n=4, k=4, reduction_tile_n=0)
