@@ -1,3 +1,4 @@
+"""NVLS multicast / symmetric-memory availability probe (measurement tool)."""
 import os, torch, torch.distributed as dist
 os.environ.setdefault("MASTER_ADDR", "127.0.0.1"); os.environ.setdefault("MASTER_PORT", "29533")
 dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
