@@ -594,7 +594,7 @@ def coda_arm(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("coda", "reference"), default="coda")
     ap.add_argument("--config", choices=tuple(CONFIGS), default="c4")
