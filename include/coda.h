@@ -84,10 +84,15 @@ typedef struct {
     int32_t storage;       /* dtype of side TILE operands and aux TILE stores */
     int32_t out_dtype;     /* dtype of the main output */
     int32_t store_main;    /* engine.py:428-430 */
-    int32_t _pad;
+    int32_t sm_limit;      /* 0: the persistent grid uses every SM; > 0: at most this many SMs,
+                              leaving the rest to concurrent work on other streams (e.g. the
+                              data-parallel weight-gradient all-reduce).  Results never change. */
     /* Optional caller-owned scratch for wave-tail splitting (split-K of the last,
-     * partial wave; deterministic fixed-order fold).  The first 64 KiB hold int32
-     * flags that must be zero before the first launch (the kernels leave them
+     * partial wave).  Every K piece of a split tile dumps its f32 partial and arrives
+     * on a counter; the last arrival sums all pieces in fixed piece order (bitwise
+     * deterministic) and runs the program.  No piece waits for another, so nothing
+     * assumes the launch's clusters are co-resident.  The first 64 KiB hold int32
+     * counters that must be zero before the first launch (the kernels leave them
      * zero); the rest holds f32 partial tiles.  NULL / 0 disables splitting.
      * Launches sharing one workspace must be stream-ordered. */
     void*   workspace;
@@ -210,13 +215,21 @@ int coda_split_operand(const coda_tensor_t* src, int k_axis, int64_t kp,
  * allreduce of weight gradients so rounding happens once (engine.py:443-447). */
 int coda_convert_f32_bf16(const coda_tensor_t* src, coda_tensor_t* dst, void* stream);
 
-/* Engine options (defaults from the environment): "pdl" 0/1 programmatic
- * dependent launch, "cg" 1/2 CTA-pair mainloop, "generic" 0/1 force the generic
- * epilogue interpreter, "raster" >= 1 raster group, "split" 0/1 wave-tail split-K,
- * "split_min_k" smallest K that is split, "ring" operand-ring stages in use
- * (0 = compiled depth), "prefetch" 0..64 L2 prefetch distance in k-blocks (0 = off,
- * measured slower), "ablate" measurement-only epilogue ablations (1 = skip side
- * loads, 2 = skip TMA stores; results are invalid).  Process-wide. */
+/* Gain folding (north_star "gamma folded into W"; B200 extension, no reference
+ * counterpart): dst[i, :] = bf16(scale[i] * src[i, :]), bf16 (rows, cols) src/dst,
+ * f32 scale[rows].  W' = diag(gamma) W is formed once per weight update, so the
+ * producing launch (gemm_residual_partial_rms, kernels.py:325-360) no longer
+ * multiplies by gamma nor stores the gained copy of its output. */
+int coda_scale_rows(const coda_tensor_t* src, const float* scale, coda_tensor_t* dst, void* stream);
+
+/* Engine schedule options (defaults from the environment); each variant computes
+ * the same program: "pdl" 0/1 programmatic dependent launch, "cg" 1/2 CTA-pair
+ * mainloop, "generic" 0/1 force the generic epilogue interpreter, "raster" >= 1
+ * raster group, "split" 0/1 wave-tail split-K and "split_min_k" the smallest K that
+ * is split (splitting changes only the deterministic f32 accumulation order).
+ * Process-wide.  Measurement knobs ("ring", "prefetch", "ablate" — the last makes
+ * results invalid) exist only in experiment builds (-DCODA_EXPERIMENTS) and return
+ * CODA_E_CONFIG from the product library. */
 int coda_set_option(const char* name, int value);
 
 /* Number of SMs the persistent kernel sizes its grid for (0 if no device). */

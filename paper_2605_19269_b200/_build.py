@@ -17,6 +17,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libcoda.so"
+LIB_EXP = LIBDIR / "libcoda_exp.so"     # -DCODA_EXPERIMENTS: measurement knobs for tools/
 INCLUDE = PKG.parent / "include"
 
 SOURCES = ["coda_api.cu"]
@@ -37,29 +38,31 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found; cannot build the CODA CUDA library")
 
 
-def needs_build() -> bool:
-    if not LIB.exists():
+def needs_build(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     srcs = [CSRC / d for d in DEPS] + [INCLUDE / "coda.h"]
     return any(s.exists() and s.stat().st_mtime > t for s in srcs)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile libcoda.so if missing or stale; returns its path."""
-    if not force and not needs_build():
-        return LIB
+def build(force: bool = False, verbose: bool = False, experiments: bool = False) -> Path:
+    """Compile libcoda.so (or the experiment build libcoda_exp.so) if missing or stale."""
+    lib = LIB_EXP if experiments else LIB
+    if not force and not needs_build(lib):
+        return lib
     LIBDIR.mkdir(parents=True, exist_ok=True)
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", str(INCLUDE), "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
+    tmp = lib.with_suffix(".so.tmp")
+    extra = ["-DCODA_EXPERIMENTS"] if experiments else []
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-I", str(INCLUDE), "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         raise RuntimeError(f"nvcc failed ({proc.returncode}):\n{proc.stderr[-4000:]}")
     if verbose:
         print(proc.stderr)
-    (LIBDIR / "ptxas.log").write_text(proc.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    (LIBDIR / ("ptxas_exp.log" if experiments else "ptxas.log")).write_text(proc.stderr)
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":  # pragma: no cover

@@ -13,7 +13,11 @@ from pathlib import Path
 
 from . import errors
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libcoda.so"
+import os
+
+# CODA_LIB=exp selects the experiment build (tools/ only: measurement knobs, see coda.h)
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / (
+    "libcoda_exp.so" if os.environ.get("CODA_LIB") == "exp" else "libcoda.so")
 
 # ---- constants mirrored from include/coda.h ----
 BF16, F32, I64, I32 = 0, 1, 2, 3
@@ -55,6 +59,7 @@ EXPORTS = (
     "coda_combine_col_pieces",
     "coda_split_operand",
     "coda_convert_f32_bf16",
+    "coda_scale_rows",
     "coda_num_sms",
     "coda_set_option",
     "coda_version",
@@ -83,7 +88,7 @@ class Problem(ctypes.Structure):
         ("storage", ctypes.c_int32),
         ("out_dtype", ctypes.c_int32),
         ("store_main", ctypes.c_int32),
-        ("_pad", ctypes.c_int32),
+        ("sm_limit", ctypes.c_int32),
         ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_int64),
     ]
@@ -143,6 +148,7 @@ def _declare(lib) -> None:
     lib.coda_combine_col_pieces.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, vp]
     lib.coda_split_operand.argtypes = [P(Tensor), i32, i64, P(ctypes.c_int32), P(Tensor), vp]
     lib.coda_convert_f32_bf16.argtypes = [P(Tensor), P(Tensor), vp]
+    lib.coda_scale_rows.argtypes = [P(Tensor), vp, P(Tensor), vp]
     lib.coda_num_sms.argtypes = []
     lib.coda_set_option.argtypes = [ctypes.c_char_p, i32]
     lib.coda_version.argtypes = []
@@ -218,9 +224,41 @@ def call(name: str, *args, tag: str | None = None, flops: float = 0.0) -> None:
 
 
 def set_option(name: str, value: int) -> None:
-    """Process-wide engine option ("pdl", "cg", "generic", "raster", "split", "split_min_k",
-    "ring", "prefetch", "ablate"); see include/coda.h."""
+    """Process-wide engine schedule option ("pdl", "cg", "generic", "raster", "split",
+    "split_min_k"); see include/coda.h.  Measurement knobs ("ring", "prefetch", "ablate")
+    exist only in experiment builds (libcoda_exp.so, CODA_LIB=exp)."""
     check(load().coda_set_option(name.encode(), int(value)))
+
+
+_tls = threading.local()
+
+
+def sm_limit() -> int:
+    """SM cap of the GEMM launches enqueued by this thread (0 = every SM)."""
+    return getattr(_tls, "sm_limit", 0)
+
+
+class limit_sms:
+    """Context manager: GEMM launches enqueued inside use at most `n` SMs (0 = all).
+
+    Used around the backward of a data-parallel step so the NCCL all-reduce of
+    the weight gradients, running on a side stream, keeps SMs of its own instead
+    of waiting for gaps between persistent launches.  Thread-local; results are
+    identical with any cap."""
+
+    def __init__(self, n: int):
+        if n < 0:
+            raise errors.ConfigError(f"SM limit must be >= 0, got {n}")
+        self.n = int(n)
+
+    def __enter__(self):
+        self.prev = sm_limit()
+        _tls.sm_limit = self.n
+        return self
+
+    def __exit__(self, *exc):
+        _tls.sm_limit = self.prev
+        return False
 
 
 WORKSPACE_BYTES = 96 << 20
@@ -228,23 +266,35 @@ _workspaces: dict = {}
 
 
 def workspace(device):
-    """Zeroed scratch for wave-tail splitting, one per (device, current stream).
+    """Zeroed scratch for wave-tail splitting, one per (device, current stream), or None.
 
-    The split-K flags are reset by the launch that consumes them, so consecutive
+    The split-K counters are reset by the launch that consumes them, so consecutive
     launches on one stream can share the buffer; launches on different streams may
-    run concurrently and therefore get their own."""
+    run concurrently and therefore get their own.  A stream that is being captured
+    into a CUDA graph without a workspace of its own gets None (the launch runs
+    unsplit): borrowing another stream's buffer would let the graph's replay and
+    eager launches on the owner stream race on the same counters.  Call
+    `prepare_stream_workspace()` on the capture stream before capturing to keep
+    the split inside graphs."""
     import torch
 
     key = (str(device), torch.cuda.current_stream(device).cuda_stream)
     ws = _workspaces.get(key)
-    if ws is None and torch.cuda.is_current_stream_capturing():
-        # CUDA-graph capture runs on a side stream: reuse this device's workspace (the
-        # captured launches replay in stream order) rather than capturing a 96 MB memset
-        ws = next((w for (d, _), w in _workspaces.items() if d == str(device)), None)
     if ws is None:
+        if torch.cuda.is_current_stream_capturing():
+            return None
         ws = torch.zeros(WORKSPACE_BYTES // 4, dtype=torch.int32, device=device)
         _workspaces[key] = ws
     return ws
+
+
+def prepare_stream_workspace(device, stream) -> None:
+    """Allocate (outside capture) the split workspace owned by `stream`."""
+    import torch
+
+    with torch.cuda.stream(stream):
+        workspace(device)
+    torch.cuda.synchronize(device)
 
 
 def launch_count() -> int:

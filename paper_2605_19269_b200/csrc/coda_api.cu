@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -51,8 +52,18 @@ int esize(int dtype) {
     }
 }
 
-// Make the runtime's current device the one owning `ptr` (torch may run on any device).
-int bind_device(const void* ptr) {
+// Make the runtime's current device the one owning `ptr` (torch may run on any device)
+// for the duration of one entry point; the caller's current device is restored when
+// the guard goes out of scope, so nothing leaks into torch's current_device.
+struct DeviceGuard {
+    int prev = -1;
+    int dev = -1;
+    ~DeviceGuard() {
+        if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+    }
+};
+
+int bind_device(const void* ptr, DeviceGuard& g) {
     cudaPointerAttributes at{};
     cudaError_t e = cudaPointerGetAttributes(&at, ptr);
     if (e != cudaSuccess) {
@@ -63,10 +74,27 @@ int bind_device(const void* ptr) {
         return fail(CODA_E_BINDING, "pointer %p is not device memory", ptr);
     int cur = -1;
     cudaGetDevice(&cur);
+    g.prev = cur;
+    g.dev = at.device;
     if (cur != at.device) {
         if (cudaSetDevice(at.device) != cudaSuccess) return fail(CODA_E_CUDA, "cudaSetDevice(%d) failed", at.device);
     }
     return CODA_OK;
+}
+
+int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+// Per-device one-time setup (function attributes are per device): bit d of `mask`.
+constexpr int MAX_DEVICES = 64;
+bool first_use_on_device(std::atomic<uint64_t>& mask) {
+    const int d = current_device();
+    if (d < 0 || d >= MAX_DEVICES) return true;
+    const uint64_t bit = 1ull << d;
+    return (mask.fetch_or(bit) & bit) == 0;
 }
 
 int check_tensor2d(const coda_tensor_t* t, const char* name, int dtype) {
@@ -151,41 +179,53 @@ int make_map(CUtensorMap* out, const void* ptr, uint64_t d0, uint64_t d1, uint64
     return CODA_OK;
 }
 
-int g_num_sms = -1;
 int num_sms() {
-    if (g_num_sms < 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        int n = 0;
-        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
-            cudaGetLastError();
-            n = 0;
-        }
-        g_num_sms = n;
+    static std::atomic<int> cache[MAX_DEVICES];   // 0 = not queried yet
+    const int d = current_device();
+    if (d >= 0 && d < MAX_DEVICES && cache[d].load() > 0) return cache[d].load();
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
     }
-    return g_num_sms;
+    if (d >= 0 && d < MAX_DEVICES && n > 0) cache[d].store(n);
+    return n;
+}
+
+// SMs a launch may occupy: all of them, or the caller's cap (sm_limit > 0) so that
+// a concurrent collective on another stream keeps SMs of its own.
+int usable_sms(int sm_limit) {
+    const int n = num_sms();
+    return (sm_limit > 0 && sm_limit < n) ? sm_limit : n;
 }
 
 // ---------------------------------------------------------------- launches (PDL + clusters)
 // Runtime options (environment defaults, overridable through coda_set_option so
-// variants can be compared interleaved inside one process).
+// variants can be compared interleaved inside one process).  Product options change
+// only the schedule: every variant computes the reference program (the wave-tail
+// split changes f32 accumulation order, deterministically).  The measurement knobs
+// (L2 prefetch, ring depth, epilogue ablations that make results invalid) exist only
+// in experiment builds (-DCODA_EXPERIMENTS, _build.build(experiments=True) ->
+// libcoda_exp.so, used by tools/); the product library rejects them.
 struct Options {
     int pdl = 1;          // programmatic dependent launch
     int cg = 2;           // CTA-pair (2) or single-CTA (1) specialised kernels
     int generic = 0;      // force the generic epilogue interpreter
     int raster = 8;       // raster group (pair m-tiles)
     int split = 1;        // split the partial last wave along K
-    int split_min_k = 8192;   // ... only for launches with at least this K
-    int prefetch = 0;     // L2 prefetch distance (k-blocks beyond the smem ring)
-    int ablate = 0;       // measurement-only epilogue ablations (results invalid)
-    int ring = 0;         // operand ring stages in use (0 = the compiled depth)
+    int split_min_k = 8192;   // ... only for launches with at least this K (measured threshold)
+    int prefetch = 0;     // [experiments] L2 prefetch distance (k-blocks beyond the smem ring)
+    int ablate = 0;       // [experiments] epilogue ablations (results invalid)
+    int ring = 0;         // [experiments] operand ring stages in use (0 = the compiled depth)
     Options() {
-        if (const char* e = getenv("CODA_PREFETCH")) prefetch = atoi(e);
         if (const char* e = getenv("CODA_PDL")) pdl = e[0] != '0';
         if (const char* e = getenv("CODA_CG")) cg = e[0] == '1' ? 1 : 2;
         if (const char* e = getenv("CODA_FORCE_GENERIC")) generic = e[0] && e[0] != '0';
         if (const char* e = getenv("CODA_RASTER_GROUP")) { const int g = atoi(e); if (g > 0) raster = g; }
         if (const char* e = getenv("CODA_SPLIT")) split = e[0] != '0';
+#ifdef CODA_EXPERIMENTS
+        if (const char* e = getenv("CODA_PREFETCH")) prefetch = atoi(e);
+#endif
     }
 };
 Options& opts() {
@@ -226,16 +266,16 @@ int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
 }
 
 template <typename TS>
-int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const coda::GemmParams& P, cudaStream_t st) {
-    static bool configured = false;
+int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const coda::GemmParams& P, cudaStream_t st,
+                int sm_limit) {
+    static std::atomic<uint64_t> configured{0};
     const size_t smem = coda::gemm_smem_bytes();
-    if (!configured) {
+    if (first_use_on_device(configured)) {
         cudaError_t e = cudaFuncSetAttribute(coda::coda_gemm_kernel<TS>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(gemm smem)");
-        configured = true;
     }
-    const int nsm = num_sms();
+    const int nsm = usable_sms(sm_limit);
     const int grid = P.ntiles < nsm ? P.ntiles : nsm;
     return launch_pdl(coda::coda_gemm_kernel<TS>, dim3(grid), dim3(coda::NUM_THREADS), smem, st, 1,
                       "coda_gemm_kernel launch", ma, mb, P);
@@ -253,6 +293,7 @@ using coda::F_RESIDUAL;
 using coda::F_RMSBWD;
 using coda::F_RMSBWD_ACC;
 using coda::F_ROPE;
+using coda::F_ROWDOT;
 using coda::F_ROWSCALE;
 using coda::F_ROWVEC;
 using coda::F_STORE_MAIN;
@@ -279,24 +320,25 @@ using coda::F_SWIGLU_BWD;
     X(F_GATHER | F_LSE | F_STORE_MAIN)                                \
     X(F_GATHER | F_LSE)                                               \
     X(F_ROWSCALE | F_GATHER | F_LSE)                                  \
-    X(F_ROWSCALE | F_GATHER | F_LSE | F_STORE_MAIN)
+    X(F_ROWSCALE | F_GATHER | F_LSE | F_STORE_MAIN)                   \
+    X(F_ROWDOT | F_ROWSCALE | F_STORE_MAIN)                           \
+    X(F_ROWDOT | F_ROWSCALE | F_STORE_MAIN | F_OUT_F32)
 
 template <int FL, int CG>
 int launch_fast_fl(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mm, const CUtensorMap& mx,
-                   const CUtensorMap& s0, const CUtensorMap& s1, const coda::FastParams& P, cudaStream_t st) {
-    static bool configured = false;
+                   const CUtensorMap& s0, const CUtensorMap& s1, const coda::FastParams& P, cudaStream_t st,
+                   int units) {
+    static std::atomic<uint64_t> configured{0};
     const size_t smem = coda::fast_smem_bytes<CG, FL>();
     auto kern = coda::coda_gemm_fast<__nv_bfloat16, FL, CG>;
-    if (!configured) {
+    if (first_use_on_device(configured)) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(fast smem)");
         if (CG > 1) {
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
             if (e != cudaSuccess) cudaGetLastError();
         }
-        configured = true;
     }
-    const int units = num_sms() / CG;
     const int grid = (P.mp.nitems < units ? P.mp.nitems : units) * CG;
     return launch_pdl(kern, dim3((unsigned)grid), dim3(coda::FAST_THREADS), smem, st, CG, "coda_gemm_fast launch",
                       ma, mb, mm, mx, s0, s1, P);
@@ -313,11 +355,11 @@ bool fast_supported(int fl) {
 
 int launch_fast(int fl, int cg, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mm,
                 const CUtensorMap& mx, const CUtensorMap& s0, const CUtensorMap& s1, const coda::FastParams& P,
-                cudaStream_t st) {
-#define CODA_FAST_CASE(F)                                                         \
-    if (fl == (F))                                                                \
-        return cg == 2 ? launch_fast_fl<(F), 2>(ma, mb, mm, mx, s0, s1, P, st)    \
-                       : launch_fast_fl<(F), 1>(ma, mb, mm, mx, s0, s1, P, st);
+                cudaStream_t st, int units) {
+#define CODA_FAST_CASE(F)                                                                \
+    if (fl == (F))                                                                       \
+        return cg == 2 ? launch_fast_fl<(F), 2>(ma, mb, mm, mx, s0, s1, P, st, units)    \
+                       : launch_fast_fl<(F), 1>(ma, mb, mm, mx, s0, s1, P, st, units);
     CODA_FAST_SETS(CODA_FAST_CASE)
 #undef CODA_FAST_CASE
     return fail(CODA_E_CONFIG, "no specialised kernel for flags 0x%x", fl);
@@ -348,31 +390,34 @@ int match_fast(const coda_problem_t* pr, const coda_step_t* steps, int nsteps, c
         const coda_step_t& st = steps[s];
         if (st.width2 != 2) return -1;   // every fast op runs at factor 1
         switch (st.op) {
-        case CODA_OP_ROW_SCALE: if (!rank_ok(1)) return -1; fl |= F_ROWSCALE; break;
-        case CODA_OP_RESIDUAL_ADD: if (!rank_ok(2)) return -1; fl |= F_RESIDUAL; break;
-        case CODA_OP_AUX_TILE_STORE: if (!rank_ok(3)) return -1; fl |= F_AUX; break;
+        case CODA_OP_PARTIAL_ROWDOT:
+            if (!rank_ok(1) || !stores[st.arg[1]].aligned) return -1;
+            fl |= F_ROWDOT; break;
+        case CODA_OP_ROW_SCALE: if (!rank_ok(2)) return -1; fl |= F_ROWSCALE; break;
+        case CODA_OP_RESIDUAL_ADD: if (!rank_ok(3)) return -1; fl |= F_RESIDUAL; break;
+        case CODA_OP_AUX_TILE_STORE: if (!rank_ok(4)) return -1; fl |= F_AUX; break;
         case CODA_OP_PARTIAL_SUMSQ:
-            if (!rank_ok(4) || !stores[st.arg[0]].aligned) return -1;
+            if (!rank_ok(5) || !stores[st.arg[0]].aligned) return -1;
             fl |= F_SUMSQ; break;
-        case CODA_OP_ROW_VEC_MUL: if (!rank_ok(5)) return -1; fl |= F_ROWVEC; break;
-        case CODA_OP_ROPE: if (!rank_ok(6)) return -1; fl |= F_ROPE; break;
-        case CODA_OP_TARGET_GATHER: if (!rank_ok(7)) return -1; fl |= F_GATHER; break;
+        case CODA_OP_ROW_VEC_MUL: if (!rank_ok(6)) return -1; fl |= F_ROWVEC; break;
+        case CODA_OP_ROPE: if (!rank_ok(7)) return -1; fl |= F_ROPE; break;
+        case CODA_OP_TARGET_GATHER: if (!rank_ok(8)) return -1; fl |= F_GATHER; break;
         case CODA_OP_ONLINE_LSE:
-            if (!rank_ok(8) || !stores[st.arg[0]].aligned) return -1;
+            if (!rank_ok(9) || !stores[st.arg[0]].aligned) return -1;
             fl |= F_LSE; break;
-        case CODA_OP_SWIGLU: if (!rank_ok(9)) return -1; fl |= F_SWIGLU; break;
+        case CODA_OP_SWIGLU: if (!rank_ok(10)) return -1; fl |= F_SWIGLU; break;
         case CODA_OP_SWIGLU_BWD:
-            if (!rank_ok(9) || !stores[st.arg[2]].aligned) return -1;
+            if (!rank_ok(10) || !stores[st.arg[2]].aligned) return -1;
             fl |= F_SWIGLU_BWD; break;
         case CODA_OP_RMSNORM_BWD:
-            if (!rank_ok(9) || !stores[st.arg[6]].aligned) return -1;
+            if (!rank_ok(10) || !stores[st.arg[6]].aligned) return -1;
             fl |= F_RMSBWD | (st.arg[4] >= 0 ? F_RMSBWD_ACC : 0); break;
         default: return -1;
         }
     }
     if (pr->store_main) fl |= F_STORE_MAIN;
     if (pr->out_dtype == CODA_F32) {
-        if (fl != F_STORE_MAIN) return -1;
+        if (fl != F_STORE_MAIN && fl != (F_ROWDOT | F_ROWSCALE | F_STORE_MAIN)) return -1;
         fl |= F_OUT_F32;
     }
     return fast_supported(fl) ? fl : -1;
@@ -386,7 +431,13 @@ extern "C" {
 
 const char* coda_last_error(void) { return g_err.c_str(); }
 
-const char* coda_version(void) { return "coda sm_100a tcgen05 128x256x64 4-stage persistent"; }
+const char* coda_version(void) {
+#ifdef CODA_EXPERIMENTS
+    return "coda sm_100a tcgen05 2-CTA 256x256x64 persistent (experiments build)";
+#else
+    return "coda sm_100a tcgen05 2-CTA 256x256x64 persistent";
+#endif
+}
 
 int coda_num_sms(void) { return num_sms(); }
 
@@ -399,17 +450,25 @@ int coda_set_option(const char* name, int value) {
         opts().cg = value;
     } else if (n == "generic") opts().generic = value != 0;
     else if (n == "split") opts().split = value != 0;
-    else if (n == "split_min_k") opts().split_min_k = value;
+    else if (n == "split_min_k") {
+        if (value < 0) return fail(CODA_E_CONFIG, "split_min_k must be >= 0");
+        opts().split_min_k = value;
+    } else if (n == "raster") {
+        if (value < 1) return fail(CODA_E_CONFIG, "raster group must be >= 1");
+        opts().raster = value;
+    }
+#ifdef CODA_EXPERIMENTS
     else if (n == "ablate") opts().ablate = value;
     else if (n == "ring") opts().ring = value;
     else if (n == "prefetch") {
         if (value < 0 || value > 64) return fail(CODA_E_CONFIG, "prefetch distance must be in [0, 64]");
         opts().prefetch = value;
     }
-    else if (n == "raster") {
-        if (value < 1) return fail(CODA_E_CONFIG, "raster group must be >= 1");
-        opts().raster = value;
-    } else return fail(CODA_E_CONFIG, "unknown option %s", name);
+#else
+    else if (n == "ablate" || n == "ring" || n == "prefetch")
+        return fail(CODA_E_CONFIG, "option %s exists only in experiment builds (-DCODA_EXPERIMENTS)", name);
+#endif
+    else return fail(CODA_E_CONFIG, "unknown option %s", name);
     return CODA_OK;
 }
 
@@ -437,7 +496,8 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
     if (nsteps < 0 || nsteps > CODA_MAX_STEPS) return fail(CODA_E_PROGRAM, "too many program steps (%d)", nsteps);
     if (noperands < 0 || noperands > CODA_MAX_OPERANDS || nstores < 0 || nstores > CODA_MAX_STORES)
         return fail(CODA_E_PROGRAM, "too many operands/stores");
-    if ((rc = bind_device(a->ptr))) return rc;
+    DeviceGuard dg;
+    if ((rc = bind_device(a->ptr, dg))) return rc;
 
     coda::GemmParams P;
     memset(&P, 0, sizeof(P));
@@ -572,7 +632,7 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         F.mp = coda::MainParams{P.M, P.N, P.K, ntm, P.ntn, P.nk, ntiles, P.a_mn, P.b_mn,
                                 raster_group(ntm, tile_m, K), ntiles, 0, 1, ntiles, opts().prefetch, opts().ring};
         // wave-tail split: the r tiles of the partial last wave run as s K-pieces each
-        const int units = num_sms() / cg;
+        const int units = std::max(1, usable_sms(pr->sm_limit) / cg);
         const int r = units > 0 ? ntiles % units : 0;
         // only long-K launches: the dump / fixed-order fold costs ~10-20 us, which a split of a
         // short mainloop cannot repay (tools/gemm_bench.py: +9 % at K=16384, -8 % at K=4096)
@@ -582,9 +642,9 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
             if (sp > P.nk / 4) sp = P.nk / 4;
             if (sp > 16) sp = 16;
             const int64_t tile_bytes = (int64_t)cg * coda::BM * coda::BN * 4;
-            while (sp >= 2 && ((int64_t)r * (sp - 1) * tile_bytes > pr->workspace_bytes - (64 << 10) ||
-                               (int64_t)r * (sp - 1) * cg * coda::FAST_EPI_WARPS * 4 > (64 << 10)))
-                --sp;
+            // every piece dumps its partial tile; one arrival counter per (tail tile, rank, warp)
+            while (sp >= 2 && (int64_t)r * sp * tile_bytes > pr->workspace_bytes - (64 << 10)) --sp;
+            if ((int64_t)r * cg * coda::FAST_EPI_WARPS * 4 > (64 << 10)) sp = 0;
             if (sp >= 2) {
                 F.mp.full_tiles = ntiles - r;
                 F.mp.tail = r;
@@ -607,6 +667,10 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
             const coda::DevOperand* o = P.opnd;
             switch (cs.op) {
             case CODA_OP_ROW_SCALE: F.rowscale = (const float*)o[cs.arg[0]].ptr; break;
+            case CODA_OP_PARTIAL_ROWDOT:
+                F.rowdot_x = o[cs.arg[0]].ptr; F.ld_rowdot_x = o[cs.arg[0]].ld;
+                F.rowpart = (float*)P.store[cs.arg[1]].ptr; F.ld_rowpart = P.store[cs.arg[1]].ld;
+                F.rowpart_map = P.store[cs.arg[1]].map; break;
             case CODA_OP_RESIDUAL_ADD: F.residual = o[cs.arg[0]].ptr; F.ld_res = o[cs.arg[0]].ld; break;
             case CODA_OP_AUX_TILE_STORE: aux_slot = cs.arg[0]; break;
             case CODA_OP_PARTIAL_SUMSQ:
@@ -677,6 +741,7 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
                             CODA_BF16, box_cols * 2);
         };
         if (fl & F_RESIDUAL) rc = side_map(&s0, F.residual, F.ld_res, N, 32);
+        if (!rc && (fl & F_ROWDOT)) rc = side_map(&s0, F.rowdot_x, F.ld_rowdot_x, N, 32);
         if (!rc && (fl & F_ROPE)) {
             if (F.rope_h > 0) {   // compact: 32 rows x 16 angles (32 B, SWIZZLE_32B)
                 rc = side_map(&s0, rope_c, ld_rope_c, F.rope_h / 2, 16);
@@ -692,10 +757,10 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
             if (!rc && (fl & F_RMSBWD_ACC)) rc = side_map(&s1, F.grad_in, F.ld_gin, N, 32);
         }
         if (rc) return rc;
-        return launch_fast(fl, cg, ma, mb, mm, mx, s0, s1, F, st);
+        return launch_fast(fl, cg, ma, mb, mm, mx, s0, s1, F, st, units);
     }
-    if (sdt == CODA_BF16) return launch_gemm<__nv_bfloat16>(ma, mb, P, st);
-    return launch_gemm<float>(ma, mb, P, st);
+    if (sdt == CODA_BF16) return launch_gemm<__nv_bfloat16>(ma, mb, P, st, pr->sm_limit);
+    return launch_gemm<float>(ma, mb, P, st, pr->sm_limit);
 }
 
 int coda_finalize_rms(const float* p, int64_t m, int64_t nb, int64_t ld, int64_t d, float eps, float* r,
@@ -703,12 +768,12 @@ int coda_finalize_rms(const float* p, int64_t m, int64_t nb, int64_t ld, int64_t
     if (m <= 0 || nb <= 0) return fail(CODA_E_DIMENSION, "finalize_rms: empty partials");
     if (d <= 0) return fail(CODA_E_DEGENERATE, "partial blocks cover no columns");
     int rc;
-    if ((rc = bind_device(p))) return rc;
+    DeviceGuard dg;
+    if ((rc = bind_device(p, dg))) return rc;
     if (nb <= 1024) {
-        static bool cfg_done = false;
-        if (!cfg_done) {
+        static std::atomic<uint64_t> cfg_done{0};
+        if (first_use_on_device(cfg_done)) {
             cudaFuncSetAttribute(coda::coda_finalize_rms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
-            cfg_done = true;
         }
         const size_t smem = (size_t)coda::FIN_ROWS * (nb + 1) * 4;
         return launch_pdl(coda::coda_finalize_rms_kernel, dim3((unsigned)((m + coda::FIN_ROWS - 1) / coda::FIN_ROWS)),
@@ -722,13 +787,13 @@ int coda_finalize_rowdot(const float* p, int64_t m, int64_t nb, int64_t ld, int6
     if (m <= 0 || nb <= 0) return fail(CODA_E_DIMENSION, "finalize_rowdot: empty partials");
     if (d <= 0) return fail(CODA_E_CONFIG, "normalized width must be positive, got %lld", (long long)d);
     int rc;
-    if ((rc = bind_device(p))) return rc;
+    DeviceGuard dg;
+    if ((rc = bind_device(p, dg))) return rc;
     if (nb <= 1024) {
-        static bool cfg_done = false;
-        if (!cfg_done) {
+        static std::atomic<uint64_t> cfg_done{0};
+        if (first_use_on_device(cfg_done)) {
             cudaFuncSetAttribute(coda::coda_finalize_rowdot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  140 * 1024);
-            cfg_done = true;
         }
         const size_t smem = (size_t)coda::FIN_ROWS * (nb + 1) * 4;
         return launch_pdl(coda::coda_finalize_rowdot_kernel, dim3((unsigned)((m + coda::FIN_ROWS - 1) / coda::FIN_ROWS)),
@@ -741,7 +806,8 @@ int coda_finalize_rowdot(const float* p, int64_t m, int64_t nb, int64_t ld, int6
 int coda_reduce_row_partials(const float* p, int64_t tm, int64_t n, int64_t ld, float* out, void* stream) {
     if (tm <= 0 || n <= 0) return fail(CODA_E_DIMENSION, "reduce_row_partials: empty partials");
     int rc;
-    if ((rc = bind_device(p))) return rc;
+    DeviceGuard dg;
+    if ((rc = bind_device(p, dg))) return rc;
     return launch_pdl(coda::coda_reduce_row_partials_kernel, dim3(grid1d(n, 256)), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_reduce_row_partials_kernel",
         p, tm, n, ld, out);
 }
@@ -749,7 +815,8 @@ int coda_reduce_row_partials(const float* p, int64_t tm, int64_t n, int64_t ld, 
 int coda_combine_lse(const float* p, int64_t m, int64_t nb, int64_t ld, float* lse, void* stream) {
     if (m <= 0 || nb <= 0) return fail(CODA_E_DIMENSION, "combine_lse: empty partials");
     int rc;
-    if ((rc = bind_device(p))) return rc;
+    DeviceGuard dg;
+    if ((rc = bind_device(p, dg))) return rc;
     return launch_pdl(coda::coda_combine_lse_kernel, dim3(grid1d(m, 256)), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_combine_lse_kernel",
         p, m, nb, ld, lse);
 }
@@ -757,7 +824,8 @@ int coda_combine_lse(const float* p, int64_t m, int64_t nb, int64_t ld, float* l
 int coda_cross_entropy_finalize(const float* target, const float* lse, int64_t m, float* losses, void* stream) {
     if (m <= 0) return fail(CODA_E_DIMENSION, "cross_entropy_finalize: empty");
     int rc;
-    if ((rc = bind_device(lse))) return rc;
+    DeviceGuard dg;
+    if ((rc = bind_device(lse, dg))) return rc;
     return launch_pdl(coda::coda_ce_finalize_kernel, dim3(grid1d(m, 256)), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_ce_finalize_kernel",
         target, lse, m, losses);
 }
@@ -787,7 +855,8 @@ int coda_rope_backward_stat_compact(const coda_tensor_t* grad, const coda_tensor
             return fail(CODA_E_DIMENSION, "compact table must be (%lld, %lld)", (long long)grad->rows,
                         (long long)(h / 2));
     }
-    if ((rc = bind_device(grad->ptr))) return rc;
+    DeviceGuard dg;
+    if ((rc = bind_device(grad->ptr, dg))) return rc;
     const unsigned grid = (unsigned)(grad->rows < 148 * 8 ? grad->rows : 148 * 8);
     return launch_pdl(coda::coda_rope_backward_stat128_compact_kernel, dim3(grid), dim3(256), 0,
                       (cudaStream_t)stream, 1, "coda::coda_rope_backward_stat128_compact_kernel",
@@ -813,7 +882,8 @@ int coda_rope_backward_stat(const coda_tensor_t* grad, const coda_tensor_t* rota
                         (long long)grad->cols);
     }
     if (grad->cols % 2) return fail(CODA_E_DIMENSION, "rotary width must be even, got %lld", (long long)grad->cols);
-    if ((rc = bind_device(grad->ptr))) return rc;
+    DeviceGuard dg;
+    if ((rc = bind_device(grad->ptr, dg))) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     if (block_start == nullptr) {
         if (nb != (grad->cols + 127) / 128) return fail(CODA_E_DIMENSION, "rope_backward_stat: nb != ceil(n/128)");
@@ -855,7 +925,8 @@ int coda_combine_row_pieces(const float* pieces, int64_t m, int64_t np, int64_t 
                             int64_t nb, int pairs, float* out, int64_t ldo, void* stream) {
     if (m <= 0 || np <= 0 || nb <= 0) return fail(CODA_E_DIMENSION, "combine_row_pieces: empty");
     int rc;
-    if ((rc = bind_device(pieces))) return rc;
+    DeviceGuard dg;
+    if ((rc = bind_device(pieces, dg))) return rc;
     return launch_pdl(coda::coda_combine_row_pieces_kernel, dim3(grid1d(m * nb, 256)), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_combine_row_pieces_kernel",
         pieces, m, np, ldp, block_ptr, nb, pairs, out, ldo);
 }
@@ -865,7 +936,8 @@ int coda_combine_col_pieces(const float* pieces, int64_t np, int64_t n, int64_t 
     if (n <= 0 || np <= 0 || nb <= 0) return fail(CODA_E_DIMENSION, "combine_col_pieces: empty");
     if (nb > 65535) return fail(CODA_E_CONFIG, "combine_col_pieces: too many blocks");
     int rc;
-    if ((rc = bind_device(pieces))) return rc;
+    DeviceGuard dg;
+    if ((rc = bind_device(pieces, dg))) return rc;
     dim3 grid(grid1d(n, 256), (unsigned)nb);
     return launch_pdl(coda::coda_combine_col_pieces_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_combine_col_pieces_kernel",
         pieces, np, n, ldp, block_ptr, nb, out, ldo);
@@ -885,10 +957,27 @@ int coda_split_operand(const coda_tensor_t* src, int k_axis, int64_t kp, const i
         if (pattern[i] < 0 || pattern[i] > 2) return fail(CODA_E_CONFIG, "split: bad pattern");
         pat.t[i] = pattern[i];
     }
-    if ((rc = bind_device(src->ptr))) return rc;
+    DeviceGuard dg;
+    if ((rc = bind_device(src->ptr, dg))) return rc;
     return launch_pdl(coda::coda_split_operand_kernel, dim3(grid1d(drows * dcols, 256)), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_split_operand_kernel",
         (const float*)src->ptr, src->rows, src->cols, src->ld, k_axis, kp, pat, (__nv_bfloat16*)dst->ptr, drows,
         dcols, dst->ld);
+}
+
+int coda_scale_rows(const coda_tensor_t* src, const float* scale, coda_tensor_t* dst, void* stream) {
+    int rc;
+    if ((rc = check_tensor2d(src, "scale_rows src", CODA_BF16))) return rc;
+    if ((rc = check_tensor2d(dst, "scale_rows dst", CODA_BF16))) return rc;
+    if (!scale) return fail(CODA_E_BINDING, "scale_rows: null scale vector");
+    if (src->rows != dst->rows || src->cols != dst->cols) return fail(CODA_E_DIMENSION, "scale_rows: shapes differ");
+    DeviceGuard dg;
+    if ((rc = bind_device(src->ptr, dg))) return rc;
+    const int vec = src->cols % 8 == 0 && src->ld % 8 == 0 && dst->ld % 8 == 0;
+    const int64_t work = vec ? src->rows * (src->cols / 8) : src->rows * src->cols;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 148 * 8));
+    return launch_pdl(coda::coda_scale_rows_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, 1,
+                      "coda::coda_scale_rows_kernel", (const __nv_bfloat16*)src->ptr, src->rows, src->cols, src->ld,
+                      scale, (__nv_bfloat16*)dst->ptr, dst->ld, vec);
 }
 
 int coda_convert_f32_bf16(const coda_tensor_t* src, coda_tensor_t* dst, void* stream) {
@@ -896,7 +985,8 @@ int coda_convert_f32_bf16(const coda_tensor_t* src, coda_tensor_t* dst, void* st
     if (src->dtype != CODA_F32 || dst->dtype != CODA_BF16) return fail(CODA_E_BINDING, "convert: dtypes");
     if (src->rows != dst->rows || src->cols != dst->cols) return fail(CODA_E_DIMENSION, "convert: shapes differ");
     int rc;
-    if ((rc = bind_device(src->ptr))) return rc;
+    DeviceGuard dg;
+    if ((rc = bind_device(src->ptr, dg))) return rc;
     const int vec = src->ld % 4 == 0 && dst->ld % 8 == 0 && reinterpret_cast<uintptr_t>(src->ptr) % 16 == 0 &&
                     reinterpret_cast<uintptr_t>(dst->ptr) % 16 == 0;
     const int64_t work = vec ? src->rows * (src->cols / 8) : src->rows;

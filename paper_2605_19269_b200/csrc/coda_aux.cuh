@@ -37,6 +37,7 @@ __global__ void coda_finalize_rms_kernel(const float* __restrict__ p, int64_t m,
                                          float d, float eps, float* __restrict__ r) {
     extern __shared__ float tile[];
     griddep_wait();
+    griddep_launch_dependents();
     const int64_t row0 = (int64_t)blockIdx.x * FIN_ROWS;
     const float t = staged_row_total(p, m, nb, ld, tile, row0);
     if (threadIdx.x < FIN_ROWS && row0 + threadIdx.x < m)
@@ -47,6 +48,7 @@ __global__ void coda_finalize_rowdot_kernel(const float* __restrict__ p, int64_t
                                             float d, float* __restrict__ s) {
     extern __shared__ float tile[];
     griddep_wait();
+    griddep_launch_dependents();
     const int64_t row0 = (int64_t)blockIdx.x * FIN_ROWS;
     const float t = staged_row_total(p, m, nb, ld, tile, row0);
     if (threadIdx.x < FIN_ROWS && row0 + threadIdx.x < m) s[row0 + threadIdx.x] = __fdiv_rn(t, d);
@@ -56,6 +58,7 @@ __global__ void coda_finalize_rowdot_kernel(const float* __restrict__ p, int64_t
 __global__ void coda_finalize_rms_wide_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld, float d,
                                               float eps, float* __restrict__ r) {
     griddep_wait();
+    griddep_launch_dependents();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
     float t = 0.0f;
@@ -66,6 +69,7 @@ __global__ void coda_finalize_rms_wide_kernel(const float* __restrict__ p, int64
 __global__ void coda_finalize_rowdot_wide_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
                                                  float d, float* __restrict__ s) {
     griddep_wait();
+    griddep_launch_dependents();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
     float t = 0.0f;
@@ -77,6 +81,7 @@ __global__ void coda_finalize_rowdot_wide_kernel(const float* __restrict__ p, in
 __global__ void coda_reduce_row_partials_kernel(const float* __restrict__ p, int64_t tm, int64_t n, int64_t ld,
                                            float* __restrict__ out) {
     griddep_wait();
+    griddep_launch_dependents();
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     float t = 0.0f;
@@ -95,6 +100,7 @@ __device__ __forceinline__ void lse_merge(float& m, float& s, float mb, float sb
 __global__ void coda_combine_lse_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
                                    float* __restrict__ lse) {
     griddep_wait();
+    griddep_launch_dependents();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
     float mx = -INFINITY, s = 0.0f;
@@ -105,6 +111,7 @@ __global__ void coda_combine_lse_kernel(const float* __restrict__ p, int64_t m, 
 __global__ void coda_ce_finalize_kernel(const float* __restrict__ target, const float* __restrict__ lse, int64_t m,
                                    float* __restrict__ loss) {
     griddep_wait();
+    griddep_launch_dependents();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) loss[i] = lse[i] - target[i];
 }
@@ -114,6 +121,7 @@ __global__ void coda_combine_row_pieces_kernel(const float* __restrict__ pc, int
                                           const int32_t* __restrict__ ptr, int64_t nb, int pairs,
                                           float* __restrict__ out, int64_t ldo) {
     griddep_wait();
+    griddep_launch_dependents();
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= m * nb) return;
     const int64_t i = idx / nb, b = idx % nb;
@@ -135,6 +143,7 @@ __global__ void coda_combine_col_pieces_kernel(const float* __restrict__ pc, int
                                           const int32_t* __restrict__ ptr, int64_t nb,
                                           float* __restrict__ out, int64_t ldo) {
     griddep_wait();
+    griddep_launch_dependents();
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t b = blockIdx.y;
     if (j >= n || b >= nb) return;
@@ -156,6 +165,7 @@ coda_rope_backward_stat_kernel(const TS* __restrict__ g, int64_t ldg, const TS* 
                           int64_t n, const int32_t* __restrict__ bstart, int64_t nb,
                           TS* __restrict__ gz, int64_t ldz, float* __restrict__ rowdot, int64_t ldd) {
     griddep_wait();
+    griddep_launch_dependents();
     extern __shared__ float prod[];
     const int64_t i = blockIdx.x;
     constexpr int V = Io<TS>::V;
@@ -212,6 +222,7 @@ coda_rope_backward_stat128_kernel(const TS* __restrict__ g, int64_t ldg, const T
                              int64_t m, int64_t n, TS* __restrict__ gz, int64_t ldz, float* __restrict__ rowdot,
                              int64_t ldd) {
     griddep_wait();
+    griddep_launch_dependents();
     constexpr int V = Io<TS>::V;
     constexpr int LPB = 128 / V;                       // lanes per 128-column block
     const int lane = threadIdx.x & 31;
@@ -271,6 +282,7 @@ coda_rope_backward_stat128_compact_kernel(const __nv_bfloat16* __restrict__ g, i
                                           int64_t m, int64_t n, __nv_bfloat16* __restrict__ gz, int64_t ldz,
                                           float* __restrict__ rowdot, int64_t ldd) {
     griddep_wait();
+    griddep_launch_dependents();
     using TS = __nv_bfloat16;
     constexpr int V = Io<TS>::V;                       // 8
     constexpr int LPB = 128 / V;
@@ -363,6 +375,7 @@ __global__ void coda_split_operand_kernel(const float* __restrict__ src, int64_t
                                      int k_axis, int64_t kp, SplitPattern pat,
                                      __nv_bfloat16* __restrict__ dst, int64_t drows, int64_t dcols, int64_t ldd) {
     griddep_wait();
+    griddep_launch_dependents();
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= drows * dcols) return;
     const int64_t r = idx / dcols, c = idx % dcols;
@@ -383,6 +396,7 @@ __global__ void __launch_bounds__(256)
 coda_convert_f32_bf16_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
                              __nv_bfloat16* __restrict__ dst, int64_t ldd, int vec) {
     griddep_wait();
+    griddep_launch_dependents();
     // 8 elements per thread step: two 16-B streaming loads, one 16-B store (when rows are
     // 16-B aligned: vec = 1); HBM-bound, 6 B per element.  Unaligned rows go scalar.
     const int64_t vpr = vec ? cols / 8 : 0;
@@ -403,6 +417,36 @@ coda_convert_f32_bf16_kernel(const float* __restrict__ src, int64_t rows, int64_
     if (c0 < cols) {
         for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride)
             for (int64_t c = c0; c < cols; ++c) dst[r * ldd + c] = __float2bfloat16_rn(src[r * lds + c]);
+    }
+}
+
+// Row scaling of a bf16 matrix: dst[i, :] = bf16(scale[i] * src[i, :]) (RNE).  Folds an
+// RMSNorm gain into the weight matrix that consumes the normalized rows,
+// W' = diag(gamma) W, once per weight update.  HBM-bound: 4 B per element; 8 elements
+// (one 16-B load and store) per thread step when rows are 16-B aligned.
+__global__ void __launch_bounds__(256)
+coda_scale_rows_kernel(const __nv_bfloat16* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
+                       const float* __restrict__ scale, __nv_bfloat16* __restrict__ dst, int64_t ldd, int vec) {
+    griddep_wait();
+    griddep_launch_dependents();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (vec) {
+        const int64_t vpr = cols / 8;
+        const int64_t total = rows * vpr;
+        for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < total; v += stride) {
+            const int64_t r = v / vpr, c = (v - r * vpr) * 8;
+            const float g = __ldg(scale + r);
+            float x[8];
+            Io<__nv_bfloat16>::load(src + r * lds + c, x);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] *= g;
+            Io<__nv_bfloat16>::store(dst + r * ldd + c, x);
+        }
+        return;
+    }
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < rows * cols; v += stride) {
+        const int64_t r = v / cols, c = v - r * cols;
+        dst[r * ldd + c] = __float2bfloat16_rn(__ldg(scale + r) * __bfloat162float(src[r * lds + c]));
     }
 }
 

@@ -16,7 +16,7 @@
 //     across the four row quadrants through 2 KiB of smem, in fixed order.
 //
 // Op order is the canonical order of the reference programs:
-//   acc_in -> RowScale -> ResidualAdd -> AuxTileStore -> PartialSumSq ->
+//   acc_in -> PartialRowDot -> RowScale -> ResidualAdd -> AuxTileStore -> PartialSumSq ->
 //   RowVecMul -> PairwiseRope -> PairwiseSwiglu | PairwiseSwigluBackward |
 //   RmsNormBackwardLocal -> main store.
 #pragma once
@@ -44,6 +44,7 @@ enum FastFlags : int {
     F_OUT_F32 = 1 << 11,
     F_GATHER = 1 << 12,     // TargetGather: target[row] = tile[row, label[row]]
     F_LSE = 1 << 13,        // OnlineLse: (max, scaled sum) pairs per piece (rowpart holds pairs)
+    F_ROWDOT = 1 << 14,     // PartialRowDot against a side tile, before RowScale (rowpart = row sums)
 };
 
 constexpr int FAST_EPI_WARPS = 8;
@@ -79,6 +80,8 @@ struct FastParams {
     float* colpart;
     int64_t ld_colpart;
     const int32_t* colpart_map;
+    const void* rowdot_x;   // F_ROWDOT: the tile operand X of sum(tile * X)
+    int64_t ld_rowdot_x;
     const int64_t* labels;
     float* target;
     // tail-split workspace: f32 partial accumulators [tail][piece < split-1][rank][128][256]
@@ -93,22 +96,23 @@ struct FastParams {
     int rope_h;
 };
 
-__device__ __forceinline__ bool item_runs_program(const MainParams& mp, const Work& w) {
-    return w.piece < 0 || w.piece == mp.split - 1;
-}
-__device__ __forceinline__ void flag_release(int* f) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(f), "r"(1) : "memory");
-}
-__device__ __forceinline__ int flag_acquire(const int* f) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-    return v;
+// Whole tiles run the program in the unit that computed them; the pieces of a split
+// tail tile are reduced by whichever piece finishes last (see the piece path below),
+// which is only known at run time, so only whole tiles prefetch their side operands.
+__device__ __forceinline__ bool item_prefetches_side(const Work& w) { return w.piece < 0; }
+// Arrival counter of one (tail tile, CTA rank, epilogue warp) region: returns the value
+// before this arrival.  Release orders this warp's dumped partial before the increment;
+// acquire orders the last arriver's reads of the other pieces after it.
+__device__ __forceinline__ int counter_arrive(int* c) {
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(c) : "memory");
+    return old;
 }
 
 // Side operands (residual, cos/sin, preact, pre_norm/grad_in) are TMA-loaded per
 // epilogue warp into a 4 KiB swizzled buffer, one 32-row chunk ahead; kernels that
 // have them give up one ring stage for the buffers.
-constexpr int F_SIDE = F_RESIDUAL | F_ROPE | F_SWIGLU_BWD | F_RMSBWD;
+constexpr int F_SIDE = F_RESIDUAL | F_ROPE | F_SWIGLU_BWD | F_RMSBWD | F_ROWDOT;
 constexpr int SIDE_BYTES = 4096;
 
 template <int CG, int FL>
@@ -121,7 +125,7 @@ struct FastGeom {
     static constexpr int CHUNK_BYTES = (FL & F_SWIGLU_BWD) ? 4096
                                      : (FL & F_ROPE) ? 4096
                                      : (FL & F_RMSBWD) ? ((FL & F_RMSBWD_ACC) ? 4096 : 2048)
-                                     : (FL & F_RESIDUAL) ? 2048 : 0;
+                                     : (FL & (F_RESIDUAL | F_ROWDOT)) ? 2048 : 0;
 };
 
 template <int CG, int FL>
@@ -401,52 +405,51 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         };
         if (FG::SIDE && lane == 0 && unit < mp.nitems) {
             const Work w0 = work_item(mp, unit);
-            if (item_runs_program(mp, w0)) side_issue(w0.tm, w0.tn, 0);
+            if (item_prefetches_side(w0)) side_issue(w0.tm, w0.tn, 0);
         }
-        const int nparts = mp.split - 1;   // partial pieces per split tile
+        const int split = mp.split;
         for (int i = unit; i < mp.nitems; i += nunits) {
             const Work w = work_item(mp, i);
             const int tm = w.tm, tn = w.tn;
             const int m0 = tm * G::TILE_M + rank * BM;
             const int n0 = tn * BN;
-            if (w.piece >= 0 && w.piece < nparts) {
-                // an early K piece of a split tail tile: dump the raw f32 accumulator and signal
+            // a K piece of a split tail tile: dump the raw f32 accumulator of this warp's
+            // 32 x 128 region, then arrive on the region's counter.  The last of the
+            // `split` arrivals sums every dumped piece in fixed piece order and runs the
+            // program; the others are done.  No piece ever waits for another, so the
+            // launch needs no co-residency of its clusters.
+            const bool piece = w.piece >= 0;
+            const int64_t ws_region = (int64_t)(q * 32 + lane) * BN + h * 128;
+            if (piece) {
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
                 const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + h * 128);
-                float* dst = P.ws + ((int64_t)(w.tail_idx * nparts + w.piece) * CG + rank) * (BM * BN) +
-                             (int64_t)(q * 32 + lane) * BN + h * 128;
+                float* dst = P.ws + ((int64_t)(w.tail_idx * split + w.piece) * CG + rank) * (BM * BN) + ws_region;
 #pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
                     float v[32];
                     tmem_ld32(tb + c * 32, v);
 #pragma unroll
                     for (int e = 0; e < 32; e += 4)
-                        *reinterpret_cast<float4*>(dst + c * 32 + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+                        __stcg(reinterpret_cast<float4*>(dst + c * 32 + e), make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]));
                 }
                 tc_fence_before();
                 __threadfence();
                 __syncwarp();
+                int old = 0;
                 if (lane == 0) {
                     if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
                     else mbar_arrive_leader(&tempty[acc]);
-                    flag_release(P.flags + ((w.tail_idx * nparts + w.piece) * CG + rank) * FAST_EPI_WARPS + ew);
+                    int* cnt = P.flags + (w.tail_idx * CG + rank) * FAST_EPI_WARPS + ew;
+                    old = counter_arrive(cnt);
+                    if (old == split - 1) *cnt = 0;   // every arrival is in: reset for the next launch
                 }
+                old = __shfl_sync(0xffffffffu, old, 0);
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
-                continue;
-            }
-            const bool last_piece = w.piece >= 0;
-            if (last_piece) {
-                // wait for every earlier piece of this tile (this warp's 32 x 128 region), reset flags
-                if (lane == 0) {
-                    for (int pc = 0; pc < nparts; ++pc) {
-                        int* f = P.flags + ((w.tail_idx * nparts + pc) * CG + rank) * FAST_EPI_WARPS + ew;
-                        while (flag_acquire(f) == 0) { }
-                        *f = 0;
-                    }
-                }
-                __syncwarp();
+                if (old != split - 1) continue;
+                __threadfence();
+                if (FG::SIDE && lane == 0) side_issue(tm, tn, 0);
             }
             const int64_t row = (int64_t)m0 + lrow;
             const bool row_ok = row < M;
@@ -463,19 +466,33 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
 
             // CTA-scope wait: the accumulator is read through tcgen05.ld after the fence below;
             // a cluster-scope acquire would emit an L1 invalidate (CCTL.IVALL) on every poll.
-            mbar_wait(&tfull[acc], acc_phase);
-            tc_fence_after();
+            if (!piece) {
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+            }
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + h * 128);
 
 #pragma unroll 1
             for (int c = 0; c < 4; ++c) {
                 float v[32];
-                tmem_ld32(tbase + c * 32, v);
-                if (last_piece) {
-                    // fixed-order sum of the earlier K pieces (L2 loads, bypassing L1)
-                    for (int pc = 0; pc < nparts; ++pc) {
-                        const float* src = P.ws + ((int64_t)(w.tail_idx * nparts + pc) * CG + rank) * (BM * BN) +
-                                           (int64_t)(q * 32 + lane) * BN + h * 128 + c * 32;
+                if (!piece) {
+                    tmem_ld32(tbase + c * 32, v);
+                    if (c == 3) {
+                        // this warp's share of the accumulator is in registers: release it
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
+                            else mbar_arrive_leader(&tempty[acc]);
+                        }
+                    }
+                } else {
+                    // fixed-order sum of every K piece (L2 loads, bypassing L1)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] = 0.0f;
+                    for (int pc = 0; pc < split; ++pc) {
+                        const float* src = P.ws + ((int64_t)(w.tail_idx * split + pc) * CG + rank) * (BM * BN) +
+                                           ws_region + c * 32;
 #pragma unroll
                         for (int e = 0; e < 32; e += 4) {
                             const float4 u = __ldcg(reinterpret_cast<const float4*>(src + e));
@@ -484,15 +501,6 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                             v[e + 2] += u.z;
                             v[e + 3] += u.w;
                         }
-                    }
-                }
-                if (c == 3) {
-                    // this warp's share of the accumulator is in registers: release it
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) {
-                        if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
-                        else mbar_arrive_leader(&tempty[acc]);
                     }
                 }
                 // side operands of this chunk: wait for the TMA load, pull this thread's row
@@ -533,7 +541,7 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                             side_issue(tm, tn, c + 1);
                         } else if (i + nunits < mp.nitems) {
                             const Work wn = work_item(mp, i + nunits);
-                            if (item_runs_program(mp, wn)) side_issue(wn.tm, wn.tn, 0);
+                            if (item_prefetches_side(wn)) side_issue(wn.tm, wn.tn, 0);
                         }
                     }
                 }
@@ -545,6 +553,19 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     fload<float, 32>(P.acc_in + row * P.ld_acc, gcol0, N, row_ok, x);
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] += x[i];
+                }
+                if constexpr ((FL & F_ROWDOT) != 0) {
+                    // PartialRowDot(X) ahead of RowScale: sum(tile * X) of this row's piece
+                    float s = 0.0f;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) s += v[i] * sd0[i];
+                    const int pid = __ldg(P.rowpart_map + gcol0);
+                    if (pid != ppid) {
+                        if (ppid >= 0 && row_ok) P.rowpart[row * P.ld_rowpart + ppid] = pacc;
+                        ppid = pid;
+                        pacc = 0.0f;
+                    }
+                    pacc += s;
                 }
                 if (FL & F_ROWSCALE) {
 #pragma unroll
@@ -711,13 +732,16 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     else staged_store<TS, 32>(sg, &tma_main, gcol0, m0 + q * 32, v, lane);
                 }
             }
-            if ((FL & (F_SUMSQ | F_SWIGLU_BWD)) && ppid >= 0 && row_ok) P.rowpart[row * P.ld_rowpart + ppid] = pacc;
+            if ((FL & (F_SUMSQ | F_SWIGLU_BWD | F_ROWDOT)) && ppid >= 0 && row_ok)
+                P.rowpart[row * P.ld_rowpart + ppid] = pacc;
             if ((FL & F_LSE) && ppid >= 0 && row_ok) {
                 P.rowpart[row * P.ld_rowpart + 2 * ppid] = pmax;
                 P.rowpart[row * P.ld_rowpart + 2 * ppid + 1] = pacc;
             }
-            acc ^= 1;
-            if (acc == 0) acc_phase ^= 1;
+            if (!piece) {
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
         }
         if (lane == 0) bulk_wait<0>();
         __syncwarp();

@@ -400,7 +400,8 @@ def run_gemm(
     def enqueue(ta, tb, kk, program_on, mdesc, acc_t, odtype):
         ws = nat.workspace(dev)
         prob = nat.Problem(p.m, p.n, kk, int(p.trans_a), int(p.trans_b), scode, odtype,
-                           int(mdesc is not None), 0, ws.data_ptr(), ws.numel() * 4)
+                           int(mdesc is not None), nat.sm_limit(),
+                           ws.data_ptr() if ws is not None else None, ws.numel() * 4 if ws is not None else 0)
         acc_desc = nat.tensor_desc(acc_t) if acc_t is not None else None
         nat.call("coda_gemm_epilogue", ctypes.byref(prob), ctypes.byref(nat.tensor_desc(ta)),
                  ctypes.byref(nat.tensor_desc(tb)), step_arr, len(steps) if program_on else 0, op_descs,

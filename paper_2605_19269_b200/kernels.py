@@ -21,6 +21,7 @@ from . import traffic
 from .engine import GemmProblem, KernelResult, block_starts, run_gemm
 from .epilogue import (
     AuxTileStore,
+    PartialRowDot,
     EpilogueProgram,
     OnlineLse,
     PairwiseRope,
@@ -77,6 +78,11 @@ class PipelineConfig:
     # GQA extension (no reference counterpart): width of each of the k and v spans of the
     # packed projection.  None = hidden, the reference's packed (q, k, v) of width 3*hidden.
     kv_width: Optional[int] = None
+    # B200 extension (north_star "gamma folded into W"): the RMSNorm gains are folded into
+    # the consuming weights (W' = diag(gamma) W, formed once per weight update by
+    # fold_gains), so the producing K4 launches store only pre_norm; the backward recovers
+    # dW = diag(gamma) dW' and dgamma = rowsum(W * dW') in the weight-gradient epilogue.
+    fold_gamma: bool = False
 
     def __post_init__(self):
         if self.hidden <= 0:
@@ -199,8 +205,8 @@ def qkv_rope_tables(m: int, hidden: int, *, base: float = 10000.0, start: int = 
         # repeats it, the v span is the identity) -- the same bf16 values, 1/6 the bytes
         spec = RopeCompact(cos=c_h.tensor[:, 0::2].contiguous(), sin=s_h.tensor[:, 0::2].contiguous(),
                            hidden=hidden)
-        out[0]._rope = spec
-        out[1]._rope = spec
+        out[0]._rope = (spec, "cos")
+        out[1]._rope = (spec, "sin")
     return out[0], out[1]
 
 
@@ -217,10 +223,15 @@ class RopeCompact:
 
 
 def rope_compact_of(cos: DenseMatrix, sin: DenseMatrix) -> Optional[RopeCompact]:
-    """The compact form shared by a (cos, sin) pair built together by qkv_rope_tables."""
-    spec = getattr(cos, "_rope", None)
-    if spec is None or getattr(sin, "_rope", None) is not spec:
+    """The compact form shared by a (cos, sin) pair built together by qkv_rope_tables.
+
+    Each table carries its role; the compact path is taken only when `cos` is that
+    pair's cos table and `sin` its sin table (swapped or duplicated tables run the
+    full-table path, which reads exactly what was bound)."""
+    c, s = getattr(cos, "_rope", None), getattr(sin, "_rope", None)
+    if c is None or s is None or c[0] is not s[0] or c[1] != "cos" or s[1] != "sin":
         return None
+    spec = c[0]
     if cos.precision is not PrecisionMode.SIMBF16 or cos.rows != spec.cos.shape[0]:
         return None
     return spec
@@ -247,6 +258,64 @@ def split_gate_up(w: DenseMatrix) -> tuple[DenseMatrix, DenseMatrix]:
     g.copy_(w.tensor[:, 0::2])
     u.copy_(w.tensor[:, 1::2])
     return DenseMatrix._wrap(g, w.precision), DenseMatrix._wrap(u, w.precision)
+
+
+def scale_rows(w: DenseMatrix, gain: Vector) -> DenseMatrix:
+    """bf16(diag(gain) W): one HBM-bound launch (csrc coda_scale_rows)."""
+    import ctypes
+    import torch
+
+    if w.precision is not PrecisionMode.SIMBF16:
+        raise ConfigError("gain folding is implemented for the bf16 (SIMBF16) path")
+    if len(gain) != w.rows:
+        raise DimensionError(f"gain has length {len(gain)}, expected {w.rows}")
+    t = w.tensor
+    out = alloc_matrix(t.shape[0], t.shape[1], torch.bfloat16, t.device)
+    g = gain.tensor if gain.tensor.dtype == torch.float32 else gain.tensor.float()
+    nat.call("coda_scale_rows", ctypes.byref(nat.tensor_desc(t)), g.contiguous().data_ptr(),
+             ctypes.byref(nat.tensor_desc(out)), torch.cuda.current_stream(t.device).cuda_stream,
+             tag="fold_gain")
+    return DenseMatrix._wrap(out, w.precision)
+
+
+@dataclass(frozen=True)
+class FoldedGains:
+    """Gain-folded consumer weights: w_gate_up' = diag(gamma_ffn) w_gate_up and
+    w_qkv' = diag(gamma_qkv) w_qkv (bf16), valid for one set of weights."""
+
+    w_gate_up: DenseMatrix
+    w_qkv: DenseMatrix
+
+
+def fold_gains(weights: "LayerWeights") -> FoldedGains:
+    """Form the folded weights once per weight update (two HBM-bound launches)."""
+    return FoldedGains(w_gate_up=scale_rows(weights.w_gate_up, weights.gamma_ffn),
+                       w_qkv=scale_rows(weights.w_qkv, weights.gamma_qkv))
+
+
+_ones_cache: dict = {}
+
+
+def _ones(n: int, precision: PrecisionMode, device) -> Vector:
+    import torch
+
+    key = (n, precision, str(device))
+    v = _ones_cache.get(key)
+    if v is None:
+        v = _ones_cache[key] = Vector._wrap(torch.ones(n, dtype=precision.vector_torch_dtype, device=device),
+                                            precision)
+    return v
+
+
+def gemm_wgrad_gain(a, b, weight, gain, *, precision=PrecisionMode.EXACT64, tile_shape=TileShape(128, 128),
+                    reduction_tile_n=128, ledger=None, out_f32=False):
+    """Weight gradient of a gain-folded weight: with dW' = a^T b (trans_a), returns
+    main = diag(gain) dW' and aux "gain_dot" = per-row block partials of sum(W * dW'),
+    i.e. [PartialRowDot(W), RowScale(gain)] on the wgrad tile (both linear in dW', so
+    they commute with the data-parallel all-reduce)."""
+    return _launch(traffic.K_GEMM, a, b, [PartialRowDot("weight", "gain_dot"), RowScale("gain")],
+                   {"weight": weight, "gain": gain}, trans_a=True, tile_shape=tile_shape,
+                   reduction_tile_n=reduction_tile_n, precision=precision, ledger=ledger, out_f32=out_f32)
 
 
 # ---------------------------------------------------------------------------
@@ -508,9 +577,12 @@ class LayerTape:
     qkv: DenseMatrix
     cos: DenseMatrix
     sin: DenseMatrix
+    folded: Optional[FoldedGains] = None   # fold_gamma: the folded weights the forward used
 
     def check(self, config: PipelineConfig) -> None:
         m, d = self.x.shape
+        if config.fold_gamma and self.folded is None:
+            raise TapeError("fold_gamma backward needs the folded weights of its forward (tape.folded)")
         f, qw = config.ffn_resolved, config.qkv_width
         for name, got, want in (
             ("pre_norm_a", self.pre_norm_a.shape, (m, d)),
@@ -535,21 +607,37 @@ class LayerForwardResult:
 
 
 def layer_forward(x: DenseMatrix, z: DenseMatrix, weights: LayerWeights, cos: DenseMatrix, sin: DenseMatrix, *,
-                  config: PipelineConfig) -> LayerForwardResult:
-    """Six launches: K4 -> finalize -> K6 -> K4 -> finalize -> K7 (kernels.py:810-869)."""
+                  config: PipelineConfig, folded: Optional[FoldedGains] = None) -> LayerForwardResult:
+    """Six launches: K4 -> finalize -> K6 -> K4 -> finalize -> K7 (kernels.py:810-869).
+
+    With `config.fold_gamma` the K4 launches store only pre_norm (no gained copy) and K6/K7
+    read pre_norm against the folded weights; `folded` (from fold_gains) may be passed when
+    the weights did not change since it was formed, otherwise two fold launches run first."""
     weights.check(config)
     if x.shape != z.shape:
         raise DimensionError(f"x and z shapes differ: {x.shape} vs {z.shape}")
     ledger = TrafficLedger()
     kw = config.launch_kw(ledger)
-    k4a = gemm_residual_partial_rms(x, weights.w_out, z, weights.gamma_ffn, **kw)
-    ra = finalize_rms(k4a.aux["sumsq"], config.eps, ledger=ledger)
-    k6 = gemm_rms_swiglu(k4a.main, weights.w_gate_up, ra, **kw)
-    k4b = gemm_residual_partial_rms(k6.main, weights.w_down, k4a.aux["pre_norm"], weights.gamma_qkv, **kw)
-    rb = finalize_rms(k4b.aux["sumsq"], config.eps, ledger=ledger)
-    k7 = gemm_rms_rope(k4b.main, weights.w_qkv, rb, cos, sin, **kw)
+    if config.fold_gamma:
+        if folded is None:
+            folded = fold_gains(weights)
+        k4a = gemm_residual_partial_rms(x, weights.w_out, z, weights.gamma_ffn, gamma_folded=True, **kw)
+        ra = finalize_rms(k4a.aux["sumsq"], config.eps, ledger=ledger)
+        k6 = gemm_rms_swiglu(k4a.aux["pre_norm"], folded.w_gate_up, ra, **kw)
+        k4b = gemm_residual_partial_rms(k6.main, weights.w_down, k4a.aux["pre_norm"], weights.gamma_qkv,
+                                        gamma_folded=True, **kw)
+        rb = finalize_rms(k4b.aux["sumsq"], config.eps, ledger=ledger)
+        k7 = gemm_rms_rope(k4b.aux["pre_norm"], folded.w_qkv, rb, cos, sin, **kw)
+    else:
+        k4a = gemm_residual_partial_rms(x, weights.w_out, z, weights.gamma_ffn, **kw)
+        ra = finalize_rms(k4a.aux["sumsq"], config.eps, ledger=ledger)
+        k6 = gemm_rms_swiglu(k4a.main, weights.w_gate_up, ra, **kw)
+        k4b = gemm_residual_partial_rms(k6.main, weights.w_down, k4a.aux["pre_norm"], weights.gamma_qkv, **kw)
+        rb = finalize_rms(k4b.aux["sumsq"], config.eps, ledger=ledger)
+        k7 = gemm_rms_rope(k4b.main, weights.w_qkv, rb, cos, sin, **kw)
     tape = LayerTape(x=x, pre_norm_a=k4a.aux["pre_norm"], inv_rms_a=ra, preact=k6.aux["preact"],
-                     pre_norm_b=k4b.aux["pre_norm"], inv_rms_b=rb, qkv=k7.main, cos=cos, sin=sin)
+                     pre_norm_b=k4b.aux["pre_norm"], inv_rms_b=rb, qkv=k7.main, cos=cos, sin=sin,
+                     folded=folded if config.fold_gamma else None)
     return LayerForwardResult(qkv=k7.main, residual=k4b.aux["pre_norm"], tape=tape, ledger=ledger)
 
 
@@ -580,8 +668,9 @@ def layer_backward(grad_qkv: DenseMatrix, tape: LayerTape, weights: LayerWeights
     parallelism) receives each weight gradient as an unrounded float32
     tensor right after its GEMM is enqueued, in production order, and must
     leave the reduced sum in place; if the hook has a `wait()` (asynchronous
-    reduction on another stream) it is called before the single rounding to
-    storage at the end.
+    reduction on another stream) it is called before returning (and before the
+    single rounding to storage in SIMBF16), so the returned gradients are
+    always complete on the caller's stream.
     """
     weights.check(config)
     tape.check(config)
@@ -598,38 +687,69 @@ def layer_backward(grad_qkv: DenseMatrix, tape: LayerTape, weights: LayerWeights
             wgrad_hook(name, res.main.tensor)
         return res.main
 
+    fold = config.fold_gamma
+    ones = _ones(d, prec, grad_qkv.tensor.device) if fold else None
+
+    def wgrad_gain(name, gname, a, b, weight, gain):
+        # folded gain: dW = diag(gain) (a^T b) and dgain = rowsum(W * a^T b) in one epilogue
+        res = gemm_wgrad_gain(a, b, weight, gain, precision=prec, tile_shape=config.tile_shape,
+                              reduction_tile_n=config.reduction_tile_n, ledger=ledger, out_f32=f32)
+        g_gain = finalize_rowdot(res.aux["gain_dot"], 1, ledger=ledger)
+        if wgrad_hook is not None:
+            wgrad_hook(name, res.main.tensor)
+            wgrad_hook(gname, g_gain.tensor)
+        return res.main, g_gain
+
     grad_zb, rowdot_b = rope_backward_stat(grad_qkv, tape.qkv, tape.cos, tape.sin, tile_n=config.tile_n,
                                            reduction_tile_n=config.reduction_tile_n, precision=prec, ledger=ledger)
     s_b = finalize_rowdot(rowdot_b, d, ledger=ledger)
-    k9b = gemm_rmsnorm_backward(grad_zb, weights.w_qkv, tape.pre_norm_b, tape.inv_rms_b, weights.gamma_qkv, s_b,
-                                grad_in=grad_residual, trans_b=True, **kw)
-    grad_h1b = k9b.main
-    g_wqkv = wgrad("w_qkv", k9b.aux["normed"], grad_zb)
-    g_gqkv = reduce_row_partials(k9b.aux["gamma_grad"], ledger=ledger)
-    if wgrad_hook is not None:
-        wgrad_hook("gamma_qkv", g_gqkv.tensor)
+    if fold:
+        # K9 against W' = diag(gamma) W: its GEMM already yields D * gamma, so the local
+        # backward runs with unit gains and `normed` is the un-gained c_n = c * r
+        k9b = gemm_rmsnorm_backward(grad_zb, tape.folded.w_qkv, tape.pre_norm_b, tape.inv_rms_b, ones, s_b,
+                                    grad_in=grad_residual, trans_b=True, **kw)
+        grad_h1b = k9b.main
+        g_wqkv, g_gqkv = wgrad_gain("w_qkv", "gamma_qkv", k9b.aux["normed"], grad_zb, weights.w_qkv,
+                                    weights.gamma_qkv)
+    else:
+        k9b = gemm_rmsnorm_backward(grad_zb, weights.w_qkv, tape.pre_norm_b, tape.inv_rms_b, weights.gamma_qkv,
+                                    s_b, grad_in=grad_residual, trans_b=True, **kw)
+        grad_h1b = k9b.main
+        g_wqkv = wgrad("w_qkv", k9b.aux["normed"], grad_zb)
+        g_gqkv = reduce_row_partials(k9b.aux["gamma_grad"], ledger=ledger)
+        if wgrad_hook is not None:
+            wgrad_hook("gamma_qkv", g_gqkv.tensor)
 
     k10 = gemm_swiglu_backward(grad_h1b, weights.w_down, tape.preact, trans_b=True, **kw)
     grad_za = k10.main
     s_a = finalize_rowdot(k10.aux["rowdot"], d, ledger=ledger)
     g_wdown = wgrad("w_down", k10.aux["recompute"], grad_h1b)
 
-    k9a = gemm_rmsnorm_backward(grad_za, weights.w_gate_up, tape.pre_norm_a, tape.inv_rms_a, weights.gamma_ffn,
-                                s_a, grad_in=grad_h1b, trans_b=True, **kw)
-    grad_h1a = k9a.main
-    g_wgu = wgrad("w_gate_up", k9a.aux["normed"], grad_za)
-    g_gffn = reduce_row_partials(k9a.aux["gamma_grad"], ledger=ledger)
-    if wgrad_hook is not None:
-        wgrad_hook("gamma_ffn", g_gffn.tensor)
+    if fold:
+        k9a = gemm_rmsnorm_backward(grad_za, tape.folded.w_gate_up, tape.pre_norm_a, tape.inv_rms_a, ones, s_a,
+                                    grad_in=grad_h1b, trans_b=True, **kw)
+        grad_h1a = k9a.main
+        g_wgu, g_gffn = wgrad_gain("w_gate_up", "gamma_ffn", k9a.aux["normed"], grad_za, weights.w_gate_up,
+                                   weights.gamma_ffn)
+    else:
+        k9a = gemm_rmsnorm_backward(grad_za, weights.w_gate_up, tape.pre_norm_a, tape.inv_rms_a,
+                                    weights.gamma_ffn, s_a, grad_in=grad_h1b, trans_b=True, **kw)
+        grad_h1a = k9a.main
+        g_wgu = wgrad("w_gate_up", k9a.aux["normed"], grad_za)
+        g_gffn = reduce_row_partials(k9a.aux["gamma_grad"], ledger=ledger)
+        if wgrad_hook is not None:
+            wgrad_hook("gamma_ffn", g_gffn.tensor)
 
     grad_x = _launch(traffic.K_GEMM, grad_h1a, weights.w_out, [], {}, trans_b=True, **kw).main
     g_wout = wgrad("w_out", tape.x, grad_h1a)
 
-    if f32:
-        # the reduced sums must be complete before their single rounding to storage
+    if wgrad_hook is not None:
+        # join an asynchronous reduction before anything reads the reduced gradients (and,
+        # in SIMBF16, before their single rounding to storage) -- whatever the precision
         wait = getattr(wgrad_hook, "wait", None)
         if wait is not None:
             wait()
+    if f32:
         g_wqkv, g_wdown, g_wgu, g_wout = (to_storage(g, prec) for g in (g_wqkv, g_wdown, g_wgu, g_wout))
     return LayerGrads(x=grad_x, z=grad_h1a, w_out=g_wout, gamma_ffn=g_gffn, w_gate_up=g_wgu, w_down=g_wdown,
                       gamma_qkv=g_gqkv, w_qkv=g_wqkv, ledger=ledger)

@@ -223,8 +223,9 @@ def test_compact_rope_tables_bit_identical(cuda_ready):
     x, z = M(rng.standard_normal((m, d))), M(rng.standard_normal((m, d)))
     gq, gr = M(rng.standard_normal((m, 3 * d))), M(rng.standard_normal((m, d)))
     cos_c, sin_c = cd.qkv_rope_tables(m, d, start=7, precision=P)
-    assert cos_c._rope is not None and cos_c._rope is sin_c._rope
-    assert cos_c._rope.cos.shape == (m, d // 2)
+    assert cos_c._rope is not None and cos_c._rope[0] is sin_c._rope[0]
+    assert (cos_c._rope[1], sin_c._rope[1]) == ("cos", "sin")
+    assert cos_c._rope[0].cos.shape == (m, d // 2)
     # the same values without the compact form (full-table path)
     cos_f, sin_f = cd.DenseMatrix.from_tensor(cos_c.tensor, P), cd.DenseMatrix.from_tensor(sin_c.tensor, P)
     assert cos_f._rope is None
@@ -239,3 +240,26 @@ def test_compact_rope_tables_bit_identical(cuda_ready):
     # and the compact path agrees with the fused-order oracle
     of = O.layer_forward(x.data, z.data, {k: getattr(w, k).data for k in WKEYS}, cos_f.data, sin_f.data, O.SIMBF16)
     assert O.rel_error(outs[0][0], of["qkv"]) <= 2e-2
+
+
+def test_compact_rope_roles_respected(cuda_ready):
+    """Swapped (sin, cos) or duplicated (cos, cos) bindings of compact-capable tables must
+    compute exactly what was bound, like the generic path and the reference."""
+    cd = _cd()
+    P = cd.PrecisionMode.SIMBF16
+    m, d = 256, 256
+    rng = np.random.default_rng(5)
+    cos_c, sin_c = cd.qkv_rope_tables(m, d, precision=P)
+    assert cd.kernels.rope_compact_of(cos_c, sin_c) is not None
+    assert cd.kernels.rope_compact_of(sin_c, cos_c) is None
+    assert cd.kernels.rope_compact_of(cos_c, cos_c) is None
+    a = cd.DenseMatrix.from_array(rng.standard_normal((m, d)), P)
+    b = cd.DenseMatrix.from_array(rng.standard_normal((d, 3 * d)) * 0.1, P)
+    for c, s in ((sin_c, cos_c), (cos_c, cos_c)):
+        got = cd.gemm_rope(a, b, c, s, precision=P).main.data
+        want = O.k_rope(a.data, b.data, c.data, s.data, O.SIMBF16)["main"]
+        assert O.rel_error(got, want) <= 1e-5
+        gq = cd.DenseMatrix.from_array(rng.standard_normal((m, 3 * d)), P)
+        gz, _ = cd.rope_backward_stat(gq, gq, c, s, precision=P)
+        ogz, _ = O.rope_backward_stat(gq.data, gq.data, c.data, s.data, O.SIMBF16)
+        assert O.rel_error(gz.data, ogz) <= 1e-5

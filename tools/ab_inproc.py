@@ -17,6 +17,12 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 import torch  # noqa: E402
+import os  # noqa: E402
+
+os.environ.setdefault("CODA_LIB", "exp")   # measurement knobs live in the experiment build
+from paper_2605_19269_b200 import _build  # noqa: E402
+
+_build.build(experiments=True)
 
 import bench  # noqa: E402
 import paper_2605_19269_b200 as cd  # noqa: E402
