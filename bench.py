@@ -202,25 +202,31 @@ def make_workload(cd, d, inter, m, start, device, seed=0, blocks=1, fp32=False, 
     return weights, acts, cos, sin
 
 
-def run_step(cd, cfg, weights, acts, cos, sin, hook=None, before_backward=None):
+def run_step(cd, cfg, weights, acts, cos, sin, hook=None, before_backward=None, bwd_sms=0):
     """One fwd+bwd step: a single block, or a stack when `weights` is a list of blocks.
 
     `before_backward` (optional) runs after the forward is enqueued — the e2e loop
-    uses it to make the backward wait for its own inputs' host-to-device copy."""
+    uses it to make the backward wait for its own inputs' host-to-device copy.
+    `bwd_sms` > 0 caps the backward's GEMM launches at that many SMs, leaving the rest to
+    the weight-gradient all-reduce the hook runs on a side stream."""
+    from paper_2605_19269_b200 import _native
+
     if isinstance(weights, (list, tuple)):
         from paper_2605_19269_b200 import stack
 
         fwd = stack.stack_forward(acts["x"], acts["z"], weights, cos, sin, config=cfg)
         if before_backward is not None:
             before_backward()
-        grads = stack.stack_backward(acts["grad_qkv"], acts["grad_residual"], fwd, weights, config=cfg,
-                                     wgrad_hook=hook)
+        with _native.limit_sms(bwd_sms):
+            grads = stack.stack_backward(acts["grad_qkv"], acts["grad_residual"], fwd, weights, config=cfg,
+                                         wgrad_hook=hook)
         return fwd, grads[0]
     fwd = cd.layer_forward(acts["x"], acts["z"], weights, cos, sin, config=cfg)
     if before_backward is not None:
         before_backward()
-    bwd = cd.layer_backward(acts["grad_qkv"], fwd.tape, weights, grad_residual=acts["grad_residual"], config=cfg,
-                            wgrad_hook=hook)
+    with _native.limit_sms(bwd_sms):
+        bwd = cd.layer_backward(acts["grad_qkv"], fwd.tape, weights, grad_residual=acts["grad_residual"],
+                                config=cfg, wgrad_hook=hook)
     return fwd, bwd
 
 
@@ -279,6 +285,93 @@ class CpuOracle:
                 "sample_tokens": self.m}
 
 
+def upload_bf16(cd, a, dev):
+    import numpy as np
+    import torch
+
+    t = cd.tensors.alloc_matrix(a.shape[0], a.shape[1], torch.bfloat16, dev)
+    t.copy_(torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev))
+    return cd.DenseMatrix.from_tensor(t, cd.PrecisionMode.SIMBF16)
+
+
+def upload_vec(cd, a, dev):
+    import numpy as np
+    import torch
+
+    return cd.Vector.from_tensor(torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev),
+                                 cd.PrecisionMode.SIMBF16)
+
+
+class NullReduce:
+    """World-size-1 stand-in for the data-parallel hook: exercises the unrounded f32
+    weight-gradient outputs and their single rounding (kernels.layer_backward)."""
+
+    def __init__(self):
+        self.names = []
+
+    def __call__(self, name, tensor):
+        self.names.append(name)
+
+
+def fullsize_parity(name: str, variant: str = "plain") -> dict:
+    """Full-size parity of config `name` (c3 / c4) on cuda:0 against the committed oracle fixture
+    tests/golden/fullsize_<name>.npz (made by tests/golden/make_fullsize.py): the same bf16 inputs
+    are regenerated from the fixture's seed, the whole block runs through the public API, and every
+    output is compared by its sketch, norm and sampled rows (oracle/fullsize.compare).  The checker
+    only; nothing here is timed.  variant: plain | f32_hook | fold."""
+    import numpy as np
+    import torch
+
+    import paper_2605_19269_b200 as cd
+    from oracle import coda_oracle as O
+    from oracle import fullsize as FS
+
+    z = np.load(ROOT / "tests" / "golden" / f"fullsize_{name}.npz")
+    dev = torch.device("cuda", 0)
+    inp = FS.make_inputs(name, seed=int(z["meta_seed"]))
+    m, d = inp["x"].shape
+    P = cd.PrecisionMode.SIMBF16
+    w = cd.LayerWeights(w_out=upload_bf16(cd, inp["w_out"], dev), gamma_ffn=upload_vec(cd, inp["gamma_ffn"], dev),
+                        w_gate_up=upload_bf16(cd, inp["w_gate_up"], dev), w_down=upload_bf16(cd, inp["w_down"], dev),
+                        gamma_qkv=upload_vec(cd, inp["gamma_qkv"], dev), w_qkv=upload_bf16(cd, inp["w_qkv"], dev))
+    acts = {k: upload_bf16(cd, inp[k], dev) for k in ("x", "z", "grad_qkv", "grad_residual")}
+    del inp
+    cfg = cd.PipelineConfig(hidden=d, ffn=w.w_gate_up.cols, precision=P, fold_gamma=(variant == "fold"))
+    cos, sin = cd.qkv_rope_tables(m, d, precision=P)
+    hook = NullReduce() if variant == "f32_hook" else None
+    fwd = cd.layer_forward(acts["x"], acts["z"], w, cos, sin, config=cfg)
+    bwd = cd.layer_backward(acts["grad_qkv"], fwd.tape, w, grad_residual=acts["grad_residual"], config=cfg,
+                            wgrad_hook=hook)
+    torch.cuda.synchronize()
+    got = {"qkv": fwd.qkv, "residual": fwd.residual}
+    got.update({k: getattr(bwd, k) for k in O.GRAD_KEYS})
+    out = {}
+    for k in FS.OUTPUTS:
+        t = got[k].tensor
+        if k.startswith("gamma"):
+            out[k] = FS.compare(k, t.double().cpu().numpy(), {"full": z[f"{k}__full"]})
+            continue
+        fp = {"sketch": z[f"{k}__sketch"], "rows": z[f"{k}__rows"].astype(np.float64), "row_idx": z[f"{k}__row_idx"]}
+        S = torch.from_numpy(FS.sketch_matrix(k, t.shape[0])).to(dev, torch.float64)
+        gs = (S @ t.double()).cpu().numpy()
+        gr = t[torch.from_numpy(fp["row_idx"]).to(dev)].double().cpu().numpy()
+        out[k] = FS.compare(k, None, fp, got_sketch=gs, got_rows=gr)
+        gnorm = float(torch.linalg.vector_norm(t.double()))
+        out[k]["norm_ratio"] = gnorm / float(z[f"{k}__norm"])
+    return out
+
+
+def fullsize_summary(res: dict, tol: float = 2e-2) -> dict:
+    worst = max(res, key=lambda k: res[k]["rel"])
+    return {"rel_err_max": res[worst]["rel"], "worst_output": worst,
+            "max_abs_err": max(r["max_abs"] for r in res.values()),
+            "rows_rel_max": max(r.get("rows_rel", 0.0) for r in res.values()),
+            "tol": tol, "pass": all(r["rel"] <= tol and r.get("rows_rel", 0.0) <= tol for r in res.values()),
+            "outputs": len(res),
+            "vs": "token-chunked fused-order CPU oracle over the full block (tests/golden/fullsize_*.npz): "
+                  "sketch-estimated Frobenius rel error per output + exact sampled rows"}
+
+
 def cpu_oracle_tokens_per_s(d, inter, sample_tokens, seconds_budget=20.0, max_reps=5, fp32=False, kv=None):
     runner = CpuOracle(d, inter, sample_tokens, fp32=fp32, kv=kv)
     times = []
@@ -326,6 +419,58 @@ def reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def wgrad_shapes(d, inter, kv=None):
+    """The all-reduced gradients of one block in production order (kernels.py:936-1001)."""
+    q = d + 2 * (d if kv is None else kv)
+    return [("w_qkv", (d, q)), ("gamma_qkv", (d,)), ("w_down", (inter, d)), ("w_gate_up", (d, 2 * inter)),
+            ("gamma_ffn", (d,)), ("w_out", (d, d))]
+
+
+def launcher_check(args, rank, world):
+    """--launcher-check: gloo on CPU, no kernels.  Each step all-reduces zero-filled f32 buffers
+    with the block's gradient shapes through the same WgradAllReduce hook the GPU path uses."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_19269_b200 import parallel
+
+    dist.init_process_group("gloo")
+    d, inter, tokens, label = CONFIGS[args.config]
+    tokens = args.tokens or tokens
+    sh = parallel.shard(tokens, rank, world, args.scaling)
+    bufs = [torch.zeros(shape, dtype=torch.float32) for _, shape in wgrad_shapes(d, inter, KV.get(args.config))]
+    hook = parallel.WgradAllReduce(dist)
+
+    def step():
+        for (name, _), b in zip(wgrad_shapes(d, inter), bufs):
+            hook(name, b)
+        hook.wait()
+
+    for _ in range(args.warmup):
+        step()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dist.barrier()
+    ms = (time.perf_counter() - t0) * 1e3
+    t = torch.tensor([ms])
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    total = torch.tensor([sh.rows])
+    dist.all_reduce(total)
+    nbytes = sum(b.numel() * 4 for b in bufs)
+    if rank == 0:
+        print(json.dumps({
+            "metric": "block fwd+bwd tokens/s", "launcher_check": True, "value": None, "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": args.scaling, "backend": "gloo (CPU, no kernels)",
+            "config": {"workload": label, "tokens_per_rank": sh.rows, "global_tokens": int(total.item())},
+            "allreduce_bytes_per_step": nbytes, "names": hook.names[:len(bufs)],
+        }), flush=True)
+    dist.destroy_process_group()
+
+
 def coda_arm(args, rank, world, local_rank):
     import torch
 
@@ -338,6 +483,12 @@ def coda_arm(args, rank, world, local_rank):
     if world > 1 or args.force_dist:
         import torch.distributed as dist  # noqa: F811
 
+        comm = args.comm_sms if args.comm_sms is not None else (16 if world > 1 else 0)
+        if comm > 0:
+            # the all-reduce runs concurrently with the SM-capped backward GEMMs: keep NCCL
+            # inside the SMs left to it
+            os.environ.setdefault("NCCL_MAX_CTAS", str(comm))
+
         if world == 1:   # --force-dist: a 1-rank NCCL group, to exercise the collective path on one GPU
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29511")
@@ -347,21 +498,27 @@ def coda_arm(args, rank, world, local_rank):
     from paper_2605_19269_b200 import parallel
 
     d, inter, tokens, label = CONFIGS[args.config]
+    tokens = args.tokens or tokens
     sh = parallel.shard(tokens, rank, world, args.scaling)
     m = sh.rows
     P = cd.PrecisionMode.SIMBF16
     kv = KV.get(args.config)
-    cfg = cd.PipelineConfig(hidden=d, ffn=2 * inter, precision=P, kv_width=kv)
+    cfg = cd.PipelineConfig(hidden=d, ffn=2 * inter, precision=P, kv_width=kv, fold_gamma=args.fold_gamma)
     nblocks = BLOCKS.get(args.config, 1)
     fp32 = args.config in FP32
     if fp32:
+        if args.fold_gamma:
+            raise SystemExit("--fold-gamma is implemented for the bf16 path")
         P = cd.PrecisionMode.SIM32
         cfg = cd.PipelineConfig(hidden=d, ffn=2 * inter, precision=P)
     weights, acts, cos, sin = make_workload(cd, d, inter, m, sh.start, device, blocks=nblocks, fp32=fp32, kv=kv)
-    hook = parallel.WgradAllReduce(dist, device) if dist is not None else None
+    hook = parallel.WgradAllReduce(dist, device, f32=args.wgrad_dtype == "f32") if dist is not None else None
+    # SMs left to the side-stream all-reduce while the backward's persistent GEMMs run
+    comm_sms = args.comm_sms if args.comm_sms is not None else (16 if world > 1 else 0)
+    bwd_sms = (_native.num_sms() - comm_sms) if (dist is not None and comm_sms > 0) else 0
 
     def step():
-        out = run_step(cd, cfg, weights, acts, cos, sin, hook)
+        out = run_step(cd, cfg, weights, acts, cos, sin, hook, bwd_sms=bwd_sms)
         if hook is not None:
             hook.wait()
         return out
@@ -433,6 +590,33 @@ def coda_arm(args, rank, world, local_rank):
     ms_step = ms / args.steps
     value = world * m / (ms_step / 1e3)
 
+    # ---- the other reading of the config text: weak scaling (the config's tokens on EVERY rank),
+    # reported beside the strong-scaled headline for N > 1
+    weak = None
+    if world > 1 and args.scaling == "strong" and graph is None:
+        ww, wa, wc, wsn = make_workload(cd, d, inter, tokens, rank * tokens, device, blocks=nblocks, fp32=fp32,
+                                        kv=kv)
+
+        def weak_step():
+            run_step(cd, cfg, ww, wa, wc, wsn, hook, bwd_sms=bwd_sms)
+            if hook is not None:
+                hook.wait()
+
+        for _ in range(2):
+            weak_step()
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            weak_step()
+        e1.record(stream)
+        barrier()
+        t = torch.tensor([e0.elapsed_time(e1)], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wms = float(t.item()) / args.steps
+        weak = {"tokens_per_gpu": tokens, "global_tokens": world * tokens, "ms_per_step": wms,
+                "value": world * tokens / (wms / 1e3), "unit": "tokens/s"}
+        del ww, wa, wc, wsn
+
     # ---- e2e through the public API from pinned host buffers.  Every step copies its
     # inputs H2D and reads its results D2H inside the timed region; the copies run on
     # their own streams (double-buffered inputs) so they overlap the previous/next step.
@@ -496,7 +680,7 @@ def coda_arm(args, rank, world, local_rank):
             mark(marks, f"step{s} start", stream)
             a = {k: cd.DenseMatrix.from_tensor(dev_in[b][k], P) for k in dev_in[b]}
             _, bwd = run_step(cd, cfg, weights, a, cos, sin, hook,
-                              before_backward=lambda: stream.wait_event(copied_b[b]))
+                              before_backward=lambda: stream.wait_event(copied_b[b]), bwd_sms=bwd_sms)
             if hook is not None:
                 hook.wait()
             consumed[b].record(stream)
@@ -561,6 +745,12 @@ def coda_arm(args, rank, world, local_rank):
                          f"{'SIM32' if fp32 else 'SIMBF16'} oracle, "
                          f"best of {reps} ({secs:.2f} s each)"}
 
+    fullsize = None
+    if rank == 0 and world == 1 and not args.no_parity and args.tokens is None and \
+            (ROOT / "tests" / "golden" / f"fullsize_{args.config}.npz").exists():
+        # the measured configuration itself, every output, against the pinned oracle (not timed)
+        fullsize = fullsize_summary(fullsize_parity(args.config, "fold" if args.fold_gamma else "plain"))
+
     if rank == 0:
         line = {
             "metric": "block fwd+bwd tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world,
@@ -584,6 +774,11 @@ def coda_arm(args, rank, world, local_rank):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "parity": parity,
+            "parity_fullsize": fullsize,
+            "weak_scaling": weak,
+            "comm_sms": comm_sms if dist is not None else 0,
+            "wgrad_allreduce_dtype": args.wgrad_dtype if dist is not None else None,
+            "fold_gamma": bool(args.fold_gamma),
             "launch_breakdown_ms": {k: round(v["avg_ms"], 4) for k, v in (prof or {}).items()},
         }
         print(json.dumps(line), flush=True)
@@ -591,30 +786,82 @@ def coda_arm(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
-def main():
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn(args, argv) -> int:
+    """`--gpus N` without a torchrun environment: launch N ranks of this script through
+    torch.distributed.run (one process per GPU, 127.0.0.1 rendezvous) and return its exit
+    code.  Fails loudly when fewer than N CUDA devices are visible (unless --launcher-check,
+    which runs the launch / rendezvous / all-reduce / max-over-ranks machinery on CPU)."""
+    if not args.launcher_check:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) are visible",
+                  file=sys.stderr, flush=True)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", str(Path(__file__).resolve()), *argv]
+    return subprocess.call(cmd, cwd=str(ROOT))
+
+
+def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("coda", "reference"), default="coda")
     ap.add_argument("--config", choices=tuple(CONFIGS), default="c4")
-    ap.add_argument("--scaling", choices=("strong", "weak"), default="weak")
+    ap.add_argument("--scaling", choices=("strong", "weak"), default=None,
+                    help="multi-GPU token sharding (default: strong for the 16384-token C4/C3 jobs, weak for "
+                         "the per-GPU C5 stack)")
+    ap.add_argument("--tokens", type=int, default=None,
+                    help="override the config's token count (per-rank shape proxies at N=1)")
+    ap.add_argument("--fold-gamma", action="store_true", help="gains folded into W (north_star variant)")
+    ap.add_argument("--comm-sms", type=int, default=None,
+                    help="SMs left to the NCCL all-reduce during the backward (default 16 when N > 1)")
+    ap.add_argument("--wgrad-dtype", choices=("f32", "bf16"), default="f32",
+                    help="dtype of the data-parallel weight-gradient all-reduce (f32: single rounding, "
+                         "the reference's; bf16 halves the bytes)")
     ap.add_argument("--cpu-sample", type=int, default=256)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the full-size oracle parity check (c3/c4)")
     ap.add_argument("--ncu", action="store_true", help="profiling pass only (no timing / JSON line)")
     ap.add_argument("--graph", action="store_true", help="replay the step as one captured CUDA graph")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the NCCL wgrad all-reduce path even at world size 1 (collective overlap check)")
-    args = ap.parse_args()
+    ap.add_argument("--launcher-check", action="store_true",
+                    help="CPU/gloo check of the multi-rank launch: rendezvous, the per-step weight-gradient "
+                         "all-reduce of this config's shapes, max-over-ranks timing and the rank-0 JSON line "
+                         "(no kernels; not a measurement)")
+    args = ap.parse_args(argv)
     args.warmup = max(3, args.warmup)
+    if args.scaling is None:
+        args.scaling = "weak" if args.config == "c5" else "strong"
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args, argv)
     rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.gpus == 1 else 1))
+    world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
-    if args.impl == "reference":
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr, flush=True)
+        return 2
+    if args.launcher_check:
+        launcher_check(args, rank, world)
+    elif args.impl == "reference":
         reference_arm(args, rank, world)
     else:
         coda_arm(args, rank, world, local_rank)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

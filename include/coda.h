@@ -61,9 +61,10 @@ extern "C" {
 #define CODA_OP_SWIGLU_BWD      12   /* PairwiseSwigluBackward epilogue.py:469 */
 #define CODA_OP_RMSNORM_BWD     13   /* RmsNormBackwardLocal   epilogue.py:522 */
 
-#define CODA_MAX_STEPS     8
-#define CODA_MAX_OPERANDS  8
-#define CODA_MAX_STORES    8
+#define CODA_MAX_STEPS       16
+#define CODA_MAX_OPERANDS    16
+#define CODA_MAX_STORES      16
+#define CODA_MAX_ROW_STREAMS  4   /* row-directed partial streams (sum / row-dot / LSE) per program */
 
 /* A dense 1-D/2-D device tensor.  1-D tensors use rows = 1, cols = length. */
 typedef struct {
@@ -105,24 +106,28 @@ typedef struct {
  *   ROW_SCALE      arg0 = operand (col vector)
  *   RESIDUAL_ADD   arg0 = operand (tile)
  *   AUX_TILE_STORE arg0 = store (tile)
- *   PARTIAL_SUMSQ  arg0 = store (row-sum pieces)
- *   PARTIAL_ROWDOT arg0 = operand (tile), arg1 = store (row-sum pieces)
+ *   PARTIAL_SUMSQ  arg0 = store (row-sum pieces), arg6 = row stream
+ *   PARTIAL_ROWDOT arg0 = operand (tile), arg1 = store (row-sum pieces), arg6 = row stream
  *   PARTIAL_COLSUM arg0 = store (col-sum pieces)
- *   ONLINE_LSE     arg0 = store (row-pair pieces)
+ *   ONLINE_LSE     arg0 = store (row-pair pieces), arg6 = row stream
  *   TARGET_GATHER  arg0 = operand (labels, int64), arg1 = store (gather, f32)
  *   ROPE           arg0 = cos operand, arg1 = sin operand, arg2 = backward flag,
  *                  arg3/arg4 = 1 + slot of compact (m, h/2) bf16 cos/sin tables or 0,
  *                  arg5 = h (q-span width; columns >= 2h are the identity)
  *   SWIGLU         —
  *   SWIGLU_BWD     arg0 = preact operand (factor 2), arg1 = recompute store,
- *                  arg2 = row-sum pieces store (factor 2)
+ *                  arg2 = row-sum pieces store (factor 2), arg6 = row stream
  *   RMSNORM_BWD    arg0 = pre, arg1 = inv_rms, arg2 = gamma, arg3 = stat,
  *                  arg4 = accumulate operand or -1, arg5 = normed store,
  *                  arg6 = gamma-grad col-sum pieces store
- * width: running width factor at step entry, encoded x2 (1 = 1/2, 2 = 1, 4 = 2). */
+ * Row streams (0 .. CODA_MAX_ROW_STREAMS-1) number the program's row-directed
+ * partial emitters in order; each carries its own running block sum per row.
+ * width: running width at step entry in values per 32 accumulator columns, i.e.
+ * 32 x the reference's running width factor (epilogue.py:626-660): 64 (factor 2),
+ * 32 (1), 16 (1/2) ... 1 (1/32).  Pairwise steps need width >= 2. */
 typedef struct {
     int32_t op;
-    int32_t width2;
+    int32_t width;
     int32_t arg[7];
     int32_t _pad;
 } coda_step_t;

@@ -38,9 +38,10 @@ OP_RMSNORM_BWD = 13
 
 STORE_TILE, STORE_ROW_SUM, STORE_ROW_PAIR, STORE_COL_SUM, STORE_GATHER = 0, 1, 2, 3, 4
 
-MAX_STEPS = 8
-MAX_OPERANDS = 8
-MAX_STORES = 8
+MAX_STEPS = 16
+MAX_OPERANDS = 16
+MAX_STORES = 16
+MAX_ROW_STREAMS = 4
 
 # GPU tile geometry of the persistent kernel (csrc/coda_gemm.cuh)
 GPU_TILE_M = 128
@@ -97,7 +98,7 @@ class Problem(ctypes.Structure):
 class Step(ctypes.Structure):
     _fields_ = [
         ("op", ctypes.c_int32),
-        ("width2", ctypes.c_int32),
+        ("width", ctypes.c_int32),
         ("arg", ctypes.c_int32 * 7),
         ("_pad", ctypes.c_int32),
     ]
@@ -295,6 +296,11 @@ def prepare_stream_workspace(device, stream) -> None:
     with torch.cuda.stream(stream):
         workspace(device)
     torch.cuda.synchronize(device)
+
+
+def num_sms() -> int:
+    """SM count of the current device as the library sees it (0 without a device)."""
+    return int(load().coda_num_sms())
 
 
 def launch_count() -> int:

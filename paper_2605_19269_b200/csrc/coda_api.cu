@@ -388,7 +388,7 @@ int match_fast(const coda_problem_t* pr, const coda_step_t* steps, int nsteps, c
     };
     for (int s = 0; s < nsteps; ++s) {
         const coda_step_t& st = steps[s];
-        if (st.width2 != 2) return -1;   // every fast op runs at factor 1
+        if (st.width != 32) return -1;   // every fast op runs at factor 1
         switch (st.op) {
         case CODA_OP_PARTIAL_ROWDOT:
             if (!rank_ok(1) || !stores[st.arg[1]].aligned) return -1;
@@ -520,22 +520,23 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         const coda_step_t& cs = steps[s];
         coda::DevStep& d = P.steps[s];
         d.op = cs.op;
-        d.w = cs.width2 * 16;
+        d.w = cs.width;
         for (int i = 0; i < 7; ++i) d.a[i] = cs.arg[i];
         if (d.w != w) return fail(CODA_E_PROGRAM, "step %d: width %d does not match running width %d", s, d.w, w);
         auto opnd_ok = [&](int i) { return i >= 0 && i < noperands; };
+        auto stream_ok = [&](int i) { return i >= 0 && i < coda::MAX_ROW_STREAMS; };
         auto store_ok = [&](int i) { return i >= 0 && i < nstores; };
         bool ok = true;
         switch (cs.op) {
         case CODA_OP_ROW_VEC_MUL: case CODA_OP_ROW_SCALE: case CODA_OP_RESIDUAL_ADD: ok = opnd_ok(cs.arg[0]); break;
         case CODA_OP_AUX_TILE_STORE: case CODA_OP_PARTIAL_COLSUM: ok = store_ok(cs.arg[0]); break;
         case CODA_OP_PARTIAL_SUMSQ: case CODA_OP_ONLINE_LSE:
-            ok = store_ok(cs.arg[0]) && w == 32 && (cs.arg[6] == 0 || cs.arg[6] == 1); break;
+            ok = store_ok(cs.arg[0]) && w == 32 && stream_ok(cs.arg[6]); break;
         case CODA_OP_PARTIAL_ROWDOT:
-            ok = opnd_ok(cs.arg[0]) && store_ok(cs.arg[1]) && w == 32 && (cs.arg[6] == 0 || cs.arg[6] == 1); break;
+            ok = opnd_ok(cs.arg[0]) && store_ok(cs.arg[1]) && w == 32 && stream_ok(cs.arg[6]); break;
         case CODA_OP_TARGET_GATHER: ok = opnd_ok(cs.arg[0]) && store_ok(cs.arg[1]) && w == 32; break;
         case CODA_OP_ROPE:
-            ok = opnd_ok(cs.arg[0]) && opnd_ok(cs.arg[1]);
+            ok = opnd_ok(cs.arg[0]) && opnd_ok(cs.arg[1]) && w >= 2;
             if (ok && cs.arg[3] > 0) {   // compact tables: arg3/arg4 = 1 + operand slot, arg5 = q-span width h
                 const int h = cs.arg[5];
                 ok = opnd_ok(cs.arg[3] - 1) && opnd_ok(cs.arg[4] - 1) && h > 0 && h % 32 == 0 && 2 * (int64_t)h <= N;
@@ -547,11 +548,11 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
             }
             break;
         case CODA_OP_SWIGLU:
-            if (w == 16) return fail(CODA_E_CONFIG, "GPU epilogue supports running width factors 1/2, 1, 2");
+            if (w < 2) return fail(CODA_E_CONFIG, "GPU epilogue supports running width factors 1/32 .. 2");
             w /= 2; break;
         case CODA_OP_SWIGLU_BWD:
             ok = opnd_ok(cs.arg[0]) && store_ok(cs.arg[1]) && store_ok(cs.arg[2]) && w == 32 &&
-                 (cs.arg[6] == 0 || cs.arg[6] == 1);
+                 stream_ok(cs.arg[6]);
             w = 64; break;
         case CODA_OP_RMSNORM_BWD:
             ok = opnd_ok(cs.arg[0]) && opnd_ok(cs.arg[1]) && opnd_ok(cs.arg[2]) && opnd_ok(cs.arg[3]) &&
@@ -644,7 +645,7 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
             const int64_t tile_bytes = (int64_t)cg * coda::BM * coda::BN * 4;
             // every piece dumps its partial tile; one arrival counter per (tail tile, rank, warp)
             while (sp >= 2 && (int64_t)r * sp * tile_bytes > pr->workspace_bytes - (64 << 10)) --sp;
-            if ((int64_t)r * cg * coda::FAST_EPI_WARPS * 4 > (64 << 10)) sp = 0;
+            if ((int64_t)r * cg * 4 > (64 << 10)) sp = 0;   // one arrival counter per (tail tile, rank)
             if (sp >= 2) {
                 F.mp.full_tiles = ntiles - r;
                 F.mp.tail = r;

@@ -413,11 +413,12 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             const int tm = w.tm, tn = w.tn;
             const int m0 = tm * G::TILE_M + rank * BM;
             const int n0 = tn * BN;
-            // a K piece of a split tail tile: dump the raw f32 accumulator of this warp's
-            // 32 x 128 region, then arrive on the region's counter.  The last of the
-            // `split` arrivals sums every dumped piece in fixed piece order and runs the
-            // program; the others are done.  No piece ever waits for another, so the
-            // launch needs no co-residency of its clusters.
+            // a K piece of a split tail tile: every epilogue warp dumps the raw f32 accumulator
+            // of its 32 x 128 region; then the CTA arrives once on the (tail tile, rank) counter.
+            // The last of the `split` arrivals sums every dumped piece in fixed piece order and
+            // runs the program; the others are done.  No piece ever waits for another, so the
+            // launch needs no co-residency of its clusters.  The decision is per CTA (not per
+            // warp) because the program's column reductions synchronise the warps of a half.
             const bool piece = w.piece >= 0;
             const int64_t ws_region = (int64_t)(q * 32 + lane) * BN + h * 128;
             if (piece) {
@@ -436,18 +437,21 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 tc_fence_before();
                 __threadfence();
                 __syncwarp();
-                int old = 0;
                 if (lane == 0) {
                     if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
                     else mbar_arrive_leader(&tempty[acc]);
-                    int* cnt = P.flags + (w.tail_idx * CG + rank) * FAST_EPI_WARPS + ew;
-                    old = counter_arrive(cnt);
-                    if (old == split - 1) *cnt = 0;   // every arrival is in: reset for the next launch
                 }
-                old = __shfl_sync(0xffffffffu, old, 0);
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
-                if (old != split - 1) continue;
+                named_bar_sync(4, 32 * FAST_EPI_WARPS);          // every region of this CTA is dumped
+                if (ew == 0 && lane == 0) {
+                    int* cnt = P.flags + w.tail_idx * CG + rank;
+                    const int old = counter_arrive(cnt);
+                    if (old == split - 1) *cnt = 0;               // every arrival is in: reset
+                    tmem_slot[1] = old == split - 1 ? 1u : 0u;
+                }
+                named_bar_sync(4, 32 * FAST_EPI_WARPS);
+                if (tmem_slot[1] == 0u) continue;
                 __threadfence();
                 if (FG::SIDE && lane == 0) side_issue(tm, tn, 0);
             }

@@ -30,8 +30,9 @@ constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;   // producer, mma, 4 epilogue 
 constexpr int CHUNK = 32;                    // accumulator columns per tcgen05.ld
 constexpr int RED_LD = 33;                   // padded row stride of the col-sum scratch
 
-constexpr int MAX_STEPS = 8;
-constexpr int MAX_SLOTS = 8;
+constexpr int MAX_STEPS = 16;
+constexpr int MAX_SLOTS = 16;
+constexpr int MAX_ROW_STREAMS = 4;           // row-directed partial streams per program
 
 enum OpCode : int {
     OP_ROW_VEC_MUL = 1, OP_ROW_SCALE = 2, OP_RESIDUAL_ADD = 3, OP_AUX_TILE_STORE = 4,
@@ -41,7 +42,7 @@ enum OpCode : int {
 
 struct DevStep {
     int op;
-    int w;          // running width in values per chunk at step entry (16, 32, 64)
+    int w;          // running width in values per 32-column chunk at step entry (1, 2, 4, ..., 64)
     int a[7];
 };
 struct DevOperand {
@@ -114,18 +115,24 @@ template <> struct Io<float> {
     __device__ static __forceinline__ void store1(float* p, float x) { p[0] = x; }
 };
 
-// Load W values of one row segment [c0, c0+W) (columns >= ncols read as 0).
+// Load W values of one row segment [c0, c0+W) (columns >= ncols read as 0).  Segments
+// narrower than one 16-byte vector (running width factors below 1/4) go element-wise.
 template <typename TS, int W>
 __device__ __forceinline__ void load_seg(const TS* rowp, int64_t c0, int64_t ncols, float* d) {
     constexpr int V = Io<TS>::V;
+    if constexpr (W < V) {
 #pragma unroll
-    for (int i = 0; i < W; i += V) {
-        if (c0 + i + V <= ncols) {
-            Io<TS>::load(rowp + c0 + i, d + i);
-        } else {
+        for (int e = 0; e < W; ++e) d[e] = (c0 + e < ncols) ? Io<TS>::load1(rowp + c0 + e) : 0.0f;
+    } else {
 #pragma unroll
-            for (int e = 0; e < V; ++e)
-                d[i + e] = (c0 + i + e < ncols) ? Io<TS>::load1(rowp + c0 + i + e) : 0.0f;
+        for (int i = 0; i < W; i += V) {
+            if (c0 + i + V <= ncols) {
+                Io<TS>::load(rowp + c0 + i, d + i);
+            } else {
+#pragma unroll
+                for (int e = 0; e < V; ++e)
+                    d[i + e] = (c0 + i + e < ncols) ? Io<TS>::load1(rowp + c0 + i + e) : 0.0f;
+            }
         }
     }
 }
@@ -133,29 +140,56 @@ __device__ __forceinline__ void load_seg(const TS* rowp, int64_t c0, int64_t nco
 template <typename TS, int W>
 __device__ __forceinline__ void store_seg(TS* rowp, int64_t c0, int64_t ncols, const float* s) {
     constexpr int V = Io<TS>::V;
+    if constexpr (W < V) {
 #pragma unroll
-    for (int i = 0; i < W; i += V) {
-        if (c0 + i + V <= ncols) {
-            Io<TS>::store(rowp + c0 + i, s + i);
-        } else {
+        for (int e = 0; e < W; ++e)
+            if (c0 + e < ncols) Io<TS>::store1(rowp + c0 + e, s[e]);
+    } else {
 #pragma unroll
-            for (int e = 0; e < V; ++e)
-                if (c0 + i + e < ncols) Io<TS>::store1(rowp + c0 + i + e, s[i + e]);
+        for (int i = 0; i < W; i += V) {
+            if (c0 + i + V <= ncols) {
+                Io<TS>::store(rowp + c0 + i, s + i);
+            } else {
+#pragma unroll
+                for (int e = 0; e < V; ++e)
+                    if (c0 + i + e < ncols) Io<TS>::store1(rowp + c0 + i + e, s[i + e]);
+            }
         }
     }
 }
 // Broadcast f32 vector segment (row vector operand, same for all rows).
 template <int W>
 __device__ __forceinline__ void load_vec_seg(const float* vp, int64_t c0, int64_t n, float* d) {
+    if constexpr (W < 4) {
 #pragma unroll
-    for (int i = 0; i < W; i += 4) {
-        if (c0 + i + 4 <= n) {
-            const float4 u = __ldg(reinterpret_cast<const float4*>(vp + c0 + i));
-            d[i] = u.x; d[i + 1] = u.y; d[i + 2] = u.z; d[i + 3] = u.w;
-        } else {
+        for (int e = 0; e < W; ++e) d[e] = (c0 + e < n) ? __ldg(vp + c0 + e) : 0.0f;
+    } else {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) d[i + e] = (c0 + i + e < n) ? __ldg(vp + c0 + i + e) : 0.0f;
+        for (int i = 0; i < W; i += 4) {
+            if (c0 + i + 4 <= n) {
+                const float4 u = __ldg(reinterpret_cast<const float4*>(vp + c0 + i));
+                d[i] = u.x; d[i + 1] = u.y; d[i + 2] = u.z; d[i + 3] = u.w;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) d[i + e] = (c0 + i + e < n) ? __ldg(vp + c0 + i + e) : 0.0f;
+            }
         }
+    }
+}
+
+// Run f(Width<W>{}) for the running width w (values per 32-column chunk), so each op body
+// is compiled once per width with static register indexing.
+template <int W> struct Width { static constexpr int value = W; };
+template <typename F>
+__device__ __forceinline__ void with_width(int w, F&& f) {
+    switch (w) {
+    case 1: f(Width<1>{}); break;
+    case 2: f(Width<2>{}); break;
+    case 4: f(Width<4>{}); break;
+    case 8: f(Width<8>{}); break;
+    case 16: f(Width<16>{}); break;
+    case 32: f(Width<32>{}); break;
+    default: f(Width<64>{}); break;
     }
 }
 
@@ -345,7 +379,9 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
             const bool row_ok = row < P.M;
             const int64_t rem_chunks = ((int64_t)P.N - n0 + CHUNK - 1) / CHUNK;
             const int nchunks = rem_chunks < BN / CHUNK ? (int)rem_chunks : BN / CHUNK;
-            RowPart rp0{0.f, -INFINITY, -1}, rp1{0.f, -INFINITY, -1};
+            RowPart rp[MAX_ROW_STREAMS];
+#pragma unroll
+            for (int i = 0; i < MAX_ROW_STREAMS; ++i) rp[i] = RowPart{0.f, -INFINITY, -1};
 
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
@@ -378,14 +414,13 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
                     case OP_ROW_VEC_MUL: {
                         const DevOperand& o = P.opnd[st.a[0]];
                         const float* vp = static_cast<const float*>(o.ptr);
-#define CODA_ROWVEC(WW)                                                              \
-    {                                                                                \
-        float g[WW];                                                                 \
-        load_vec_seg<WW>(vp, gcol0 * WW / CHUNK, o.cols, g);                         \
-        _Pragma("unroll") for (int i = 0; i < WW; ++i) v[i] *= g[i];                 \
-    }
-                        if (w == 16) CODA_ROWVEC(16) else if (w == 32) CODA_ROWVEC(32) else CODA_ROWVEC(64)
-#undef CODA_ROWVEC
+                        with_width(w, [&](auto wc) {
+                            constexpr int W = decltype(wc)::value;
+                            float g[W];
+                            load_vec_seg<W>(vp, gcol0 * W / CHUNK, o.cols, g);
+#pragma unroll
+                            for (int i = 0; i < W; ++i) v[i] *= g[i];
+                        });
                         break;
                     }
                     case OP_ROW_SCALE: {
@@ -398,25 +433,25 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
                     case OP_RESIDUAL_ADD: {
                         const DevOperand& o = P.opnd[st.a[0]];
                         if (row_ok) {
-                            const TS* rp = static_cast<const TS*>(o.ptr) + row * o.ld;
-#define CODA_RES(WW)                                                                 \
-    {                                                                                \
-        float x[WW];                                                                 \
-        load_seg<TS, WW>(rp, gcol0 * WW / CHUNK, o.cols, x);                         \
-        _Pragma("unroll") for (int i = 0; i < WW; ++i) v[i] += x[i];                 \
-    }
-                            if (w == 16) CODA_RES(16) else if (w == 32) CODA_RES(32) else CODA_RES(64)
-#undef CODA_RES
+                            const TS* rp_ = static_cast<const TS*>(o.ptr) + row * o.ld;
+                            with_width(w, [&](auto wc) {
+                                constexpr int W = decltype(wc)::value;
+                                float x[W];
+                                load_seg<TS, W>(rp_, gcol0 * W / CHUNK, o.cols, x);
+#pragma unroll
+                                for (int i = 0; i < W; ++i) v[i] += x[i];
+                            });
                         }
                         break;
                     }
                     case OP_AUX_TILE_STORE: {
                         const DevStore& o = P.store[st.a[0]];
                         if (row_ok) {
-                            TS* rp = static_cast<TS*>(o.ptr) + row * o.ld;
-                            if (w == 16) store_seg<TS, 16>(rp, gcol0 / 2, o.cols, v);
-                            else if (w == 32) store_seg<TS, 32>(rp, gcol0, o.cols, v);
-                            else store_seg<TS, 64>(rp, gcol0 * 2, o.cols, v);
+                            TS* rp_ = static_cast<TS*>(o.ptr) + row * o.ld;
+                            with_width(w, [&](auto wc) {
+                                constexpr int W = decltype(wc)::value;
+                                store_seg<TS, W>(rp_, gcol0 * W / CHUNK, o.cols, v);
+                            });
                         }
                         break;
                     }
@@ -425,8 +460,7 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
 #pragma unroll
                         for (int i = 0; i < 32; ++i) x[i] = v[i] * v[i];
                         const DevStore& o = P.store[st.a[0]];
-                        if (st.a[6] == 0) rowsum_accum<32>(o, rp0, row, row_ok, gcol0, P.N, x);
-                        else rowsum_accum<32>(o, rp1, row, row_ok, gcol0, P.N, x);
+                        rowsum_accum<32>(o, rp[st.a[6]], row, row_ok, gcol0, P.N, x);
                         break;
                     }
                     case OP_PARTIAL_ROWDOT: {
@@ -440,8 +474,7 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
 #pragma unroll
                         for (int i = 0; i < 32; ++i) x[i] *= v[i];
                         const DevStore& o = P.store[st.a[1]];
-                        if (st.a[6] == 0) rowsum_accum<32>(o, rp0, row, row_ok, gcol0, P.N, x);
-                        else rowsum_accum<32>(o, rp1, row, row_ok, gcol0, P.N, x);
+                        rowsum_accum<32>(o, rp[st.a[6]], row, row_ok, gcol0, P.N, x);
                         break;
                     }
                     case OP_PARTIAL_COLSUM: {
@@ -450,8 +483,7 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
                     }
                     case OP_ONLINE_LSE: {
                         const DevStore& o = P.store[st.a[0]];
-                        if (st.a[6] == 0) rowlse_accum<32>(o, rp0, row, row_ok, gcol0, P.N, v);
-                        else rowlse_accum<32>(o, rp1, row, row_ok, gcol0, P.N, v);
+                        rowlse_accum<32>(o, rp[st.a[6]], row, row_ok, gcol0, P.N, v);
                         break;
                     }
                     case OP_TARGET_GATHER: {
@@ -475,24 +507,26 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
                         if (row_ok) {
                             const TS* cp = static_cast<const TS*>(oc.ptr) + row * oc.ld;
                             const TS* sp = static_cast<const TS*>(os.ptr) + row * os.ld;
-#define CODA_ROPE(WW)                                                                \
-    {                                                                                \
-        float cs[WW], sn[WW];                                                        \
-        load_seg<TS, WW>(cp, gcol0 * WW / CHUNK, oc.cols, cs);                       \
-        load_seg<TS, WW>(sp, gcol0 * WW / CHUNK, os.cols, sn);                       \
-        _Pragma("unroll") for (int k = 0; k < WW / 2; ++k) {                         \
-            const float x0 = v[2 * k], x1 = v[2 * k + 1];                            \
-            const float se = sgn * sn[2 * k], so = sgn * sn[2 * k + 1];              \
-            v[2 * k] = x0 * cs[2 * k] - x1 * se;                                     \
-            v[2 * k + 1] = x0 * so + x1 * cs[2 * k + 1];                             \
-        }                                                                            \
-    }
-                            if (w == 16) CODA_ROPE(16) else if (w == 32) CODA_ROPE(32) else CODA_ROPE(64)
-#undef CODA_ROPE
+                            with_width(w, [&](auto wc) {
+                                constexpr int W = decltype(wc)::value;
+                                if constexpr (W >= 2) {
+                                    float cs[W], sn[W];
+                                    load_seg<TS, W>(cp, gcol0 * W / CHUNK, oc.cols, cs);
+                                    load_seg<TS, W>(sp, gcol0 * W / CHUNK, os.cols, sn);
+#pragma unroll
+                                    for (int k = 0; k < W / 2; ++k) {
+                                        const float x0 = v[2 * k], x1 = v[2 * k + 1];
+                                        const float se = sgn * sn[2 * k], so = sgn * sn[2 * k + 1];
+                                        v[2 * k] = x0 * cs[2 * k] - x1 * se;
+                                        v[2 * k + 1] = x0 * so + x1 * cs[2 * k + 1];
+                                    }
+                                }
+                            });
                         }
                         break;
                     }
                     case OP_SWIGLU: {
+                        // pairs (2k, 2k+1) -> k; w >= 2 (validated on the host)
 #pragma unroll
                         for (int k = 0; k < 32; ++k) {
                             if (2 * k < w) {
@@ -530,8 +564,7 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
                         const DevStore& orc = P.store[st.a[1]];
                         if (row_ok) store_seg<TS, 32>(static_cast<TS*>(orc.ptr) + row * orc.ld, gcol0, orc.cols, rec);
                         const DevStore& opd = P.store[st.a[2]];
-                        if (st.a[6] == 0) rowsum_accum<64>(opd, rp0, row, row_ok, gcol0 * 2, (int64_t)P.N * 2, z);
-                        else rowsum_accum<64>(opd, rp1, row, row_ok, gcol0 * 2, (int64_t)P.N * 2, z);
+                        rowsum_accum<64>(opd, rp[st.a[6]], row, row_ok, gcol0 * 2, (int64_t)P.N * 2, z);
                         w = 64;
                         break;
                     }
@@ -576,18 +609,15 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
                 }
                 if (P.store_main && row_ok) {
                     const int64_t ncols = (int64_t)P.N * w / CHUNK;
-                    const int64_t c0 = gcol0 * w / CHUNK;
-                    if (P.out_f32) {
-                        float* rp = static_cast<float*>(P.out) + row * P.ld_out;
-                        if (w == 16) store_seg<float, 16>(rp, c0, ncols, v);
-                        else if (w == 32) store_seg<float, 32>(rp, c0, ncols, v);
-                        else store_seg<float, 64>(rp, c0, ncols, v);
-                    } else {
-                        __nv_bfloat16* rp = static_cast<__nv_bfloat16*>(P.out) + row * P.ld_out;
-                        if (w == 16) store_seg<__nv_bfloat16, 16>(rp, c0, ncols, v);
-                        else if (w == 32) store_seg<__nv_bfloat16, 32>(rp, c0, ncols, v);
-                        else store_seg<__nv_bfloat16, 64>(rp, c0, ncols, v);
-                    }
+                    with_width(w, [&](auto wc) {
+                        constexpr int W = decltype(wc)::value;
+                        const int64_t c0 = gcol0 * W / CHUNK;
+                        if (P.out_f32)
+                            store_seg<float, W>(static_cast<float*>(P.out) + row * P.ld_out, c0, ncols, v);
+                        else
+                            store_seg<__nv_bfloat16, W>(static_cast<__nv_bfloat16*>(P.out) + row * P.ld_out, c0,
+                                                        ncols, v);
+                    });
                 }
             }
             // flush the row-directed partials of this tile (pieces end at tile edges)
@@ -599,8 +629,7 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
                 else if (st.op == OP_PARTIAL_ROWDOT) { si = st.a[6]; slot = st.a[1]; }
                 else if (st.op == OP_ONLINE_LSE) { si = st.a[6]; slot = st.a[0]; pair = true; }
                 else if (st.op == OP_SWIGLU_BWD) { si = st.a[6]; slot = st.a[2]; }
-                if (si == 0) rowpart_flush(P.store[slot], rp0, row, row_ok, pair);
-                else if (si == 1) rowpart_flush(P.store[slot], rp1, row, row_ok, pair);
+                if (si >= 0 && si < MAX_ROW_STREAMS) rowpart_flush(P.store[slot], rp[si], row, row_ok, pair);
             }
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;

@@ -330,7 +330,7 @@ def run_gemm(
     if prec is PrecisionMode.SIMBF16:
         from .kernels import rope_compact_of
 
-        for si, (op, w2, args) in enumerate(steps):
+        for si, (op, wd, args) in enumerate(steps):
             if op != nat.OP_ROPE or len(onames) + 2 > nat.MAX_OPERANDS:
                 continue
             spec = rope_compact_of(bindings[onames[args[0]]], bindings[onames[args[1]]])
@@ -342,7 +342,7 @@ def run_gemm(
             grown[nops], grown[nops + 1] = nat.tensor_desc(spec.cos), nat.tensor_desc(spec.sin)
             keep.extend((spec.cos, spec.sin))
             op_descs = grown
-            steps[si] = (op, w2, list(args[:3]) + [nops + 1, nops + 2, spec.hidden, 0])
+            steps[si] = (op, wd, list(args[:3]) + [nops + 1, nops + 2, spec.hidden, 0])
             nops += 2
 
     # ---- stores
@@ -394,8 +394,8 @@ def run_gemm(
         main_desc = nat.tensor_desc(main_t)
         write_bytes += p.m * n_out * prec.storage_bytes
     step_arr = (nat.Step * max(1, len(steps)))()
-    for i, (op, w2, args) in enumerate(steps):
-        step_arr[i] = nat.Step(op, w2, (ctypes.c_int32 * 7)(*args), 0)
+    for i, (op, wd, args) in enumerate(steps):
+        step_arr[i] = nat.Step(op, wd, (ctypes.c_int32 * 7)(*args), 0)
 
     def enqueue(ta, tb, kk, program_on, mdesc, acc_t, odtype):
         ws = nat.workspace(dev)

@@ -678,7 +678,7 @@ def layer_backward(grad_qkv: DenseMatrix, tape: LayerTape, weights: LayerWeights
     ledger = TrafficLedger()
     kw = config.launch_kw(ledger)
     prec = config.precision
-    f32 = wgrad_hook is not None and prec is PrecisionMode.SIMBF16
+    f32 = wgrad_hook is not None and prec is PrecisionMode.SIMBF16 and getattr(wgrad_hook, "f32", True)
 
     def wgrad(name, a, b):
         res = _launch(traffic.K_GEMM, a, b, [], {}, trans_a=True, tile_shape=config.tile_shape,

@@ -59,8 +59,12 @@ class WgradAllReduce:
     tensors (gloo, tests) it is a plain synchronous all_reduce.
     """
 
-    def __init__(self, dist, device=None):
+    def __init__(self, dist, device=None, f32: bool = True):
         self.dist = dist
+        # f32: layer_backward hands over unrounded float32 weight gradients and rounds the
+        # reduced sums once (the reference's single rounding); False: bf16 gradients are
+        # reduced as stored (half the bytes on the wire, one rounding per partial)
+        self.f32 = f32
         self.side = None
         if device is not None and getattr(device, "type", None) == "cuda":
             import torch

@@ -8,8 +8,10 @@ import numpy as np
 GOLDEN = Path(__file__).resolve().parent / "golden"
 
 
-def load_programs(mode: str):
-    z = np.load(GOLDEN / f"programs_{mode}.npz")
+def load_programs(mode: str, kind: str = "programs"):
+    """kind: "programs" (random compositions, make_programs.py) or "programs_ext" (widened device
+    program space: >2 row streams, factors down to 1/32, > 8 steps/operands/stores)."""
+    z = np.load(GOLDEN / f"{kind}_{mode}.npz")
     specs = json.loads(bytes(z["specs"]).decode())
     return z, specs
 

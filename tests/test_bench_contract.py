@@ -39,3 +39,40 @@ def test_strong_and_weak_sharding_cover_the_job(world):
     assert all(a.stop == b.start for a, b in zip(strong, strong[1:]))
     weak = [parallel.shard(tokens, r, world, "weak") for r in range(world)]
     assert all(s.rows == tokens for s in weak) and weak[-1].stop == world * tokens
+
+
+def _run_bench(*args, timeout=240):
+    import subprocess
+
+    root = Path(__file__).resolve().parents[1]
+    return subprocess.run([sys.executable, str(root / "bench.py"), *args], capture_output=True, text=True,
+                          timeout=timeout, cwd=str(root))
+
+
+def test_launcher_spawns_ranks_gloo():
+    """`bench.py --gpus 2` without a torchrun environment launches 2 ranks itself (gloo on CPU
+    here): one JSON line from rank 0 with n_gpus 2, strong sharding of the config's tokens, and
+    the block's weight gradients all-reduced in production order (VERDICT r01 next #2)."""
+    import json
+
+    p = _run_bench("--gpus", "2", "--launcher-check", "--config", "c1", "--steps", "2", "--warmup", "3")
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    out = json.loads(lines[0])
+    assert out["n_gpus"] == 2 and out["launcher_check"] is True
+    assert out["scaling"] == "strong"
+    assert out["config"]["global_tokens"] == 128 and out["config"]["tokens_per_rank"] == 64
+    assert out["names"] == ["w_qkv", "gamma_qkv", "w_down", "w_gate_up", "gamma_ffn", "w_out"]
+    d, inter = 256, 1024
+    assert out["allreduce_bytes_per_step"] == 4 * (d * 3 * d + d + inter * d + d * 2 * inter + d + d * d)
+
+
+def test_launcher_fails_loudly_without_enough_gpus():
+    import torch
+
+    if torch.cuda.device_count() >= 8:
+        pytest.skip("enough GPUs for --gpus 8")
+    p = _run_bench("--gpus", "8", "--steps", "2", "--warmup", "3", timeout=120)
+    assert p.returncode == 2
+    assert "CUDA device" in p.stderr

@@ -19,6 +19,7 @@ Tolerance: bf16 path <= 2e-2 relative (north star), max abs error reported.
 
 from __future__ import annotations
 
+import sys
 import time
 from pathlib import Path
 
@@ -27,6 +28,8 @@ import pytest
 
 from oracle import coda_oracle as O
 from oracle import fullsize as FS
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 pytestmark = pytest.mark.gpu
 
@@ -40,72 +43,10 @@ def _cd():
     return cd
 
 
-def _upload(a: np.ndarray, dev):
-    import torch
-
-    cd = _cd()
-    t = cd.tensors.alloc_matrix(a.shape[0], a.shape[1], torch.bfloat16, dev)
-    t.copy_(torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev))
-    return cd.DenseMatrix.from_tensor(t, cd.PrecisionMode.SIMBF16)
-
-
-def _vec(a: np.ndarray, dev):
-    import torch
-
-    cd = _cd()
-    return cd.Vector.from_tensor(torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev),
-                                 cd.PrecisionMode.SIMBF16)
-
-
-class _NullReduce:
-    """World-size-1 stand-in for the data-parallel hook: exercises the unrounded f32
-    weight-gradient outputs and their single rounding (kernels.layer_backward)."""
-
-    def __init__(self):
-        self.names = []
-
-    def __call__(self, name, tensor):
-        self.names.append(name)
-
-
 def run_fullsize(name: str, variant: str = "plain") -> dict:
-    """Run config `name` on cuda:0 with the fixture's inputs; returns {output: compare dict}."""
-    import torch
+    import bench
 
-    cd = _cd()
-    z = np.load(GOLDEN / f"fullsize_{name}.npz")
-    dev = torch.device("cuda", 0)
-    inp = FS.make_inputs(name, seed=int(z["meta_seed"]))
-    m, d = inp["x"].shape
-    P = cd.PrecisionMode.SIMBF16
-    w = cd.LayerWeights(w_out=_upload(inp["w_out"], dev), gamma_ffn=_vec(inp["gamma_ffn"], dev),
-                        w_gate_up=_upload(inp["w_gate_up"], dev), w_down=_upload(inp["w_down"], dev),
-                        gamma_qkv=_vec(inp["gamma_qkv"], dev), w_qkv=_upload(inp["w_qkv"], dev))
-    acts = {k: _upload(inp[k], dev) for k in ("x", "z", "grad_qkv", "grad_residual")}
-    del inp
-    cfg = cd.PipelineConfig(hidden=d, ffn=w.w_gate_up.cols, precision=P, fold_gamma=(variant == "fold"))
-    cos, sin = cd.qkv_rope_tables(m, d, precision=P)
-    hook = _NullReduce() if variant == "f32_hook" else None
-    fwd = cd.layer_forward(acts["x"], acts["z"], w, cos, sin, config=cfg)
-    bwd = cd.layer_backward(acts["grad_qkv"], fwd.tape, w, grad_residual=acts["grad_residual"], config=cfg,
-                            wgrad_hook=hook)
-    torch.cuda.synchronize()
-    got = {"qkv": fwd.qkv, "residual": fwd.residual}
-    got.update({k: getattr(bwd, k) for k in O.GRAD_KEYS})
-    out = {}
-    for k in FS.OUTPUTS:
-        t = got[k].tensor
-        if k.startswith("gamma"):
-            out[k] = FS.compare(k, t.double().cpu().numpy(), {"full": z[f"{k}__full"]})
-            continue
-        fp = {"sketch": z[f"{k}__sketch"], "rows": z[f"{k}__rows"].astype(np.float64), "row_idx": z[f"{k}__row_idx"]}
-        S = torch.from_numpy(FS.sketch_matrix(k, t.shape[0])).to(dev, torch.float64)
-        gs = (S @ t.double()).cpu().numpy()
-        gr = t[torch.from_numpy(fp["row_idx"]).to(dev)].double().cpu().numpy()
-        out[k] = FS.compare(k, None, fp, got_sketch=gs, got_rows=gr)
-        gnorm = float(torch.linalg.vector_norm(t.double()))
-        out[k]["norm_ratio"] = gnorm / float(z[f"{k}__norm"])
-    return out
+    return bench.fullsize_parity(name, variant)
 
 
 def _check(res: dict, label: str):
@@ -139,6 +80,18 @@ def test_fullsize_c4_folded_gamma_vs_oracle(cuda_ready):
 
 
 # ----------------------------------------------------------------------------- C2 sweep
+
+
+def _upload(a, dev):
+    import bench
+
+    return bench.upload_bf16(_cd(), a, dev)
+
+
+def _vec(a, dev):
+    import bench
+
+    return bench.upload_vec(_cd(), a, dev)
 
 
 def _c2_operands(seed=0, n=4096):

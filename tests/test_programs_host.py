@@ -10,10 +10,11 @@ import paper_2605_19269_b200 as cd
 from programs_common import build_program, load_programs
 
 
+@pytest.mark.parametrize("kind", ["programs", "programs_ext"])
 @pytest.mark.parametrize("mode", ["simbf16", "sim32"])
-def test_reference_programs_lower(mode):
-    z, specs = load_programs(mode)
-    assert len(specs) >= 16
+def test_reference_programs_lower(mode, kind):
+    z, specs = load_programs(mode, kind)
+    assert len(specs) >= (16 if kind == "programs" else 8)
     for i, sp in enumerate(specs):
         prog = build_program(cd, sp["steps"])
         steps, onames, snames = prog.lower()
