@@ -389,7 +389,7 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             fence_proxy_async_smem();
             if ((FL & F_ROPE) && rope_h > 0) {
                 // one angle per pair: 16 columns (32 B) of each compact table
-                const int pc = (x % rope_h) / 2;
+                const int pc = (x % (rope_h > 0 ? rope_h : 1)) / 2;
                 mbar_arrive_expect_tx(&sidebar[ew], 2048);
                 tma_load_2d(sbase, &tma_s0, pc, y, &sidebar[ew]);
                 tma_load_2d(sbase + 2048, &tma_s1, pc, y, &sidebar[ew]);
@@ -696,8 +696,15 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         tmp[i] = cp[i] * g[i];   // normed
                     }
                     staged_store<TS, 32>(sg, &tma_aux, gcol0, m0 + q * 32, tmp, lane);
+                    // one pass: the gamma-grad terms D * c_n, and the output (D g - c_n s) r (+ grad_in)
+                    // in place -- c_n, g and grad_in die element by element, so the column sum below
+                    // runs with only its 32 inputs and the 32 outputs live (no spills at 168 regs)
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) tmp[i] = v[i] * cp[i];
+                    for (int i = 0; i < 32; ++i) {
+                        tmp[i] = v[i] * cp[i];
+                        v[i] = (v[i] * g[i] - cp[i] * ss) * rr;
+                        if constexpr ((FL & F_RMSBWD_ACC) != 0) v[i] += sd1[i];
+                    }
                     const float csum = warp_colsum32(tmp, lane);
                     float* red = colred + ((h * 2 + cbuf) * 4) * 32;
                     red[q * 32 + lane] = csum;
@@ -724,12 +731,6 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         }
                     }
                     cbuf ^= 1;
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] = (v[i] * g[i] - cp[i] * ss) * rr;
-                    if constexpr ((FL & F_RMSBWD_ACC) != 0) {
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) v[i] += sd1[i];
-                    }
                     if (FL & F_STORE_MAIN) staged_store<TS, 32>(sg, &tma_main, gcol0, m0 + q * 32, v, lane);
                 } else if (FL & F_STORE_MAIN) {
                     if (FL & F_OUT_F32) staged_store<float, 32>(sg, &tma_main, gcol0, m0 + q * 32, v, lane);

@@ -139,7 +139,7 @@ def test_wgrad_gain_epilogue_vs_oracle(cuda_ready):
     res = cd.gemm_wgrad_gain(a, b, w, gain, precision=P)
     dgain = cd.finalize_rowdot(res.aux["gain_dot"], 1)
     t = O.gemm(a.data, b.data, O.SIMBF16, trans_a=True)
-    assert O.rel_error(res.main.data, O.q(t * gain.data[:, None], O.SIMBF16)) <= 1e-5
+    assert O.rel_error(res.main.data, O.q(t * gain.data[:, None], O.SIMBF16)) <= 1e-3   # bf16 1-ulp flips
     assert O.rel_error(dgain.data, (t.astype(np.float64) * w.data).sum(axis=1)) <= 1e-5
 
 
