@@ -64,7 +64,9 @@ extern "C" {
 #define CODA_MAX_STEPS       16
 #define CODA_MAX_OPERANDS    16
 #define CODA_MAX_STORES      16
-#define CODA_MAX_ROW_STREAMS  4   /* row-directed partial streams (sum / row-dot / LSE) per program */
+#define CODA_MAX_ROW_STREAMS  4
+#define CODA_FIN_RMS          1   /* coda_step_t.fin_kind: finalize_rms    reductions.py:64-80 */
+#define CODA_FIN_ROWDOT       2   /*                       finalize_rowdot reductions.py:83-98 */   /* row-directed partial streams (sum / row-dot / LSE) per program */
 
 /* A dense 1-D/2-D device tensor.  1-D tensors use rows = 1, cols = length. */
 typedef struct {
@@ -129,6 +131,17 @@ typedef struct {
     int32_t op;
     int32_t width;
     int32_t arg[7];
+    /* Deferred finalizer (B200 extension; values identical to the standalone launch):
+     * fin_src = 1 + operand slot of an f32 (m, nb) partial-block matrix, or 0.  When set,
+     * the step's column-vector operand (ROW_SCALE: arg0, RMSNORM_BWD: the stat, arg3) is
+     * computed inside this launch from those partials -- fin_kind 1: finalize_rms
+     * r = 1/sqrt(sum_b p / fin_d + fin_eps) (reductions.py:64-80), 2: finalize_rowdot
+     * s = sum_b p / fin_d (reductions.py:83-98), same f32 op order -- and written back to
+     * that operand's vector by the launch, so the separate finalize launch disappears. */
+    int32_t fin_src;
+    int32_t fin_kind;
+    int32_t fin_d;
+    float   fin_eps;
     int32_t _pad;
 } coda_step_t;
 

@@ -36,6 +36,8 @@ OP_SWIGLU = 11
 OP_SWIGLU_BWD = 12
 OP_RMSNORM_BWD = 13
 
+FIN_RMS, FIN_ROWDOT = 1, 2   # deferred finalizer kinds (coda_step_t.fin_kind)
+
 STORE_TILE, STORE_ROW_SUM, STORE_ROW_PAIR, STORE_COL_SUM, STORE_GATHER = 0, 1, 2, 3, 4
 
 MAX_STEPS = 16
@@ -100,6 +102,10 @@ class Step(ctypes.Structure):
         ("op", ctypes.c_int32),
         ("width", ctypes.c_int32),
         ("arg", ctypes.c_int32 * 7),
+        ("fin_src", ctypes.c_int32),
+        ("fin_kind", ctypes.c_int32),
+        ("fin_d", ctypes.c_int32),
+        ("fin_eps", ctypes.c_float),
         ("_pad", ctypes.c_int32),
     ]
 

@@ -515,6 +515,7 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
     P.out_f32 = pr->out_dtype == CODA_F32 ? 1 : 0;
 
     const int sdt = pr->storage;
+    bool fin_source[CODA_MAX_OPERANDS] = {};
     int w = 32;
     for (int s = 0; s < nsteps; ++s) {
         const coda_step_t& cs = steps[s];
@@ -522,6 +523,23 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         d.op = cs.op;
         d.w = cs.width;
         for (int i = 0; i < 7; ++i) d.a[i] = cs.arg[i];
+        d.fin_src = cs.fin_src;
+        d.fin_kind = cs.fin_kind;
+        d.fin_d = cs.fin_d;
+        d.fin_eps = cs.fin_eps;
+        if (cs.fin_src != 0) {
+            const int fs = cs.fin_src - 1;
+            if (cs.op != CODA_OP_ROW_SCALE && cs.op != CODA_OP_RMSNORM_BWD)
+                return fail(CODA_E_PROGRAM, "step %d: deferred finalizers apply to RowScale / RmsNormBackwardLocal", s);
+            if (fs < 0 || fs >= noperands) return fail(CODA_E_PROGRAM, "step %d: bad finalizer source slot", s);
+            const coda_tensor_t& t = operands[fs];
+            if (t.dtype != CODA_F32 || t.rows != M || t.cols <= 0 || !t.ptr)
+                return fail(CODA_E_BINDING, "step %d: finalizer source must be f32 (m, nb) partials", s);
+            if (cs.fin_kind != CODA_FIN_RMS && cs.fin_kind != CODA_FIN_ROWDOT)
+                return fail(CODA_E_PROGRAM, "step %d: unknown finalizer kind %d", s, cs.fin_kind);
+            if (cs.fin_d <= 0) return fail(CODA_E_DEGENERATE, "step %d: finalizer width must be positive", s);
+            fin_source[fs] = true;
+        }
         if (d.w != w) return fail(CODA_E_PROGRAM, "step %d: width %d does not match running width %d", s, d.w, w);
         auto opnd_ok = [&](int i) { return i >= 0 && i < noperands; };
         auto stream_ok = [&](int i) { return i >= 0 && i < coda::MAX_ROW_STREAMS; };
@@ -566,7 +584,7 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
     for (int i = 0; i < noperands; ++i) {
         const coda_tensor_t& t = operands[i];
         if (!t.ptr) return fail(CODA_E_BINDING, "operand %d is null", i);
-        if (t.rows > 1 && t.dtype == sdt) {
+        if (t.rows > 1 && t.dtype == sdt && !fin_source[i]) {
             char nm[32];
             snprintf(nm, sizeof(nm), "operand %d", i);
             if ((rc = check_tensor2d(&t, nm, sdt))) return rc;
@@ -667,7 +685,14 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
             const coda_step_t& cs = steps[s];
             const coda::DevOperand* o = P.opnd;
             switch (cs.op) {
-            case CODA_OP_ROW_SCALE: F.rowscale = (const float*)o[cs.arg[0]].ptr; break;
+            case CODA_OP_ROW_SCALE:
+                F.rowscale = (const float*)o[cs.arg[0]].ptr;
+                if (cs.fin_src) {
+                    const coda::DevOperand& fp = o[cs.fin_src - 1];
+                    F.rs_fin = (const float*)fp.ptr; F.ld_rs_fin = fp.ld; F.rs_fin_nb = (int)fp.cols;
+                    F.rs_fin_kind = cs.fin_kind; F.rs_fin_d = (float)cs.fin_d; F.rs_fin_eps = cs.fin_eps;
+                }
+                break;
             case CODA_OP_PARTIAL_ROWDOT:
                 F.rowdot_x = o[cs.arg[0]].ptr; F.ld_rowdot_x = o[cs.arg[0]].ld;
                 F.rowpart = (float*)P.store[cs.arg[1]].ptr; F.ld_rowpart = P.store[cs.arg[1]].ld;
@@ -704,6 +729,11 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
                 F.inv_rms = (const float*)o[cs.arg[1]].ptr;
                 F.gamma = (const float*)o[cs.arg[2]].ptr;
                 F.stat = (const float*)o[cs.arg[3]].ptr;
+                if (cs.fin_src) {
+                    const coda::DevOperand& fp = o[cs.fin_src - 1];
+                    F.st_fin = (const float*)fp.ptr; F.ld_st_fin = fp.ld; F.st_fin_nb = (int)fp.cols;
+                    F.st_fin_kind = cs.fin_kind; F.st_fin_d = (float)cs.fin_d; F.st_fin_eps = cs.fin_eps;
+                }
                 if (cs.arg[4] >= 0) { F.grad_in = o[cs.arg[4]].ptr; F.ld_gin = o[cs.arg[4]].ld; }
                 aux_slot = cs.arg[5];
                 F.colpart = (float*)P.store[cs.arg[6]].ptr; F.ld_colpart = P.store[cs.arg[6]].ld;

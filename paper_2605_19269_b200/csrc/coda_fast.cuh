@@ -89,6 +89,16 @@ struct FastParams {
     float* ws;
     int* flags;
     int ablate;   // measurement-only ablations (results invalid): 1 = no side loads, 2 = no TMA stores
+    // deferred finalizers (coda_step_t.fin_*): the RowScale vector / the RMSNorm-backward
+    // stat computed per row from (M, nb) f32 partials and written back by the tn == 0 tiles
+    const float* rs_fin;
+    int64_t ld_rs_fin;
+    int rs_fin_nb, rs_fin_kind;
+    float rs_fin_d, rs_fin_eps;
+    const float* st_fin;
+    int64_t ld_st_fin;
+    int st_fin_nb, st_fin_kind;
+    float st_fin_d, st_fin_eps;
     // compact RoPE tables (F_ROPE): 0 = full (M, N) cos/sin tables.  h > 0: tma_s0/s1 map
     // (M, h/2) tables of one angle per pair; columns [0, 2h) rotate by pair (col mod h)/2
     // (the q and k spans of the packed projection share angles), columns >= 2h are the
@@ -458,10 +468,24 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             const int64_t row = (int64_t)m0 + lrow;
             const bool row_ok = row < M;
             float rsc = 1.0f, rr = 0.0f, ss = 0.0f;
-            if ((FL & F_ROWSCALE) && row_ok) rsc = __ldg(P.rowscale + row);
+            if ((FL & F_ROWSCALE) && row_ok) {
+                if (P.rs_fin != nullptr) {
+                    rsc = finalize_row(P.rs_fin + row * P.ld_rs_fin, P.rs_fin_nb, P.rs_fin_kind, P.rs_fin_d,
+                                       P.rs_fin_eps);
+                    if (tn == 0 && h == 0) const_cast<float*>(P.rowscale)[row] = rsc;
+                } else {
+                    rsc = __ldg(P.rowscale + row);
+                }
+            }
             if ((FL & F_RMSBWD) && row_ok) {
                 rr = __ldg(P.inv_rms + row);
-                ss = __ldg(P.stat + row);
+                if (P.st_fin != nullptr) {
+                    ss = finalize_row(P.st_fin + row * P.ld_st_fin, P.st_fin_nb, P.st_fin_kind, P.st_fin_d,
+                                      P.st_fin_eps);
+                    if (tn == 0 && h == 0) const_cast<float*>(P.stat)[row] = ss;
+                } else {
+                    ss = __ldg(P.stat + row);
+                }
             }
             float pacc = 0.0f, pmax = -INFINITY;
             int ppid = -1;

@@ -44,7 +44,20 @@ struct DevStep {
     int op;
     int w;          // running width in values per 32-column chunk at step entry (1, 2, 4, ..., 64)
     int a[7];
+    int fin_src;    // deferred finalizer: 1 + operand slot of the (m, nb) f32 partials, or 0
+    int fin_kind;   // 1 finalize_rms, 2 finalize_rowdot
+    int fin_d;
+    float fin_eps;
 };
+
+// The finalizers of reductions.py:64-98 for one row, in their f32 op order (ascending
+// block sum, IEEE-rounded div / sqrt): bit-identical to coda_finalize_rms / _rowdot.
+__device__ __forceinline__ float finalize_row(const float* __restrict__ p, int nb, int kind, float d, float eps) {
+    float t = 0.0f;
+#pragma unroll 8
+    for (int b = 0; b < nb; ++b) t = __fadd_rn(t, __ldg(p + b));
+    return kind == 1 ? __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(t, d), eps))) : __fdiv_rn(t, d);
+}
 struct DevOperand {
     const void* ptr;
     int64_t ld;
@@ -425,7 +438,17 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
                     }
                     case OP_ROW_SCALE: {
                         const float* vp = static_cast<const float*>(P.opnd[st.a[0]].ptr);
-                        const float r = row_ok ? __ldg(vp + row) : 0.0f;
+                        float r = 0.0f;
+                        if (row_ok) {
+                            if (st.fin_src) {
+                                const DevOperand& fp = P.opnd[st.fin_src - 1];
+                                r = finalize_row(static_cast<const float*>(fp.ptr) + row * fp.ld, (int)fp.cols,
+                                                 st.fin_kind, (float)st.fin_d, st.fin_eps);
+                                if (n0 == 0 && j == 0) const_cast<float*>(vp)[row] = r;
+                            } else {
+                                r = __ldg(vp + row);
+                            }
+                        }
 #pragma unroll
                         for (int i = 0; i < 64; ++i) v[i] *= r;
                         break;
@@ -575,7 +598,15 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
                         if (row_ok) {
                             load_seg<TS, 32>(static_cast<const TS*>(op_pre.ptr) + row * op_pre.ld, gcol0, op_pre.cols, cpre);
                             r = __ldg(static_cast<const float*>(P.opnd[st.a[1]].ptr) + row);
-                            sstat = __ldg(static_cast<const float*>(P.opnd[st.a[3]].ptr) + row);
+                            float* sp_ = static_cast<float*>(const_cast<void*>(P.opnd[st.a[3]].ptr));
+                            if (st.fin_src) {
+                                const DevOperand& fp = P.opnd[st.fin_src - 1];
+                                sstat = finalize_row(static_cast<const float*>(fp.ptr) + row * fp.ld, (int)fp.cols,
+                                                     st.fin_kind, (float)st.fin_d, st.fin_eps);
+                                if (n0 == 0 && j == 0) sp_[row] = sstat;
+                            } else {
+                                sstat = __ldg(sp_ + row);
+                            }
                         } else {
 #pragma unroll
                             for (int i = 0; i < 32; ++i) cpre[i] = 0.f;

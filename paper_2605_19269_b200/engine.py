@@ -271,9 +271,19 @@ def run_gemm(
     read_bytes = a.rows * a.cols * a.precision.storage_bytes + b.rows * b.cols * b.precision.storage_bytes
     write_bytes = 0
 
+    # deferred finalizers (reductions.PendingFinalize): a pending statistic vector bound once,
+    # as a RowScale operand or as RmsNormBackwardLocal's stat, is computed by this launch
+    fin_targets = {}
+    for si, (op, wd, args) in enumerate(steps):
+        slot = args[0] if op == nat.OP_ROW_SCALE else args[3] if op == nat.OP_RMSNORM_BWD else None
+        if slot is not None:
+            fin_targets.setdefault(slot, []).append(si)
+    bound_ids = [id(bindings.get(n)) for n in onames]
+
     # ---- operands
     keep = []
-    op_descs = (nat.Tensor * max(1, len(onames)))()
+    descs = []
+    deferred = []       # (operand slot, consuming step, vector, PendingFinalize)
     for i, name in enumerate(onames):
         op = program.operands[name]
         if name not in bindings:
@@ -297,8 +307,14 @@ def run_gemm(
                     raise DimensionError(f"operand {name!r} has length {len(val)}, expected {want}")
             elif len(val) != p.m:
                 raise DimensionError(f"operand {name!r} has length {len(val)}, expected {p.m}")
-            t = val.tensor if val.tensor.dtype == torch.float32 else val.tensor.float()
-            t = t.contiguous()
+            pend = getattr(val, "_pending", None)
+            if (pend is not None and op.kind is OperandKind.COL_VEC and len(fin_targets.get(i, ())) == 1
+                    and bound_ids.count(id(val)) == 1):
+                t = val._t                       # written by this launch
+                deferred.append((i, fin_targets[i][0], val, pend))
+            else:
+                t = val.tensor if val.tensor.dtype == torch.float32 else val.tensor.float()
+                t = t.contiguous()
             read_bytes += len(val) * val.precision.storage_bytes
         else:  # LABELS
             if isinstance(val, torch.Tensor):
@@ -321,29 +337,35 @@ def run_gemm(
             t = arr_dev.to(device=dev, dtype=torch.int64).contiguous()
             read_bytes += p.m * LABEL_BYTES
         keep.append(t)
-        op_descs[i] = nat.tensor_desc(t)
+        descs.append(nat.tensor_desc(t))
 
     # ---- compact RoPE tables (qkv_rope_tables pairs): extra operands the specialised
     # kernel loads instead of the full (m, n) tables; the generic interpreter ignores them
-    nops = len(onames)
     steps = list(steps)   # the lowering is memoized on the program: never edit it in place
     if prec is PrecisionMode.SIMBF16:
         from .kernels import rope_compact_of
 
         for si, (op, wd, args) in enumerate(steps):
-            if op != nat.OP_ROPE or len(onames) + 2 > nat.MAX_OPERANDS:
+            if op != nat.OP_ROPE or len(descs) + 2 > nat.MAX_OPERANDS:
                 continue
             spec = rope_compact_of(bindings[onames[args[0]]], bindings[onames[args[1]]])
             if spec is None or 2 * spec.hidden > p.n or spec.cos.shape[0] != p.m:
                 continue
-            grown = (nat.Tensor * (nops + 2))()
-            for j in range(nops):
-                grown[j] = op_descs[j]
-            grown[nops], grown[nops + 1] = nat.tensor_desc(spec.cos), nat.tensor_desc(spec.sin)
+            nops = len(descs)
+            descs += [nat.tensor_desc(spec.cos), nat.tensor_desc(spec.sin)]
             keep.extend((spec.cos, spec.sin))
-            op_descs = grown
             steps[si] = (op, wd, list(args[:3]) + [nops + 1, nops + 2, spec.hidden, 0])
-            nops += 2
+    # ---- deferred finalizers: the partials become an extra operand of the consuming step
+    fin = {}
+    for slot, si, vec, pend in deferred:
+        if len(descs) + 1 > nat.MAX_OPERANDS:
+            vec.tensor                               # no operand slot left: finalize standalone
+            continue
+        descs.append(nat.tensor_desc(pend.partials, nat.F32))
+        keep.append(pend.partials)
+        fin[si] = (len(descs), pend.kind, pend.d, pend.eps)
+    nops = len(descs)
+    op_descs = (nat.Tensor * max(1, nops))(*descs)
 
     # ---- stores
     st_descs = (nat.Store * max(1, len(snames)))()
@@ -395,7 +417,8 @@ def run_gemm(
         write_bytes += p.m * n_out * prec.storage_bytes
     step_arr = (nat.Step * max(1, len(steps)))()
     for i, (op, wd, args) in enumerate(steps):
-        step_arr[i] = nat.Step(op, wd, (ctypes.c_int32 * 7)(*args), 0)
+        fs, fk, fd, fe = fin.get(i, (0, 0, 0, 0.0))
+        step_arr[i] = nat.Step(op, wd, (ctypes.c_int32 * 7)(*args), fs, fk, fd, fe, 0)
 
     def enqueue(ta, tb, kk, program_on, mdesc, acc_t, odtype):
         ws = nat.workspace(dev)
@@ -432,6 +455,10 @@ def run_gemm(
                 acc = part
             else:
                 enqueue(ta, tb, 6 * kp, True, main_desc, acc, out_code)
+
+    for _, si, vec, pend in deferred:
+        if si in fin:
+            pend.adopt(vec)                          # the enqueued launch writes the vector
 
     # ---- fold pieces into the reference block layout
     aux: dict = {}

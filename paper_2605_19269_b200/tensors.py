@@ -274,13 +274,14 @@ class DenseMatrix:
 class Vector:
     """1-D device tensor (float32 in simulated modes) tagged with a precision."""
 
-    __slots__ = ("_t", "precision", "_host")
+    __slots__ = ("_t", "precision", "_host", "_pending")
 
     def __init__(self, data, precision: PrecisionMode = PrecisionMode.EXACT64):
         import torch
 
         self.precision = precision
         self._host = None
+        self._pending = None
         if isinstance(data, np.ndarray):
             if data.ndim != 1:
                 raise DimensionError(f"Vector needs a 1-D array, got ndim={data.ndim}")
@@ -322,16 +323,21 @@ class Vector:
         obj._t = tensor
         obj.precision = precision
         obj._host = None
+        obj._pending = None
         return obj
 
     @property
     def tensor(self):
+        # a deferred finalizer result (reductions.py) that no consuming launch has taken over
+        # yet is computed now, by its standalone kernel
+        if self._pending is not None:
+            self._pending.materialize(self)
         return self._t
 
     @property
     def data(self) -> np.ndarray:
         if self._host is None:
-            arr = np.ascontiguousarray(self._t.detach().cpu().double().numpy())
+            arr = np.ascontiguousarray(self.tensor.detach().cpu().double().numpy())
             arr.setflags(write=False)
             self._host = arr
         return self._host
