@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cuda_bf16.h>
 #include "coda_gemm.cuh"
+#include "coda_ptx.cuh"
 
 namespace coda {
 
@@ -355,6 +356,108 @@ coda_rope_backward_stat128_compact_kernel(const __nv_bfloat16* __restrict__ g, i
                 if (ok[u] && (lane % LPB) == 0) rowdot[i * ldd + c0[u] / 128] = p;
             }
         }
+    }
+}
+
+// Compact-table boundary RoPE backward with bulk-copy staging (bf16, default 128-column
+// row blocks).  The plain compact kernel keeps only one 16-B vector of each operand in
+// flight per thread, which leaves it latency-bound (0.6 of HBM under the power cap).  Here
+// each CTA owns a contiguous run of rows and streams them in RBS_SEG-column segments: one
+// thread issues cp.async.bulk copies of the grad / rotated row segments and of the two
+// compact-table segments into an RBS_STAGES-deep shared-memory ring (RBS_STAGES - 1 segments,
+// ~42 KiB, in flight per CTA); all threads compute from shared memory, store the counter-
+// rotated gradient with coalesced 16-B stores and reduce each 128-column block's dot with a
+// 16-lane shuffle tree.  Same arithmetic as coda_rope_backward_stat128_compact_kernel.
+constexpr int RBS_SEG = 1024;                         // columns per segment
+constexpr int RBS_THREADS = RBS_SEG / 8;              // one 16-B bf16 vector per thread per operand
+constexpr int RBS_STAGES = 8;
+constexpr int RBS_STAGE_BYTES = 2 * RBS_SEG * 2 + 2 * (RBS_SEG / 2) * 2;   // grad, rotated, cos, sin
+constexpr size_t rbs_smem_bytes() { return (size_t)RBS_STAGES * RBS_STAGE_BYTES + RBS_STAGES * 8 + 128; }
+
+__global__ void __launch_bounds__(RBS_THREADS)
+coda_rope_backward_stat_bulk_kernel(const __nv_bfloat16* __restrict__ g, int64_t ldg,
+                                    const __nv_bfloat16* __restrict__ rot, int64_t ldr,
+                                    const __nv_bfloat16* __restrict__ cs, int64_t ldc,
+                                    const __nv_bfloat16* __restrict__ sn, int64_t lds, int64_t h,
+                                    int64_t m, int64_t n, __nv_bfloat16* __restrict__ gz, int64_t ldz,
+                                    float* __restrict__ rowdot, int64_t ldd) {
+    extern __shared__ __align__(128) uint8_t rbs_smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(rbs_smem + RBS_STAGES * RBS_STAGE_BYTES);
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int64_t segs_per_row = n / RBS_SEG;
+    // contiguous rows per CTA (balanced to within one row)
+    const int64_t r0 = m * blockIdx.x / gridDim.x, r1 = m * (blockIdx.x + 1) / gridDim.x;
+    const int64_t nseg = (r1 - r0) * segs_per_row;
+    if (tid == 0) {
+        for (int s = 0; s < RBS_STAGES; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    griddep_wait();
+    griddep_launch_dependents();
+    auto issue = [&](int64_t sidx) {
+        const int st = (int)(sidx % RBS_STAGES);
+        const int64_t row = r0 + sidx / segs_per_row;
+        const int64_t c0 = (sidx % segs_per_row) * RBS_SEG;
+        const uint32_t base = smem_u32(rbs_smem + st * RBS_STAGE_BYTES);
+        const bool rotates = c0 < 2 * h;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full[st], (uint32_t)(rotates ? RBS_STAGE_BYTES : 2 * RBS_SEG * 2));
+        bulk_load_1d(base, g + row * ldg + c0, RBS_SEG * 2, &full[st]);
+        bulk_load_1d(base + RBS_SEG * 2, rot + row * ldr + c0, RBS_SEG * 2, &full[st]);
+        if (rotates) {
+            const int64_t p0 = (c0 % h) / 2;
+            bulk_load_1d(base + 4 * RBS_SEG, cs + row * ldc + p0, RBS_SEG, &full[st]);
+            bulk_load_1d(base + 5 * RBS_SEG, sn + row * lds + p0, RBS_SEG, &full[st]);
+        }
+    };
+    if (tid == 0)
+        for (int64_t s = 0; s < RBS_STAGES - 1 && s < nseg; ++s) issue(s);
+    for (int64_t sidx = 0; sidx < nseg; ++sidx) {
+        const int st = (int)(sidx % RBS_STAGES);
+        if (tid == 0 && sidx + RBS_STAGES - 1 < nseg) issue(sidx + RBS_STAGES - 1);
+        mbar_wait(&full[st], (uint32_t)((sidx / RBS_STAGES) & 1));
+        const int64_t row = r0 + sidx / segs_per_row;
+        const int64_t c0 = (sidx % segs_per_row) * RBS_SEG;
+        const uint8_t* sb = rbs_smem + st * RBS_STAGE_BYTES;
+        float gv[8], rv[8], cv[8], sv[8], zv[8];
+        Io<__nv_bfloat16>::load_shared(reinterpret_cast<const __nv_bfloat16*>(sb) + tid * 8, gv);
+        Io<__nv_bfloat16>::load_shared(reinterpret_cast<const __nv_bfloat16*>(sb + RBS_SEG * 2) + tid * 8, rv);
+        if (c0 < 2 * h) {
+            const uint2 uc = *reinterpret_cast<const uint2*>(sb + 4 * RBS_SEG + tid * 8);
+            const uint2 us = *reinterpret_cast<const uint2*>(sb + 5 * RBS_SEG + tid * 8);
+            const uint32_t wc[2] = {uc.x, uc.y}, ws[2] = {us.x, us.y};
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const float c_lo = __uint_as_float(wc[j] << 16), c_hi = __uint_as_float(wc[j] & 0xFFFF0000u);
+                const float s_lo = __uint_as_float(ws[j] << 16), s_hi = __uint_as_float(ws[j] & 0xFFFF0000u);
+                cv[4 * j] = cv[4 * j + 1] = c_lo;
+                cv[4 * j + 2] = cv[4 * j + 3] = c_hi;
+                sv[4 * j] = sv[4 * j + 1] = s_lo;
+                sv[4 * j + 2] = sv[4 * j + 3] = s_hi;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                cv[e] = 1.0f;
+                sv[e] = 0.0f;
+            }
+        }
+        float p = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float g0 = gv[2 * k], g1 = gv[2 * k + 1];
+            zv[2 * k] = g0 * cv[2 * k] + g1 * sv[2 * k];
+            zv[2 * k + 1] = -g0 * sv[2 * k + 1] + g1 * cv[2 * k + 1];
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) p += gv[e] * rv[e];
+        Io<__nv_bfloat16>::store(gz + row * ldz + c0 + tid * 8, zv);
+#pragma unroll
+        for (int off = 8; off >= 1; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+        if ((lane & 15) == 0) rowdot[row * ldd + (c0 + tid * 8) / 128] = p;
+        __syncthreads();   // every thread is done with stage `st` before it is refilled
     }
 }
 

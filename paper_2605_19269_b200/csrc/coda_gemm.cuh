@@ -111,6 +111,15 @@ template <> struct Io<__nv_bfloat16> {
         }
         *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
     }
+    __device__ static __forceinline__ void load_shared(const __nv_bfloat16* p, float* d) {
+        const uint4 u = *reinterpret_cast<const uint4*>(p);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            d[2 * i] = __uint_as_float(w[i] << 16);
+            d[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+        }
+    }
     __device__ static __forceinline__ float load1(const __nv_bfloat16* p) { return __bfloat162float(p[0]); }
     __device__ static __forceinline__ void store1(__nv_bfloat16* p, float x) { p[0] = __float2bfloat16_rn(x); }
 };

@@ -54,6 +54,15 @@ __device__ __forceinline__ void tma_load_2d(uint32_t smem_dst, const void* desc,
         : "memory");
 }
 
+// 1-D bulk copy global -> shared (no tensor map): `bytes` a multiple of 16, both addresses
+// 16-byte aligned; completes `bytes` of transaction count on `bar`.
+__device__ __forceinline__ void bulk_load_1d(uint32_t smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        :: "r"(smem_dst), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // L2 prefetch of a TMA box (no smem, no barrier): warms L2 ahead of the real load.
 __device__ __forceinline__ void tma_prefetch_2d(const void* desc, int c0, int c1) {
     asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];"

@@ -428,7 +428,7 @@ def run_gemm(
         acc_desc = nat.tensor_desc(acc_t) if acc_t is not None else None
         nat.call("coda_gemm_epilogue", ctypes.byref(prob), ctypes.byref(nat.tensor_desc(ta)),
                  ctypes.byref(nat.tensor_desc(tb)), step_arr, len(steps) if program_on else 0, op_descs,
-                 nops, st_descs, len(snames) if program_on else 0,
+                 nops if program_on else 0, st_descs, len(snames) if program_on else 0,
                  ctypes.byref(mdesc) if mdesc is not None else None,
                  ctypes.byref(acc_desc) if acc_desc is not None else None, _stream(dev),
                  tag=f"{kernel_name} {p.m}x{p.n}x{p.k}{' TN' if p.trans_a else ''}{' NT' if p.trans_b else ''}",
