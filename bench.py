@@ -20,6 +20,7 @@ Python reference cannot travel to the GPU box) on all host cores instead.
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
 import statistics
@@ -44,6 +45,10 @@ CONFIGS = {
 }
 KV = {"c4gqa": 1024}   # k / v span width (default: d, the reference's packed 3d)
 BLOCKS = {"c5": 4}
+# SMs reserved for the NCCL weight-gradient all-reduce while it overlaps the backward (N > 1).
+# Measured cost on one GPU with the same caps: 8 SMs +4.5 % step, 16 SMs +9.4 %
+# (profiles/r02_ab_fold_cap.json); NCCL is limited to the same number of CTAs.
+DEFAULT_COMM_SMS = 8
 FP32 = {"c1"}          # BASELINE config 0 is the fp32 (SIM32) path
 
 
@@ -217,14 +222,14 @@ def run_step(cd, cfg, weights, acts, cos, sin, hook=None, before_backward=None, 
         fwd = stack.stack_forward(acts["x"], acts["z"], weights, cos, sin, config=cfg)
         if before_backward is not None:
             before_backward()
-        with _native.limit_sms(bwd_sms):
+        with (_native.limit_sms(bwd_sms) if bwd_sms else contextlib.nullcontext()):
             grads = stack.stack_backward(acts["grad_qkv"], acts["grad_residual"], fwd, weights, config=cfg,
                                          wgrad_hook=hook)
         return fwd, grads[0]
     fwd = cd.layer_forward(acts["x"], acts["z"], weights, cos, sin, config=cfg)
     if before_backward is not None:
         before_backward()
-    with _native.limit_sms(bwd_sms):
+    with (_native.limit_sms(bwd_sms) if bwd_sms else contextlib.nullcontext()):
         bwd = cd.layer_backward(acts["grad_qkv"], fwd.tape, weights, grad_residual=acts["grad_residual"],
                                 config=cfg, wgrad_hook=hook)
     return fwd, bwd
@@ -483,7 +488,7 @@ def coda_arm(args, rank, world, local_rank):
     if world > 1 or args.force_dist:
         import torch.distributed as dist  # noqa: F811
 
-        comm = args.comm_sms if args.comm_sms is not None else (16 if world > 1 else 0)
+        comm = args.comm_sms if args.comm_sms is not None else (DEFAULT_COMM_SMS if world > 1 else 0)
         if comm > 0:
             # the all-reduce runs concurrently with the SM-capped backward GEMMs: keep NCCL
             # inside the SMs left to it
@@ -512,10 +517,12 @@ def coda_arm(args, rank, world, local_rank):
         P = cd.PrecisionMode.SIM32
         cfg = cd.PipelineConfig(hidden=d, ffn=2 * inter, precision=P)
     weights, acts, cos, sin = make_workload(cd, d, inter, m, sh.start, device, blocks=nblocks, fp32=fp32, kv=kv)
-    hook = parallel.WgradAllReduce(dist, device, f32=args.wgrad_dtype == "f32") if dist is not None else None
-    # SMs left to the side-stream all-reduce while the backward's persistent GEMMs run
-    comm_sms = args.comm_sms if args.comm_sms is not None else (16 if world > 1 else 0)
-    bwd_sms = (_native.num_sms() - comm_sms) if (dist is not None and comm_sms > 0) else 0
+    # SMs left to the side-stream all-reduce while a reduction is in flight (the hook caps the
+    # persistent GEMMs from the first weight gradient of the backward until wait())
+    comm_sms = args.comm_sms if args.comm_sms is not None else (DEFAULT_COMM_SMS if world > 1 else 0)
+    hook = parallel.WgradAllReduce(dist, device, f32=args.wgrad_dtype == "f32",
+                                   reserve_sms=comm_sms) if dist is not None else None
+    bwd_sms = 0
 
     def step():
         out = run_step(cd, cfg, weights, acts, cos, sin, hook, bwd_sms=bwd_sms)
@@ -827,7 +834,7 @@ def main(argv=None):
                     help="override the config's token count (per-rank shape proxies at N=1)")
     ap.add_argument("--fold-gamma", action="store_true", help="gains folded into W (north_star variant)")
     ap.add_argument("--comm-sms", type=int, default=None,
-                    help="SMs left to the NCCL all-reduce during the backward (default 16 when N > 1)")
+                    help="SMs left to the NCCL all-reduce while it overlaps the backward (default 8 when N > 1)")
     ap.add_argument("--wgrad-dtype", choices=("f32", "bf16"), default="f32",
                     help="dtype of the data-parallel weight-gradient all-reduce (f32: single rounding, "
                          "the reference's; bf16 halves the bytes)")

@@ -888,20 +888,14 @@ int coda_rope_backward_stat_compact(const coda_tensor_t* grad, const coda_tensor
     }
     DeviceGuard dg;
     if ((rc = bind_device(grad->ptr, dg))) return rc;
-    // bulk-copy staging when rows split into whole segments and every row start is 16-B aligned
-    const bool bulk = grad->cols % coda::RBS_SEG == 0 && h % coda::RBS_SEG == 0 && grad->ld % 8 == 0 &&
-                      rotated->ld % 8 == 0 && cos_c->ld % 8 == 0 && sin_c->ld % 8 == 0 && grad_z->ld % 8 == 0;
-    if (bulk) {
-        static std::atomic<uint64_t> configured{0};
-        const size_t smem = coda::rbs_smem_bytes();
-        if (first_use_on_device(configured)) {
-            cudaError_t e = cudaFuncSetAttribute(coda::coda_rope_backward_stat_bulk_kernel,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(rope bulk)");
-        }
-        const int64_t ctas = std::min<int64_t>(grad->rows, (int64_t)num_sms() * 4);
-        return launch_pdl(coda::coda_rope_backward_stat_bulk_kernel, dim3((unsigned)ctas), dim3(coda::RBS_THREADS),
-                          smem, (cudaStream_t)stream, 1, "coda::coda_rope_backward_stat_bulk_kernel",
+    // deep-load variant when rows split into whole 3 x 2048-column sweeps (16-B aligned rows)
+    const bool deep = grad->cols % (coda::RBD_U * 2048) == 0 && grad->ld % 8 == 0 && rotated->ld % 8 == 0 &&
+                      grad_z->ld % 8 == 0 && cos_c->ld % 4 == 0 && sin_c->ld % 4 == 0;
+    if (deep) {
+        const int64_t items = grad->rows * (grad->cols / (coda::RBD_U * 2048));
+        const unsigned g = (unsigned)std::min<int64_t>(items, (int64_t)num_sms() * 8);
+        return launch_pdl(coda::coda_rope_backward_stat_deep_kernel, dim3(g), dim3(256), 0, (cudaStream_t)stream, 1,
+                          "coda::coda_rope_backward_stat_deep_kernel",
                           (const __nv_bfloat16*)grad->ptr, grad->ld, (const __nv_bfloat16*)rotated->ptr, rotated->ld,
                           (const __nv_bfloat16*)cos_c->ptr, cos_c->ld, (const __nv_bfloat16*)sin_c->ptr, sin_c->ld, h,
                           grad->rows, grad->cols, (__nv_bfloat16*)grad_z->ptr, grad_z->ld, rowdot, ld_rowdot);

@@ -359,75 +359,64 @@ coda_rope_backward_stat128_compact_kernel(const __nv_bfloat16* __restrict__ g, i
     }
 }
 
-// Compact-table boundary RoPE backward with bulk-copy staging (bf16, default 128-column
-// row blocks).  The plain compact kernel keeps only one 16-B vector of each operand in
-// flight per thread, which leaves it latency-bound (0.6 of HBM under the power cap).  Here
-// each CTA owns a contiguous run of rows and streams them in RBS_SEG-column segments: one
-// thread issues cp.async.bulk copies of the grad / rotated row segments and of the two
-// compact-table segments into an RBS_STAGES-deep shared-memory ring (RBS_STAGES - 1 segments,
-// ~42 KiB, in flight per CTA); all threads compute from shared memory, store the counter-
-// rotated gradient with coalesced 16-B stores and reduce each 128-column block's dot with a
-// 16-lane shuffle tree.  Same arithmetic as coda_rope_backward_stat128_compact_kernel.
-constexpr int RBS_SEG = 1024;                         // columns per segment
-constexpr int RBS_THREADS = RBS_SEG / 8;              // one 16-B bf16 vector per thread per operand
-constexpr int RBS_STAGES = 8;
-constexpr int RBS_STAGE_BYTES = 2 * RBS_SEG * 2 + 2 * (RBS_SEG / 2) * 2;   // grad, rotated, cos, sin
-constexpr size_t rbs_smem_bytes() { return (size_t)RBS_STAGES * RBS_STAGE_BYTES + RBS_STAGES * 8 + 128; }
+// Compact-table boundary RoPE backward, deep-load variant (bf16, default 128-column blocks,
+// n % (RBD_U * 2048) == 0, h % 32 == 0).  The plain compact kernel holds one 16-B vector of
+// each operand per thread in flight and is latency-bound under the power cap (0.6 of HBM).
+// Here every thread first issues RBD_U independent 16-B loads of grad and of rotated (kept as
+// raw bf16 words, 8 registers each) plus their table words, then converts and computes, so
+// ~3x the bytes are in flight per thread at the same register budget.  Same arithmetic and
+// reduction order as coda_rope_backward_stat128_compact_kernel.
+constexpr int RBD_U = 3;
 
-__global__ void __launch_bounds__(RBS_THREADS)
-coda_rope_backward_stat_bulk_kernel(const __nv_bfloat16* __restrict__ g, int64_t ldg,
+__global__ void __launch_bounds__(256)
+coda_rope_backward_stat_deep_kernel(const __nv_bfloat16* __restrict__ g, int64_t ldg,
                                     const __nv_bfloat16* __restrict__ rot, int64_t ldr,
                                     const __nv_bfloat16* __restrict__ cs, int64_t ldc,
                                     const __nv_bfloat16* __restrict__ sn, int64_t lds, int64_t h,
                                     int64_t m, int64_t n, __nv_bfloat16* __restrict__ gz, int64_t ldz,
                                     float* __restrict__ rowdot, int64_t ldd) {
-    extern __shared__ __align__(128) uint8_t rbs_smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(rbs_smem + RBS_STAGES * RBS_STAGE_BYTES);
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int64_t segs_per_row = n / RBS_SEG;
-    // contiguous rows per CTA (balanced to within one row)
-    const int64_t r0 = m * blockIdx.x / gridDim.x, r1 = m * (blockIdx.x + 1) / gridDim.x;
-    const int64_t nseg = (r1 - r0) * segs_per_row;
-    if (tid == 0) {
-        for (int s = 0; s < RBS_STAGES; ++s) mbar_init(&full[s], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
     griddep_wait();
     griddep_launch_dependents();
-    auto issue = [&](int64_t sidx) {
-        const int st = (int)(sidx % RBS_STAGES);
-        const int64_t row = r0 + sidx / segs_per_row;
-        const int64_t c0 = (sidx % segs_per_row) * RBS_SEG;
-        const uint32_t base = smem_u32(rbs_smem + st * RBS_STAGE_BYTES);
-        const bool rotates = c0 < 2 * h;
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&full[st], (uint32_t)(rotates ? RBS_STAGE_BYTES : 2 * RBS_SEG * 2));
-        bulk_load_1d(base, g + row * ldg + c0, RBS_SEG * 2, &full[st]);
-        bulk_load_1d(base + RBS_SEG * 2, rot + row * ldr + c0, RBS_SEG * 2, &full[st]);
-        if (rotates) {
-            const int64_t p0 = (c0 % h) / 2;
-            bulk_load_1d(base + 4 * RBS_SEG, cs + row * ldc + p0, RBS_SEG, &full[st]);
-            bulk_load_1d(base + 5 * RBS_SEG, sn + row * lds + p0, RBS_SEG, &full[st]);
+    using TS = __nv_bfloat16;
+    const int lane = threadIdx.x & 31;
+    constexpr int64_t SWEEP = 256 * 8;
+    const int64_t per_row = n / (RBD_U * SWEEP);
+    const int64_t total = m * per_row;
+    for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+        const int64_t i = it / per_row;
+        const int64_t base = (it - i * per_row) * (RBD_U * SWEEP);
+        const TS* gr = g + i * ldg;
+        const TS* rr = rot + i * ldr;
+        uint4 gw[RBD_U], rw[RBD_U];
+        uint2 cw[RBD_U], sw[RBD_U];
+        int64_t c0[RBD_U];
+#pragma unroll
+        for (int u = 0; u < RBD_U; ++u) {
+            c0[u] = base + u * SWEEP + (int64_t)threadIdx.x * 8;
+            gw[u] = __ldg(reinterpret_cast<const uint4*>(gr + c0[u]));
+            rw[u] = __ldg(reinterpret_cast<const uint4*>(rr + c0[u]));
+            if (c0[u] < 2 * h) {
+                const int64_t p0 = (c0[u] % h) / 2;
+                cw[u] = __ldg(reinterpret_cast<const uint2*>(cs + i * ldc + p0));
+                sw[u] = __ldg(reinterpret_cast<const uint2*>(sn + i * lds + p0));
+            } else {
+                cw[u] = make_uint2(0x3F803F80u, 0x3F803F80u);   // bf16 1.0 pairs
+                sw[u] = make_uint2(0u, 0u);
+            }
         }
-    };
-    if (tid == 0)
-        for (int64_t s = 0; s < RBS_STAGES - 1 && s < nseg; ++s) issue(s);
-    for (int64_t sidx = 0; sidx < nseg; ++sidx) {
-        const int st = (int)(sidx % RBS_STAGES);
-        if (tid == 0 && sidx + RBS_STAGES - 1 < nseg) issue(sidx + RBS_STAGES - 1);
-        mbar_wait(&full[st], (uint32_t)((sidx / RBS_STAGES) & 1));
-        const int64_t row = r0 + sidx / segs_per_row;
-        const int64_t c0 = (sidx % segs_per_row) * RBS_SEG;
-        const uint8_t* sb = rbs_smem + st * RBS_STAGE_BYTES;
-        float gv[8], rv[8], cv[8], sv[8], zv[8];
-        Io<__nv_bfloat16>::load_shared(reinterpret_cast<const __nv_bfloat16*>(sb) + tid * 8, gv);
-        Io<__nv_bfloat16>::load_shared(reinterpret_cast<const __nv_bfloat16*>(sb + RBS_SEG * 2) + tid * 8, rv);
-        if (c0 < 2 * h) {
-            const uint2 uc = *reinterpret_cast<const uint2*>(sb + 4 * RBS_SEG + tid * 8);
-            const uint2 us = *reinterpret_cast<const uint2*>(sb + 5 * RBS_SEG + tid * 8);
-            const uint32_t wc[2] = {uc.x, uc.y}, ws[2] = {us.x, us.y};
+#pragma unroll
+        for (int u = 0; u < RBD_U; ++u) {
+            const uint32_t gv_[4] = {gw[u].x, gw[u].y, gw[u].z, gw[u].w};
+            const uint32_t rv_[4] = {rw[u].x, rw[u].y, rw[u].z, rw[u].w};
+            const uint32_t wc[2] = {cw[u].x, cw[u].y}, ws[2] = {sw[u].x, sw[u].y};
+            float gv[8], rv[8], cv[8], sv[8], zv[8];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                gv[2 * e] = __uint_as_float(gv_[e] << 16);
+                gv[2 * e + 1] = __uint_as_float(gv_[e] & 0xFFFF0000u);
+                rv[2 * e] = __uint_as_float(rv_[e] << 16);
+                rv[2 * e + 1] = __uint_as_float(rv_[e] & 0xFFFF0000u);
+            }
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const float c_lo = __uint_as_float(wc[j] << 16), c_hi = __uint_as_float(wc[j] & 0xFFFF0000u);
@@ -437,27 +426,20 @@ coda_rope_backward_stat_bulk_kernel(const __nv_bfloat16* __restrict__ g, int64_t
                 sv[4 * j] = sv[4 * j + 1] = s_lo;
                 sv[4 * j + 2] = sv[4 * j + 3] = s_hi;
             }
-        } else {
+            float p = 0.0f;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                cv[e] = 1.0f;
-                sv[e] = 0.0f;
+            for (int k = 0; k < 4; ++k) {
+                const float g0 = gv[2 * k], g1 = gv[2 * k + 1];
+                zv[2 * k] = g0 * cv[2 * k] + g1 * sv[2 * k];
+                zv[2 * k + 1] = -g0 * sv[2 * k + 1] + g1 * cv[2 * k + 1];
             }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) p += gv[e] * rv[e];
+            Io<TS>::store(gz + i * ldz + c0[u], zv);
+#pragma unroll
+            for (int off = 8; off >= 1; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+            if ((lane & 15) == 0) rowdot[i * ldd + c0[u] / 128] = p;
         }
-        float p = 0.0f;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float g0 = gv[2 * k], g1 = gv[2 * k + 1];
-            zv[2 * k] = g0 * cv[2 * k] + g1 * sv[2 * k];
-            zv[2 * k + 1] = -g0 * sv[2 * k + 1] + g1 * cv[2 * k + 1];
-        }
-#pragma unroll
-        for (int e = 0; e < 8; ++e) p += gv[e] * rv[e];
-        Io<__nv_bfloat16>::store(gz + row * ldz + c0 + tid * 8, zv);
-#pragma unroll
-        for (int off = 8; off >= 1; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
-        if ((lane & 15) == 0) rowdot[row * ldd + (c0 + tid * 8) / 128] = p;
-        __syncthreads();   // every thread is done with stage `st` before it is refilled
     }
 }
 

@@ -59,8 +59,14 @@ class WgradAllReduce:
     tensors (gloo, tests) it is a plain synchronous all_reduce.
     """
 
-    def __init__(self, dist, device=None, f32: bool = True):
+    def __init__(self, dist, device=None, f32: bool = True, reserve_sms: int = 0):
         self.dist = dist
+        # while a reduction is in flight the persistent GEMMs this thread enqueues use
+        # num_sms - reserve_sms SMs, so the collective on the side stream has SMs of its own
+        # (the first weight gradient arrives a quarter into the backward: the launches before
+        # it, and the next step's forward after wait(), run on every SM)
+        self.reserve_sms = int(reserve_sms)
+        self._capped = None
         # f32: layer_backward hands over unrounded float32 weight gradients and rounds the
         # reduced sums once (the reference's single rounding); False: bf16 gradients are
         # reduced as stored (half the bytes on the wire, one rounding per partial)
@@ -79,6 +85,8 @@ class WgradAllReduce:
             return
         import torch
 
+        self._cap()
+
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(tensor.device))
         with torch.cuda.stream(self.side):
@@ -86,8 +94,19 @@ class WgradAllReduce:
             self.dist.all_reduce(tensor)
         tensor.record_stream(self.side)
 
+    def _cap(self) -> None:
+        """First reduction in flight: cap this thread's GEMM launches until wait()."""
+        from . import _native
+
+        if self.reserve_sms > 0 and self._capped is None:
+            self._capped = _native.limit_sms(max(1, _native.num_sms() - self.reserve_sms))
+            self._capped.__enter__()
+
     def wait(self) -> None:
         if self.side is not None:
             import torch
 
             torch.cuda.current_stream(self.side.device).wait_stream(self.side)
+        if self._capped is not None:
+            self._capped.__exit__(None, None, None)
+            self._capped = None

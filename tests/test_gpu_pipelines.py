@@ -360,12 +360,12 @@ def test_pending_finalizer_materializes_on_read(cuda_ready):
     assert y.main.shape == (200, 64)
 
 
-def test_rope_backward_stat_bulk_path(cuda_ready):
-    """The bulk-copy staged boundary kernel (compact tables, h % 1024 == 0) matches the oracle
-    and is bit-identical to the full-table kernel on the same values."""
+def test_rope_backward_stat_deep_path(cuda_ready):
+    """The deep-load boundary kernel (compact tables, n % 6144 == 0) matches the oracle and is
+    bit-identical to the full-table kernel on the same values."""
     cd = _cd()
     P = cd.PrecisionMode.SIMBF16
-    m, d = 301, 1024
+    m, d = 301, 2048
     rng = np.random.default_rng(13)
     cos_c, sin_c = cd.qkv_rope_tables(m, d, start=5, precision=P)
     assert cd.kernels.rope_compact_of(cos_c, sin_c) is not None

@@ -106,3 +106,36 @@ def test_layer_backward_waits_for_async_reduction_before_rounding():
 
     src = inspect.getsource(kernels.layer_backward)
     assert src.index("wait()") < src.index("to_storage(g, prec)")
+
+
+def test_hook_caps_sms_only_while_reductions_are_in_flight():
+    """WgradAllReduce(reserve_sms=k): from the first reduction until wait(), this thread's GEMM
+    launches are capped at num_sms - k (room for the NCCL kernels on the side stream); before
+    the first weight gradient and after wait() they use every SM.  Exercised with a stand-in
+    side stream and collective (no GPU)."""
+    sys.path.insert(0, str(ROOT))
+    from paper_2605_19269_b200 import _native, parallel
+
+    class FakeDist:
+        def __init__(self):
+            self.calls = []
+
+        def all_reduce(self, t):
+            self.calls.append(t)
+
+    hook = parallel.WgradAllReduce(FakeDist(), None, reserve_sms=8)
+    orig_num_sms = _native.num_sms
+    try:
+        _native.num_sms = lambda: 148
+        assert _native.sm_limit() == 0
+        hook._cap()                     # what the first reduction does on the CUDA path
+        assert _native.sm_limit() == 140
+        hook._cap()                     # later reductions keep the same cap
+        assert _native.sm_limit() == 140
+        hook.wait()
+        assert _native.sm_limit() == 0 and hook._capped is None
+        none = parallel.WgradAllReduce(FakeDist(), None)
+        none._cap()
+        assert _native.sm_limit() == 0
+    finally:
+        _native.num_sms = orig_num_sms
