@@ -729,12 +729,17 @@ def coda_arm(args, rank, world, local_rank):
         top = max(prof.values(), key=lambda r: r["total_ms"])
         achieved = top["flops"] / (top["avg_ms"] / 1e3) / 1e12
         peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
-        traffic = None
+        traffic, traffic_src = None, None
         tp = ROOT / "profiles" / "traffic.json"
         if tp.exists():
-            traffic = json.loads(tp.read_text()).get(f"{args.config}:{top['name']}")
+            tj = json.loads(tp.read_text())
+            traffic = tj.get(f"{args.config}:{top['name']}")
+            meta = tj.get("_meta", {}).get(args.config)
+            if traffic is not None:
+                traffic_src = ("profiles/traffic.json: " + (f"ncu DRAM bytes of build {meta['git']} ({meta['date']})"
+                                                            if meta else "ncu DRAM bytes of a round-1 build"))
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": traffic, "kernel": top["name"],
+                    "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src, "kernel": top["name"],
                     "peak_kind": "measured sustained bf16 (MEASURED_PEAKS.json)",
                     "share_of_step": top["total_ms"] / sum(r["total_ms"] for r in prof.values())}
     total_flops = flops_per_token(d, inter, kv) * m * nblocks

@@ -888,13 +888,15 @@ int coda_rope_backward_stat_compact(const coda_tensor_t* grad, const coda_tensor
     }
     DeviceGuard dg;
     if ((rc = bind_device(grad->ptr, dg))) return rc;
-    // deep-load variant when rows split into whole 3 x 2048-column sweeps (16-B aligned rows)
-    const bool deep = grad->cols % (coda::RBD_U * 2048) == 0 && grad->ld % 8 == 0 && rotated->ld % 8 == 0 &&
+    // deep-load variant when rows split into whole 6 (or 3) x 2048-column sweeps (16-B aligned rows)
+    const int U = grad->cols % (6 * 2048) == 0 ? 6 : 3;
+    const bool deep = grad->cols % (U * 2048) == 0 && grad->ld % 8 == 0 && rotated->ld % 8 == 0 &&
                       grad_z->ld % 8 == 0 && cos_c->ld % 4 == 0 && sin_c->ld % 4 == 0;
     if (deep) {
-        const int64_t items = grad->rows * (grad->cols / (coda::RBD_U * 2048));
+        const int64_t items = grad->rows * (grad->cols / (U * 2048));
         const unsigned g = (unsigned)std::min<int64_t>(items, (int64_t)num_sms() * 8);
-        return launch_pdl(coda::coda_rope_backward_stat_deep_kernel, dim3(g), dim3(256), 0, (cudaStream_t)stream, 1,
+        auto kern = U == 6 ? coda::coda_rope_backward_stat_deep_kernel<6> : coda::coda_rope_backward_stat_deep_kernel<3>;
+        return launch_pdl(kern, dim3(g), dim3(256), 0, (cudaStream_t)stream, 1,
                           "coda::coda_rope_backward_stat_deep_kernel",
                           (const __nv_bfloat16*)grad->ptr, grad->ld, (const __nv_bfloat16*)rotated->ptr, rotated->ld,
                           (const __nv_bfloat16*)cos_c->ptr, cos_c->ld, (const __nv_bfloat16*)sin_c->ptr, sin_c->ld, h,

@@ -364,10 +364,17 @@ coda_rope_backward_stat128_compact_kernel(const __nv_bfloat16* __restrict__ g, i
 // each operand per thread in flight and is latency-bound under the power cap (0.6 of HBM).
 // Here every thread first issues RBD_U independent 16-B loads of grad and of rotated (kept as
 // raw bf16 words, 8 registers each) plus their table words, then converts and computes, so
-// ~3x the bytes are in flight per thread at the same register budget.  Same arithmetic and
+// ~3-6x the bytes are in flight per thread (RBD_U = 3 or 6 sweeps; streaming, L1-bypassing
+// loads and stores).  Same arithmetic and
 // reduction order as coda_rope_backward_stat128_compact_kernel.
-constexpr int RBD_U = 3;
+__device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
 
+template <int RBD_U>
 __global__ void __launch_bounds__(256)
 coda_rope_backward_stat_deep_kernel(const __nv_bfloat16* __restrict__ g, int64_t ldg,
                                     const __nv_bfloat16* __restrict__ rot, int64_t ldr,
@@ -393,8 +400,8 @@ coda_rope_backward_stat_deep_kernel(const __nv_bfloat16* __restrict__ g, int64_t
 #pragma unroll
         for (int u = 0; u < RBD_U; ++u) {
             c0[u] = base + u * SWEEP + (int64_t)threadIdx.x * 8;
-            gw[u] = __ldg(reinterpret_cast<const uint4*>(gr + c0[u]));
-            rw[u] = __ldg(reinterpret_cast<const uint4*>(rr + c0[u]));
+            gw[u] = ld_stream_v4(gr + c0[u]);
+            rw[u] = ld_stream_v4(rr + c0[u]);
             if (c0[u] < 2 * h) {
                 const int64_t p0 = (c0[u] % h) / 2;
                 cw[u] = __ldg(reinterpret_cast<const uint2*>(cs + i * ldc + p0));
@@ -435,7 +442,14 @@ coda_rope_backward_stat_deep_kernel(const __nv_bfloat16* __restrict__ g, int64_t
             }
 #pragma unroll
             for (int e = 0; e < 8; ++e) p += gv[e] * rv[e];
-            Io<TS>::store(gz + i * ldz + c0[u], zv);
+            {
+                uint4 o;
+                o.x = pack_bf16x2(zv[0], zv[1]);
+                o.y = pack_bf16x2(zv[2], zv[3]);
+                o.z = pack_bf16x2(zv[4], zv[5]);
+                o.w = pack_bf16x2(zv[6], zv[7]);
+                __stcs(reinterpret_cast<uint4*>(gz + i * ldz + c0[u]), o);
+            }
 #pragma unroll
             for (int off = 8; off >= 1; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
             if ((lane & 15) == 0) rowdot[i * ldd + c0[u] / 128] = p;

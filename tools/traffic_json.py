@@ -33,6 +33,16 @@ def main():
         sys.exit(f"{len(tags)} tags vs {len(launches)} ncu launches: not one measured step")
     out_path = ROOT / "profiles" / "traffic.json"
     out = json.loads(out_path.read_text()) if out_path.exists() else {}
+    out = {k: v for k, v in out.items() if not k.startswith(config + ":")}   # drop stale launches
+    import subprocess
+    import time
+
+    sha = subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], capture_output=True, text=True,
+                         cwd=str(ROOT)).stdout.strip()
+    meta = out.setdefault("_meta", {})
+    meta[config] = {"source": str(Path(csv_path).name), "git": sha, "date": time.strftime("%Y-%m-%d"),
+                    "how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none, "
+                           "one measured step of bench.py --ncu"}
     acc = {}
     for tag, (_, b) in zip(tags, launches):
         acc.setdefault(tag, []).append(b)
