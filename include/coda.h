@@ -60,6 +60,7 @@ extern "C" {
 #define CODA_OP_SWIGLU          11   /* PairwiseSwiglu     epilogue.py:449 */
 #define CODA_OP_SWIGLU_BWD      12   /* PairwiseSwigluBackward epilogue.py:469 */
 #define CODA_OP_RMSNORM_BWD     13   /* RmsNormBackwardLocal   epilogue.py:522 */
+#define CODA_OP_XENT_BWD        14   /* CrossEntropyBackward (B200 extension: softmax CE gradient) */
 
 #define CODA_MAX_STEPS       16
 #define CODA_MAX_OPERANDS    16
@@ -122,6 +123,9 @@ typedef struct {
  *   RMSNORM_BWD    arg0 = pre, arg1 = inv_rms, arg2 = gamma, arg3 = stat,
  *                  arg4 = accumulate operand or -1, arg5 = normed store,
  *                  arg6 = gamma-grad col-sum pieces store
+ *   XENT_BWD       arg0 = lse operand (col vector), arg1 = labels operand (int64),
+ *                  arg2 = row-sum pieces store of sum(tile * grad), arg3 = grad_scale
+ *                  (float bits), arg6 = row stream
  * Row streams (0 .. CODA_MAX_ROW_STREAMS-1) number the program's row-directed
  * partial emitters in order; each carries its own running block sum per row.
  * width: running width at step entry in values per 32 accumulator columns, i.e.

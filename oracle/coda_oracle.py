@@ -443,3 +443,55 @@ def layer_ref_backward(grad_qkv, grad_residual, fwd: dict, x, w: dict, cos, sin,
 
 
 GRAD_KEYS = ("x", "z", "w_out", "gamma_ffn", "w_gate_up", "w_down", "gamma_qkv", "w_qkv")
+
+
+# ----------------------------------------------------------------------------- LM head (forward pinned, backward derived)
+
+
+def lm_head_forward(a, b, z, gamma, w_vocab, labels, mode, eps=1e-6, tile_n=128, rtn=128) -> dict:
+    """K4 -> finalize -> K8 -> combine_lse -> CE finalize (kernels.py:1032-1076)."""
+    k4 = k_residual_partial_rms(a, b, z, gamma, mode, tile_n, rtn)
+    r = finalize_rms(k4["sumsq"], eps, mode)
+    k8 = k_partial_xent(k4["main"], w_vocab, labels, mode, tile_n, rtn, scale=r)
+    lse = combine_lse(k8["lse"], mode)
+    losses = stat_q(lse - k8["target"], mode)
+    return {"losses": losses, "mean": float(np.mean(losses)), "lse": lse, "normed": k4["main"],
+            "pre_norm": k4["pre_norm"], "inv_rms": r, "logits": k8["main"]}
+
+
+def lm_head_backward(fwd: dict, a, b, gamma, w_vocab, labels, mode, grad_loss=1.0, tile_m=128, tile_n=128,
+                     rtn=128) -> dict:
+    """Backward of the mean cross entropy through the LM head, in the fused order of the GPU
+    extension (no reference counterpart; SPEC.md:415 ends at the loss).  The pieces follow the
+    reference's own backward patterns: the logit gradient is softmax - onehot; the RMSNorm
+    statistic is relocated to <logits, d logits> exactly as rope_backward_stat relocates it to
+    <qkv, d qkv> (kernels.py:560-617), then k_rmsnorm_backward (kernels.py:474-525) and the
+    weight gradients as in layer_backward (kernels.py:885-1013).  Pinned by finite differences
+    of the f64 forward (tests/test_oracle_golden.py)."""
+    dt = acc_dtype(mode)
+    m = fwd["normed"].shape[0]
+    t = gemm(fwd["normed"], w_vocab, mode) * _cast(fwd["inv_rms"], mode)[:, None]
+    p = np.exp(t - _cast(fwd["lse"], mode)[:, None])
+    p[np.arange(m), np.asarray(labels, dtype=np.int64)] -= dt(1.0)
+    g = p * dt(grad_loss / m)
+    blocks = row_blocks(t.shape[1], tile_n, rtn)
+    s = finalize_rowdot((row_partials(t * g, blocks), counts_of(blocks)), fwd["normed"].shape[1], mode)
+    glog = q(g, mode)
+    k9 = k_rmsnorm_backward(glog, w_vocab, fwd["pre_norm"], fwd["inv_rms"], gamma, s, mode, tile_m=tile_m,
+                            trans_b=True)
+    gh = k9["main"]
+    return {"a": q(gemm(gh, b, mode, trans_b=True), mode), "b": q(gemm(a, gh, mode, trans_a=True), mode),
+            "z": gh, "gamma": reduce_row_partials(k9["gamma_grad"], mode),
+            "w_vocab": q(gemm(k9["normed"], glog, mode, trans_a=True), mode), "d_logits": glog, "s": s}
+
+
+def lm_head_loss64(a, b, z, gamma, w_vocab, labels, eps=1e-6) -> float:
+    """Canonical float64 mean cross entropy of the LM head (oracles.py restated): RMSNorm with
+    gain, vocabulary projection, log-softmax at the label."""
+    f = lambda x: np.asarray(x, dtype=np.float64)  # noqa: E731
+    h = f(a) @ f(b) + f(z)
+    r = 1.0 / np.sqrt(np.mean(h * h, axis=1) + eps)
+    logits = (h * r[:, None] * f(gamma)[None, :]) @ f(w_vocab)
+    mx = logits.max(axis=1)
+    lse = mx + np.log(np.exp(logits - mx[:, None]).sum(axis=1))
+    return float(np.mean(lse - logits[np.arange(len(labels)), np.asarray(labels, dtype=np.int64)]))

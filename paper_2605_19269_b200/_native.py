@@ -35,6 +35,7 @@ OP_ROPE = 10
 OP_SWIGLU = 11
 OP_SWIGLU_BWD = 12
 OP_RMSNORM_BWD = 13
+OP_XENT_BWD = 14
 
 FIN_RMS, FIN_ROWDOT = 1, 2   # deferred finalizer kinds (coda_step_t.fin_kind)
 

@@ -300,6 +300,7 @@ using coda::F_STORE_MAIN;
 using coda::F_SUMSQ;
 using coda::F_SWIGLU;
 using coda::F_SWIGLU_BWD;
+using coda::F_XENT_BWD;
 
 #define CODA_FAST_SETS(X)                                             \
     X(F_STORE_MAIN)                                                   \
@@ -322,6 +323,7 @@ using coda::F_SWIGLU_BWD;
     X(F_ROWSCALE | F_GATHER | F_LSE)                                  \
     X(F_ROWSCALE | F_GATHER | F_LSE | F_STORE_MAIN)                   \
     X(F_ROWDOT | F_ROWSCALE | F_STORE_MAIN)                           \
+    X(F_ROWSCALE | F_XENT_BWD | F_STORE_MAIN)                         \
     X(F_ROWDOT | F_ROWSCALE | F_STORE_MAIN | F_OUT_F32)
 
 template <int FL, int CG>
@@ -409,6 +411,9 @@ int match_fast(const coda_problem_t* pr, const coda_step_t* steps, int nsteps, c
         case CODA_OP_SWIGLU_BWD:
             if (!rank_ok(10) || !stores[st.arg[2]].aligned) return -1;
             fl |= F_SWIGLU_BWD; break;
+        case CODA_OP_XENT_BWD:
+            if (!rank_ok(10) || !stores[st.arg[2]].aligned) return -1;
+            fl |= F_XENT_BWD; break;
         case CODA_OP_RMSNORM_BWD:
             if (!rank_ok(10) || !stores[st.arg[6]].aligned) return -1;
             fl |= F_RMSBWD | (st.arg[4] >= 0 ? F_RMSBWD_ACC : 0); break;
@@ -572,6 +577,9 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
             ok = opnd_ok(cs.arg[0]) && store_ok(cs.arg[1]) && store_ok(cs.arg[2]) && w == 32 &&
                  stream_ok(cs.arg[6]);
             w = 64; break;
+        case CODA_OP_XENT_BWD:
+            ok = opnd_ok(cs.arg[0]) && opnd_ok(cs.arg[1]) && store_ok(cs.arg[2]) && w == 32 && stream_ok(cs.arg[6]);
+            break;
         case CODA_OP_RMSNORM_BWD:
             ok = opnd_ok(cs.arg[0]) && opnd_ok(cs.arg[1]) && opnd_ok(cs.arg[2]) && opnd_ok(cs.arg[3]) &&
                  (cs.arg[4] == -1 || opnd_ok(cs.arg[4])) && store_ok(cs.arg[5]) && store_ok(cs.arg[6]) && w == 32;
@@ -706,6 +714,12 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
             case CODA_OP_TARGET_GATHER:
                 F.labels = (const int64_t*)o[cs.arg[0]].ptr;
                 F.target = (float*)P.store[cs.arg[1]].ptr; break;
+            case CODA_OP_XENT_BWD:
+                F.xent_lse = (const float*)o[cs.arg[0]].ptr;
+                F.labels = (const int64_t*)o[cs.arg[1]].ptr;
+                memcpy(&F.xent_scale, &cs.arg[3], sizeof(float));
+                F.rowpart = (float*)P.store[cs.arg[2]].ptr; F.ld_rowpart = P.store[cs.arg[2]].ld;
+                F.rowpart_map = P.store[cs.arg[2]].map; break;
             case CODA_OP_ONLINE_LSE:
                 F.rowpart = (float*)P.store[cs.arg[0]].ptr; F.ld_rowpart = P.store[cs.arg[0]].ld;
                 F.rowpart_map = P.store[cs.arg[0]].map; break;

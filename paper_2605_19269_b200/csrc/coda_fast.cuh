@@ -45,6 +45,7 @@ enum FastFlags : int {
     F_GATHER = 1 << 12,     // TargetGather: target[row] = tile[row, label[row]]
     F_LSE = 1 << 13,        // OnlineLse: (max, scaled sum) pairs per piece (rowpart holds pairs)
     F_ROWDOT = 1 << 14,     // PartialRowDot against a side tile, before RowScale (rowpart = row sums)
+    F_XENT_BWD = 1 << 15,   // CrossEntropyBackward: grad = (exp(x - lse) - onehot) * scale, rowpart = sum x*grad
 };
 
 constexpr int FAST_EPI_WARPS = 8;
@@ -84,6 +85,8 @@ struct FastParams {
     int64_t ld_rowdot_x;
     const int64_t* labels;
     float* target;
+    const float* xent_lse;  // F_XENT_BWD: per-row log-sum-exp
+    float xent_scale;
     // tail-split workspace: f32 partial accumulators [tail][piece < split-1][rank][128][256]
     // and one flag per (tail, piece, rank, epilogue warp), zero between launches
     float* ws;
@@ -490,7 +493,9 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             float pacc = 0.0f, pmax = -INFINITY;
             int ppid = -1;
             int64_t label = -1;
-            if ((FL & F_GATHER) && row_ok) label = __ldg(P.labels + row);
+            if ((FL & (F_GATHER | F_XENT_BWD)) && row_ok) label = __ldg(P.labels + row);
+            float xlse = 0.0f;
+            if ((FL & F_XENT_BWD) && row_ok) xlse = __ldg(P.xent_lse + row);
 
             // CTA-scope wait: the accumulator is read through tcgen05.ld after the fence below;
             // a cluster-scope acquire would emit an L1 invalidate (CCTL.IVALL) on every poll.
@@ -676,6 +681,24 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     pacc = pacc * (pmax == -INFINITY ? 0.0f : __expf(pmax - mn)) + sc * __expf(mc - mn);
                     pmax = mn;
                 }
+                if constexpr ((FL & F_XENT_BWD) != 0) {
+                    float s = 0.0f;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        float pr = __expf(v[i] - xlse);
+                        if (gcol0 + i == label) pr -= 1.0f;
+                        pr *= P.xent_scale;
+                        if (!edge || gcol0 + i < N) s += v[i] * pr;
+                        v[i] = pr;
+                    }
+                    const int pid = __ldg(P.rowpart_map + gcol0);
+                    if (pid != ppid) {
+                        if (ppid >= 0 && row_ok) P.rowpart[row * P.ld_rowpart + ppid] = pacc;
+                        ppid = pid;
+                        pacc = 0.0f;
+                    }
+                    pacc += s;
+                }
                 if (FL & F_SWIGLU) {
 #pragma unroll
                     for (int k = 0; k < 16; ++k) {
@@ -761,7 +784,7 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     else staged_store<TS, 32>(sg, &tma_main, gcol0, m0 + q * 32, v, lane);
                 }
             }
-            if ((FL & (F_SUMSQ | F_SWIGLU_BWD | F_ROWDOT)) && ppid >= 0 && row_ok)
+            if ((FL & (F_SUMSQ | F_SWIGLU_BWD | F_ROWDOT | F_XENT_BWD)) && ppid >= 0 && row_ok)
                 P.rowpart[row * P.ld_rowpart + ppid] = pacc;
             if ((FL & F_LSE) && ppid >= 0 && row_ok) {
                 P.rowpart[row * P.ld_rowpart + 2 * ppid] = pmax;

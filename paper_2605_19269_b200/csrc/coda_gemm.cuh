@@ -38,6 +38,7 @@ enum OpCode : int {
     OP_ROW_VEC_MUL = 1, OP_ROW_SCALE = 2, OP_RESIDUAL_ADD = 3, OP_AUX_TILE_STORE = 4,
     OP_PARTIAL_SUMSQ = 5, OP_PARTIAL_ROWDOT = 6, OP_PARTIAL_COLSUM = 7, OP_ONLINE_LSE = 8,
     OP_TARGET_GATHER = 9, OP_ROPE = 10, OP_SWIGLU = 11, OP_SWIGLU_BWD = 12, OP_RMSNORM_BWD = 13,
+    OP_XENT_BWD = 14,
 };
 
 struct DevStep {
@@ -643,6 +644,27 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
                         }
                         break;
                     }
+                    case OP_XENT_BWD: {
+                        // d loss / d logits = (exp(x - lse) - onehot(label)) * scale; partials of x * grad
+                        float lse_r = 0.0f;
+                        int64_t lab = -1;
+                        if (row_ok) {
+                            lse_r = __ldg(static_cast<const float*>(P.opnd[st.a[0]].ptr) + row);
+                            lab = static_cast<const int64_t*>(P.opnd[st.a[1]].ptr)[row];
+                        }
+                        const float gsc = __int_as_float(st.a[3]);
+                        float x[32];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            float pr = __expf(v[i] - lse_r);
+                            if (gcol0 + i == lab) pr -= 1.0f;
+                            pr *= gsc;
+                            x[i] = v[i] * pr;
+                            v[i] = pr;
+                        }
+                        rowsum_accum<32>(P.store[st.a[2]], rp[st.a[6]], row, row_ok, gcol0, P.N, x);
+                        break;
+                    }
                     default:
                         break;
                     }
@@ -669,6 +691,7 @@ coda_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
                 else if (st.op == OP_PARTIAL_ROWDOT) { si = st.a[6]; slot = st.a[1]; }
                 else if (st.op == OP_ONLINE_LSE) { si = st.a[6]; slot = st.a[0]; pair = true; }
                 else if (st.op == OP_SWIGLU_BWD) { si = st.a[6]; slot = st.a[2]; }
+                else if (st.op == OP_XENT_BWD) { si = st.a[6]; slot = st.a[2]; }
                 if (si >= 0 && si < MAX_ROW_STREAMS) rowpart_flush(P.store[slot], rp[si], row, row_ok, pair);
             }
             acc ^= 1;

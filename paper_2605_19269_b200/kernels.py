@@ -21,6 +21,7 @@ from . import traffic
 from .engine import GemmProblem, KernelResult, block_starts, run_gemm
 from .epilogue import (
     AuxTileStore,
+    CrossEntropyBackward,
     PartialRowDot,
     EpilogueProgram,
     OnlineLse,
@@ -783,6 +784,10 @@ class LmHeadResult:
     inv_rms: Vector
     logits: Optional[DenseMatrix]
     ledger: TrafficLedger
+    # B200 extension: the gained normalized rows K8 consumed (K4's main output) and the
+    # labels, kept for lm_head_backward
+    normed: Optional[DenseMatrix] = None
+    labels: object = None
 
 
 def lm_head_forward(a, b, z, gamma, w_vocab, labels, *, config: PipelineConfig,
@@ -797,4 +802,55 @@ def lm_head_forward(a, b, z, gamma, w_vocab, labels, *, config: PipelineConfig,
     lse = combine_lse(k8.aux["lse"], ledger=ledger, check=False)
     losses, mean = cross_entropy_finalize(k8.aux["target"], lse, ledger=ledger, check_lse=True)
     return LmHeadResult(losses=losses, mean_loss=mean, lse=lse, target=k8.aux["target"],
-                        pre_norm=k4.aux["pre_norm"], inv_rms=r, logits=k8.main, ledger=ledger)
+                        pre_norm=k4.aux["pre_norm"], inv_rms=r, logits=k8.main, ledger=ledger,
+                        normed=k4.main, labels=labels)
+
+
+def gemm_xent_backward(a, b, scale, lse, labels, *, grad_scale=1.0, trans_b=False, tile_shape=TileShape(128, 128),
+                       reduction_tile_n=128, precision=PrecisionMode.EXACT64, ledger=None):
+    """Logit-gradient launch (B200 extension): recompute the K8 logits tile r * (a @ b) and turn
+    it into d loss / d logits = (softmax - onehot) * grad_scale in the epilogue; aux
+    "xent_rowdot" carries the row-blocked <logits, d logits> partials."""
+    return _launch(traffic.K_RMS_XENT, a, b,
+                   [RowScale("scale"), CrossEntropyBackward("lse", "labels", "xent_rowdot", grad_scale)],
+                   {"scale": scale, "lse": lse, "labels": labels}, trans_b=trans_b, tile_shape=tile_shape,
+                   reduction_tile_n=reduction_tile_n, precision=precision, ledger=ledger)
+
+
+@dataclass
+class LmHeadGrads:
+    a: DenseMatrix
+    b: DenseMatrix
+    z: DenseMatrix
+    gamma: Vector
+    w_vocab: DenseMatrix
+    ledger: TrafficLedger
+
+
+def lm_head_backward(res: LmHeadResult, a, b, gamma, w_vocab, *, config: PipelineConfig,
+                     grad_loss: float = 1.0) -> LmHeadGrads:
+    """Backward of lm_head_forward for the mean cross-entropy loss (B200 extension; the
+    reference stops at the loss).  Five GEMM launches + two finalizers:
+
+      1. logit gradient: recompute r * (normed @ w_vocab), (softmax - onehot) * grad_loss / m,
+         with <logits, d logits> partials (the relocated RMSNorm statistic)
+      2. finalize_rowdot -> s
+      3. K9 gemm_rmsnorm_backward: d logits @ w_vocab^T through the normalization -> d h
+         (h = a @ b + z), `normed`, gamma-grad partials (+ reduce_row_partials)
+      4. w_vocab gradient: normed^T @ d logits
+      5-6. d a = d h @ b^T, d b = a^T @ d h; d z = d h.
+    """
+    if res.normed is None or res.labels is None:
+        raise TapeError("lm_head_backward needs the forward's normed rows and labels (lm_head_forward result)")
+    ledger = TrafficLedger()
+    kw = config.launch_kw(ledger)
+    m = res.normed.rows
+    k = gemm_xent_backward(res.normed, w_vocab, res.inv_rms, res.lse, res.labels, grad_scale=grad_loss / m, **kw)
+    s = finalize_rowdot(k.aux["xent_rowdot"], res.normed.cols, ledger=ledger)
+    k9 = gemm_rmsnorm_backward(k.main, w_vocab, res.pre_norm, res.inv_rms, gamma, s, trans_b=True, **kw)
+    gh = k9.main
+    g_gamma = reduce_row_partials(k9.aux["gamma_grad"], ledger=ledger)
+    g_vocab = _launch(traffic.K_GEMM, k9.aux["normed"], k.main, [], {}, trans_a=True, **kw).main
+    g_a = _launch(traffic.K_GEMM, gh, b, [], {}, trans_b=True, **kw).main
+    g_b = _launch(traffic.K_GEMM, a, gh, [], {}, trans_a=True, **kw).main
+    return LmHeadGrads(a=g_a, b=g_b, z=gh, gamma=g_gamma, w_vocab=g_vocab, ledger=ledger)
