@@ -23,6 +23,8 @@ def main():
     rows = list(csv.DictReader(lines[start:]))
     per = {}
     for r in rows:
+        if not r["Metric Name"].startswith("dram__bytes"):
+            continue
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "byte")
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
