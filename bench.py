@@ -566,8 +566,10 @@ def coda_arm(args, rank, world, local_rank):
     if args.graph:
         # capture one whole step (19 launches) once; replaying it removes host launch overhead
         graph = torch.cuda.CUDAGraph()
+        cap_stream = torch.cuda.Stream(device)
+        _native.prepare_stream_workspace(device, cap_stream)   # keep the split-K tail inside the graph
         c0 = _native.launch_count()
-        with torch.cuda.graph(graph):
+        with torch.cuda.graph(graph, stream=cap_stream):
             step()
         per_step_launches = _native.launch_count() - c0
         for _ in range(2):

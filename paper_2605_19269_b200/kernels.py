@@ -696,6 +696,7 @@ def layer_backward(grad_qkv: DenseMatrix, tape: LayerTape, weights: LayerWeights
         res = gemm_wgrad_gain(a, b, weight, gain, precision=prec, tile_shape=config.tile_shape,
                               reduction_tile_n=config.reduction_tile_n, ledger=ledger, out_f32=f32)
         g_gain = finalize_rowdot(res.aux["gain_dot"], 1, ledger=ledger)
+        g_gain.tensor   # no later launch consumes the gain gradient: finalize it now, inside the step
         if wgrad_hook is not None:
             wgrad_hook(name, res.main.tensor)
             wgrad_hook(gname, g_gain.tensor)

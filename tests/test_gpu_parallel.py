@@ -40,7 +40,7 @@ def _inputs():
     return m, d, ffn, w, x, z, gq, gr
 
 
-def _run(rank, world, sl, hook=None):
+def _run(rank, world, sl, hook=None, fold=False):
     import paper_2605_19269_b200 as cd
 
     m, d, ffn, w, x, z, gq, gr = _inputs()
@@ -49,7 +49,7 @@ def _run(rank, world, sl, hook=None):
     weights = cd.LayerWeights(w_out=M(w["w_out"]), gamma_ffn=cd.Vector.from_array(w["gamma_ffn"], P),
                               w_gate_up=M(w["w_gate_up"]), w_down=M(w["w_down"]),
                               gamma_qkv=cd.Vector.from_array(w["gamma_qkv"], P), w_qkv=M(w["w_qkv"]))
-    cfg = cd.PipelineConfig(hidden=d, ffn=ffn, precision=P)
+    cfg = cd.PipelineConfig(hidden=d, ffn=ffn, precision=P, fold_gamma=fold)
     rows = sl.stop - sl.start
     cos, sin = cd.qkv_rope_tables(rows, d, start=sl.start, precision=P)
     fwd = cd.layer_forward(M(x[sl]), M(z[sl]), weights, cos, sin, config=cfg)
@@ -63,7 +63,7 @@ def _run(rank, world, sl, hook=None):
                                               "w_qkv")}
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, reserve=0, fold=False):
     sys.path.insert(0, str(ROOT))
     import torch
     import torch.distributed as dist
@@ -75,24 +75,31 @@ def _worker(rank, world, port, out_dir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     m = _inputs()[0]
     sh = parallel.shard(m, rank, world)
-    hook = parallel.WgradAllReduce(dist, torch.device("cuda", 0))
-    grads = _run(rank, world, slice(sh.start, sh.stop), hook)
+    hook = parallel.WgradAllReduce(dist, torch.device("cuda", 0), reserve_sms=reserve)
+    grads = _run(rank, world, slice(sh.start, sh.stop), hook, fold=fold)
+    from paper_2605_19269_b200 import _native
+
+    assert _native.sm_limit() == 0                   # the cap ends with wait()
     assert set(hook.names) == set(parallel.REDUCED)
     np.savez(Path(out_dir) / f"rank{rank}.npz", **grads)
     dist.destroy_process_group()
 
 
-def test_sharded_fused_backward_matches_full_batch(cuda_ready, tmp_path):
+@pytest.mark.parametrize("reserve,fold", [(0, False), (8, False), (8, True)])
+def test_sharded_fused_backward_matches_full_batch(cuda_ready, tmp_path, reserve, fold):
+    """reserve > 0: the hook caps the GEMMs' SMs while the all-reduce is in flight; fold: the
+    gain-folded block, whose gain gradients come from the weight-gradient epilogue and are
+    all-reduced like the weights."""
     import torch.multiprocessing as mp
 
     from oracle import coda_oracle as O
     from paper_2605_19269_b200 import parallel
 
     world = 2
-    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), reserve, fold), nprocs=world, join=True,
                        start_method="spawn")
     m = _inputs()[0]
-    full = _run(0, 1, slice(0, m))
+    full = _run(0, 1, slice(0, m), fold=fold)
     shards = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
     for name in parallel.REDUCED:
         for s in shards:

@@ -380,3 +380,17 @@ def test_rope_backward_stat_deep_path(cuda_ready):
     assert O.rel_error(gz_b.data, ogz) <= 1e-3
     assert O.rel_error(rd_b.data, ord_) <= 1e-5
     assert list(rd_b.counts) == list(cnt)
+
+
+@pytest.mark.parametrize("fold", [False, True])
+def test_step_leaves_no_deferred_work(cuda_ready, fold):
+    """Every statistic a layer step returns has been computed inside the step: no pending
+    finalizer survives in the tape or the gradients (a deferred finalizer nobody consumes would
+    otherwise run outside a timed region, or never)."""
+    cd = _cd()
+    P = cd.PrecisionMode.SIMBF16
+    case = _layer_case(P, m=256)
+    cfg = cd.PipelineConfig(hidden=case["d"], ffn=case["ffn"], precision=P, fold_gamma=fold)
+    fwd, bwd = _run_layer(case, cfg)
+    vecs = [fwd.tape.inv_rms_a, fwd.tape.inv_rms_b, bwd.gamma_ffn, bwd.gamma_qkv]
+    assert all(getattr(v, "_pending", None) is None for v in vecs)
