@@ -599,6 +599,29 @@ def coda_arm(args, rank, world, local_rank):
     ms_step = ms / args.steps
     value = world * m / (ms_step / 1e3)
 
+    # ---- gamma folded into W (north_star), A/B against the reference schedule: the two step
+    # variants interleaved on this GPU (same power state), median device time of each
+    fold_ab = None
+    if world == 1 and not fp32 and not args.fold_gamma and args.ab_rounds > 0:
+        cfg_f = cd.PipelineConfig(hidden=d, ffn=2 * inter, precision=P, kv_width=kv, fold_gamma=True)
+        variants = {"reference_schedule": cfg, "gamma_folded": cfg_f}
+        times = {k: [] for k in variants}
+        for k, c in variants.items():
+            run_step(cd, c, weights, acts, cos, sin)
+        for _ in range(args.ab_rounds):
+            for k, c in variants.items():
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                run_step(cd, c, weights, acts, cos, sin)
+                a1.record(stream)
+                torch.cuda.synchronize()
+                times[k].append(a0.elapsed_time(a1))
+        med = {k: statistics.median(v) for k, v in times.items()}
+        fold_ab = {"rounds": args.ab_rounds, "ms_reference_schedule": med["reference_schedule"],
+                   "ms_gamma_folded": med["gamma_folded"],
+                   "speedup": med["reference_schedule"] / med["gamma_folded"],
+                   "note": "fold launches (W' = diag(gamma) W) inside every folded step"}
+
     # ---- the other reading of the config text: weak scaling (the config's tokens on EVERY rank),
     # reported beside the strong-scaled headline for N > 1
     weak = None
@@ -790,6 +813,7 @@ def coda_arm(args, rank, world, local_rank):
             "parity": parity,
             "parity_fullsize": fullsize,
             "weak_scaling": weak,
+            "fold_gamma_ab": fold_ab,
             "comm_sms": comm_sms if dist is not None else 0,
             "wgrad_allreduce_dtype": args.wgrad_dtype if dist is not None else None,
             "fold_gamma": bool(args.fold_gamma),
@@ -840,6 +864,8 @@ def main(argv=None):
     ap.add_argument("--tokens", type=int, default=None,
                     help="override the config's token count (per-rank shape proxies at N=1)")
     ap.add_argument("--fold-gamma", action="store_true", help="gains folded into W (north_star variant)")
+    ap.add_argument("--ab-rounds", type=int, default=8,
+                    help="interleaved same-GPU A/B rounds of the reference schedule vs gamma folded (0 = skip)")
     ap.add_argument("--comm-sms", type=int, default=None,
                     help="SMs left to the NCCL all-reduce while it overlaps the backward (default 8 when N > 1)")
     ap.add_argument("--wgrad-dtype", choices=("f32", "bf16"), default="f32",
