@@ -9,14 +9,12 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 import paper_2605_19269_b200 as cd  # noqa: E402
-from paper_2605_19269_b200 import _native  # noqa: E402
 
 P = cd.PrecisionMode.SIMBF16
 dev = torch.device("cuda", 0)
 peak = bench.peaks()["hbm_gbs"]
 out = []
-for ws, m, d in ((1, 16384, 4096), (0, 16384, 4096), (0, 32768, 2048), (0, 8192, 2048)):
-    _native.set_option("rope_ws", ws)
+for m, d in ((16384, 4096), (32768, 2048), (8192, 2048)):
     q = 3 * d
     cos, sin = cd.qkv_rope_tables(m, d, precision=P)
     g = cd.DenseMatrix.from_tensor(torch.randn(m, q, device=dev).to(torch.bfloat16), P)
@@ -34,6 +32,5 @@ for ws, m, d in ((1, 16384, 4096), (0, 16384, 4096), (0, 32768, 2048), (0, 8192,
     ms = e0.elapsed_time(e1) / reps
     nb = q // 128
     byts = 2 * m * q * 2 + 2 * m * (d // 2) * 2 + m * q * 2 + m * nb * 4
-    out.append({"kernel": "ws" if ws else "deep", "m": m, "d": d, "ms": ms, "GB": byts / 1e9, "GBps": byts / ms / 1e6, "frac": byts / ms / 1e6 / peak})
-_native.set_option("rope_ws", 1)
+    out.append({"m": m, "d": d, "ms": ms, "GB": byts / 1e9, "GBps": byts / ms / 1e6, "frac": byts / ms / 1e6 / peak})
 print(json.dumps(out))
