@@ -248,8 +248,7 @@ int coda_scale_rows(const coda_tensor_t* src, const float* scale, coda_tensor_t*
  * the same program: "pdl" 0/1 programmatic dependent launch, "cg" 1/2 CTA-pair
  * mainloop, "generic" 0/1 force the generic epilogue interpreter, "raster" >= 1
  * raster group, "split" 0/1 wave-tail split-K and "split_min_k" the smallest K that
- * is split (splitting changes only the deterministic f32 accumulation order),
- * "rope_ws" 0/1 warp-specialised bulk-copy rope_backward_stat where the layout allows.
+ * is split (splitting changes only the deterministic f32 accumulation order).
  * Process-wide.  Measurement knobs ("ring", "prefetch", "ablate" — the last makes
  * results invalid) exist only in experiment builds (-DCODA_EXPERIMENTS) and return
  * CODA_E_CONFIG from the product library. */

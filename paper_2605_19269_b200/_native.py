@@ -233,7 +233,7 @@ def call(name: str, *args, tag: str | None = None, flops: float = 0.0) -> None:
 
 def set_option(name: str, value: int) -> None:
     """Process-wide engine schedule option ("pdl", "cg", "generic", "raster", "split",
-    "split_min_k", "rope_ws"); see include/coda.h.  Measurement knobs ("ring", "prefetch", "ablate")
+    "split_min_k"); see include/coda.h.  Measurement knobs ("ring", "prefetch", "ablate")
     exist only in experiment builds (libcoda_exp.so, CODA_LIB=exp)."""
     check(load().coda_set_option(name.encode(), int(value)))
 

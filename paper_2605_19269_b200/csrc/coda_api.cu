@@ -217,14 +217,12 @@ struct Options {
     int prefetch = 0;     // [experiments] L2 prefetch distance (k-blocks beyond the smem ring)
     int ablate = 0;       // [experiments] epilogue ablations (results invalid)
     int ring = 0;         // [experiments] operand ring stages in use (0 = the compiled depth)
-    int rope_ws = 1;      // warp-specialised bulk-copy rope_backward_stat where the layout allows
     Options() {
         if (const char* e = getenv("CODA_PDL")) pdl = e[0] != '0';
         if (const char* e = getenv("CODA_CG")) cg = e[0] == '1' ? 1 : 2;
         if (const char* e = getenv("CODA_FORCE_GENERIC")) generic = e[0] && e[0] != '0';
         if (const char* e = getenv("CODA_RASTER_GROUP")) { const int g = atoi(e); if (g > 0) raster = g; }
         if (const char* e = getenv("CODA_SPLIT")) split = e[0] != '0';
-        if (const char* e = getenv("CODA_ROPE_WS")) rope_ws = e[0] != '0';
 #ifdef CODA_EXPERIMENTS
         if (const char* e = getenv("CODA_PREFETCH")) prefetch = atoi(e);
 #endif
@@ -236,7 +234,6 @@ Options& opts() {
 }
 
 bool pdl_enabled() { return opts().pdl != 0; }
-bool ws_rope_enabled() { return opts().rope_ws != 0; }
 
 // Launch with programmatic stream serialization (kernel N+1's prologue overlaps
 // kernel N's tail; every kernel calls griddep_wait() before touching global
@@ -458,7 +455,6 @@ int coda_set_option(const char* name, int value) {
         opts().cg = value;
     } else if (n == "generic") opts().generic = value != 0;
     else if (n == "split") opts().split = value != 0;
-    else if (n == "rope_ws") opts().rope_ws = value != 0;
     else if (n == "split_min_k") {
         if (value < 0) return fail(CODA_E_CONFIG, "split_min_k must be >= 0");
         opts().split_min_k = value;
@@ -906,26 +902,7 @@ int coda_rope_backward_stat_compact(const coda_tensor_t* grad, const coda_tensor
     }
     DeviceGuard dg;
     if ((rc = bind_device(grad->ptr, dg))) return rc;
-    // warp-specialised bulk-copy variant for whole 4096-column segments (default since round 2
-    // at C4); deep-load variant when rows split into whole 6 (or 3) x 2048-column sweeps
-    const bool ws = ws_rope_enabled() && grad->cols % coda::RWS_SEG == 0 && h % coda::RWS_SEG == 0 &&
-                    grad->ld % 8 == 0 && rotated->ld % 8 == 0 && cos_c->ld % 8 == 0 && sin_c->ld % 8 == 0;
-    if (ws) {
-        static std::atomic<uint64_t> configured{0};
-        const size_t smem = coda::rws_smem_bytes();
-        if (first_use_on_device(configured)) {
-            cudaError_t e = cudaFuncSetAttribute(coda::coda_rope_backward_stat_ws_kernel,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(rope ws)");
-        }
-        const int64_t ctas = std::min<int64_t>(grad->rows, (int64_t)num_sms());
-        return launch_pdl(coda::coda_rope_backward_stat_ws_kernel, dim3((unsigned)ctas),
-                          dim3(32 * (coda::RWS_CONSUMERS + 1)), smem, (cudaStream_t)stream, 1,
-                          "coda::coda_rope_backward_stat_ws_kernel",
-                          (const __nv_bfloat16*)grad->ptr, grad->ld, (const __nv_bfloat16*)rotated->ptr, rotated->ld,
-                          (const __nv_bfloat16*)cos_c->ptr, cos_c->ld, (const __nv_bfloat16*)sin_c->ptr, sin_c->ld, h,
-                          grad->rows, grad->cols, (__nv_bfloat16*)grad_z->ptr, grad_z->ld, rowdot, ld_rowdot);
-    }
+    // deep-load variant when rows split into whole 6 (or 3) x 2048-column sweeps (16-B aligned rows)
     const int U = grad->cols % (6 * 2048) == 0 ? 6 : 3;
     const bool deep = grad->cols % (U * 2048) == 0 && grad->ld % 8 == 0 && rotated->ld % 8 == 0 &&
                       grad_z->ld % 8 == 0 && cos_c->ld % 4 == 0 && sin_c->ld % 4 == 0;

@@ -457,119 +457,6 @@ coda_rope_backward_stat_deep_kernel(const __nv_bfloat16* __restrict__ g, int64_t
     }
 }
 
-// Warp-specialised bulk-copy variant (compact tables, n % RWS_SEG == 0, h % RWS_SEG == 0):
-// one producer warp streams whole 4096-column row segments of grad and rotated (8 KiB
-// cp.async.bulk copies, 4 KiB for each compact-table segment) into an RWS_STAGES-deep ring;
-// eight consumer warps compute from shared memory and hand each stage back with one
-// mbarrier arrival per warp (no CTA-wide barrier).  ~168 KiB in flight per SM without any
-// registers held.  Same arithmetic and reduction order as the other compact kernels.
-constexpr int RWS_SEG = 4096;
-constexpr int RWS_STAGES = 7;
-constexpr int RWS_CONSUMERS = 8;                                   // warps
-constexpr int RWS_STAGE_BYTES = 2 * RWS_SEG * 2 + 2 * (RWS_SEG / 2) * 2;   // 24 KiB
-constexpr size_t rws_smem_bytes() { return (size_t)RWS_STAGES * RWS_STAGE_BYTES + 2 * RWS_STAGES * 8 + 64; }
-
-__global__ void __launch_bounds__(32 * (RWS_CONSUMERS + 1), 1)
-coda_rope_backward_stat_ws_kernel(const __nv_bfloat16* __restrict__ g, int64_t ldg,
-                                  const __nv_bfloat16* __restrict__ rot, int64_t ldr,
-                                  const __nv_bfloat16* __restrict__ cs, int64_t ldc,
-                                  const __nv_bfloat16* __restrict__ sn, int64_t lds, int64_t h,
-                                  int64_t m, int64_t n, __nv_bfloat16* __restrict__ gz, int64_t ldz,
-                                  float* __restrict__ rowdot, int64_t ldd) {
-    extern __shared__ __align__(128) uint8_t rws_smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(rws_smem + RWS_STAGES * RWS_STAGE_BYTES);
-    uint64_t* empty = full + RWS_STAGES;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t segs = n / RWS_SEG;
-    const int64_t r0 = m * blockIdx.x / gridDim.x, r1 = m * (blockIdx.x + 1) / gridDim.x;
-    const int64_t nseg = (r1 - r0) * segs;
-    if (threadIdx.x == 0) {
-        for (int st = 0; st < RWS_STAGES; ++st) {
-            mbar_init(&full[st], 1);
-            mbar_init(&empty[st], RWS_CONSUMERS);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-    griddep_wait();
-    griddep_launch_dependents();
-    if (warp == RWS_CONSUMERS) {
-        if (lane == 0) {
-            for (int64_t i = 0; i < nseg; ++i) {
-                const int st = (int)(i % RWS_STAGES);
-                if (i >= RWS_STAGES) mbar_wait(&empty[st], (uint32_t)(((i / RWS_STAGES) - 1) & 1));
-                const int64_t row = r0 + i / segs, c0 = (i % segs) * RWS_SEG;
-                const uint32_t base = smem_u32(rws_smem + st * RWS_STAGE_BYTES);
-                const bool rotates = c0 < 2 * h;
-                mbar_arrive_expect_tx(&full[st], (uint32_t)(rotates ? RWS_STAGE_BYTES : 4 * RWS_SEG));
-                bulk_load_1d(base, g + row * ldg + c0, RWS_SEG * 2, &full[st]);
-                bulk_load_1d(base + 2 * RWS_SEG, rot + row * ldr + c0, RWS_SEG * 2, &full[st]);
-                if (rotates) {
-                    const int64_t p0 = (c0 % h) / 2;
-                    bulk_load_1d(base + 4 * RWS_SEG, cs + row * ldc + p0, RWS_SEG, &full[st]);
-                    bulk_load_1d(base + 5 * RWS_SEG, sn + row * lds + p0, RWS_SEG, &full[st]);
-                }
-            }
-        }
-        return;
-    }
-    constexpr int PER = RWS_SEG / (32 * RWS_CONSUMERS);    // 16 columns per thread per segment
-    for (int64_t i = 0; i < nseg; ++i) {
-        const int st = (int)(i % RWS_STAGES);
-        mbar_wait(&full[st], (uint32_t)((i / RWS_STAGES) & 1));
-        const int64_t row = r0 + i / segs, c0 = (i % segs) * RWS_SEG;
-        const uint8_t* sb = rws_smem + st * RWS_STAGE_BYTES;
-#pragma unroll
-        for (int half = 0; half < PER / 8; ++half) {
-            // thread t of the CTA's 256 consumers covers columns [8 t, 8 t + 8) of each 2048-column half
-            const int col = half * 2048 + (warp * 32 + lane) * 8;
-            float gv[8], rv[8], cv[8], sv[8], zv[8];
-            Io<__nv_bfloat16>::load_shared(reinterpret_cast<const __nv_bfloat16*>(sb) + col, gv);
-            Io<__nv_bfloat16>::load_shared(reinterpret_cast<const __nv_bfloat16*>(sb + 2 * RWS_SEG) + col, rv);
-            if (c0 < 2 * h) {
-                const uint2 uc = *reinterpret_cast<const uint2*>(sb + 4 * RWS_SEG + col);
-                const uint2 us = *reinterpret_cast<const uint2*>(sb + 5 * RWS_SEG + col);
-                const uint32_t wc[2] = {uc.x, uc.y}, ws[2] = {us.x, us.y};
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    const float c_lo = __uint_as_float(wc[j] << 16), c_hi = __uint_as_float(wc[j] & 0xFFFF0000u);
-                    const float s_lo = __uint_as_float(ws[j] << 16), s_hi = __uint_as_float(ws[j] & 0xFFFF0000u);
-                    cv[4 * j] = cv[4 * j + 1] = c_lo;
-                    cv[4 * j + 2] = cv[4 * j + 3] = c_hi;
-                    sv[4 * j] = sv[4 * j + 1] = s_lo;
-                    sv[4 * j + 2] = sv[4 * j + 3] = s_hi;
-                }
-            } else {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    cv[e] = 1.0f;
-                    sv[e] = 0.0f;
-                }
-            }
-            float p = 0.0f;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float g0 = gv[2 * k], g1 = gv[2 * k + 1];
-                zv[2 * k] = g0 * cv[2 * k] + g1 * sv[2 * k];
-                zv[2 * k + 1] = -g0 * sv[2 * k + 1] + g1 * cv[2 * k + 1];
-            }
-#pragma unroll
-            for (int e = 0; e < 8; ++e) p += gv[e] * rv[e];
-            uint4 o;
-            o.x = pack_bf16x2(zv[0], zv[1]);
-            o.y = pack_bf16x2(zv[2], zv[3]);
-            o.z = pack_bf16x2(zv[4], zv[5]);
-            o.w = pack_bf16x2(zv[6], zv[7]);
-            __stcs(reinterpret_cast<uint4*>(gz + row * ldz + c0 + col), o);
-#pragma unroll
-            for (int off = 8; off >= 1; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
-            if ((lane & 15) == 0) rowdot[row * ldd + (c0 + col) / 128] = p;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
-    }
-}
-
 // SIM32 split: x = x0 + x1 + x2 with x0 = bf16(x), x1 = bf16(x - x0), x2 = bf16(x - x0 - x1)
 // (each difference is exact in f32).  dst holds 6 K-blocks of kp, block j = term pattern[j].
 struct SplitPattern { int t[6]; };
