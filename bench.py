@@ -319,11 +319,12 @@ class NullReduce:
 
 
 def fullsize_parity(name: str, variant: str = "plain") -> dict:
-    """Full-size parity of config `name` (c3 / c4) on cuda:0 against the committed oracle fixture
-    tests/golden/fullsize_<name>.npz (made by tests/golden/make_fullsize.py): the same bf16 inputs
-    are regenerated from the fixture's seed, the whole block runs through the public API, and every
-    output is compared by its sketch, norm and sampled rows (oracle/fullsize.compare).  The checker
-    only; nothing here is timed.  variant: plain | f32_hook | fold."""
+    """Full-size parity of config `name` (c3 / c4, or the c5 4-block stack) on cuda:0 against the
+    committed oracle fixture tests/golden/fullsize_<name>.npz (made by
+    tests/golden/make_fullsize.py): the same bf16 inputs are regenerated from the fixture's seed,
+    the whole block (stack) runs through the public API, and every output is compared by its
+    sketch, norm and sampled rows (oracle/fullsize.compare).  The checker only; nothing here is
+    timed.  variant: plain | f32_hook | fold."""
     import numpy as np
     import torch
 
@@ -333,31 +334,52 @@ def fullsize_parity(name: str, variant: str = "plain") -> dict:
 
     z = np.load(ROOT / "tests" / "golden" / f"fullsize_{name}.npz")
     dev = torch.device("cuda", 0)
-    inp = FS.make_inputs(name, seed=int(z["meta_seed"]))
-    m, d = inp["x"].shape
     P = cd.PrecisionMode.SIMBF16
-    w = cd.LayerWeights(w_out=upload_bf16(cd, inp["w_out"], dev), gamma_ffn=upload_vec(cd, inp["gamma_ffn"], dev),
-                        w_gate_up=upload_bf16(cd, inp["w_gate_up"], dev), w_down=upload_bf16(cd, inp["w_down"], dev),
-                        gamma_qkv=upload_vec(cd, inp["gamma_qkv"], dev), w_qkv=upload_bf16(cd, inp["w_qkv"], dev))
-    acts = {k: upload_bf16(cd, inp[k], dev) for k in ("x", "z", "grad_qkv", "grad_residual")}
-    del inp
-    cfg = cd.PipelineConfig(hidden=d, ffn=w.w_gate_up.cols, precision=P, fold_gamma=(variant == "fold"))
+
+    def weights(w):
+        return cd.LayerWeights(w_out=upload_bf16(cd, w["w_out"], dev), gamma_ffn=upload_vec(cd, w["gamma_ffn"], dev),
+                               w_gate_up=upload_bf16(cd, w["w_gate_up"], dev),
+                               w_down=upload_bf16(cd, w["w_down"], dev),
+                               gamma_qkv=upload_vec(cd, w["gamma_qkv"], dev), w_qkv=upload_bf16(cd, w["w_qkv"], dev))
+
+    if name in FS.BLOCKS:
+        ws_np, acts_np = FS.make_stack_inputs(name, seed=int(z["meta_seed"]))
+        ws = [weights(w) for w in ws_np]
+    else:
+        acts_np = FS.make_inputs(name, seed=int(z["meta_seed"]))
+        ws = weights(FS.weights_of(acts_np))
+    acts = {k: upload_bf16(cd, acts_np[k], dev) for k in ("x", "z", "grad_qkv", "grad_residual")}
+    del acts_np
+    m, d = acts["x"].shape
+    f = (ws[0] if isinstance(ws, list) else ws).w_gate_up.cols
+    cfg = cd.PipelineConfig(hidden=d, ffn=f, precision=P, fold_gamma=(variant == "fold"))
     cos, sin = cd.qkv_rope_tables(m, d, precision=P)
     hook = NullReduce() if variant == "f32_hook" else None
-    fwd = cd.layer_forward(acts["x"], acts["z"], w, cos, sin, config=cfg)
-    bwd = cd.layer_backward(acts["grad_qkv"], fwd.tape, w, grad_residual=acts["grad_residual"], config=cfg,
-                            wgrad_hook=hook)
+    got = {}
+    if isinstance(ws, list):
+        from paper_2605_19269_b200 import stack
+
+        fwd = stack.stack_forward(acts["x"], acts["z"], ws, cos, sin, config=cfg)
+        grads = stack.stack_backward(acts["grad_qkv"], acts["grad_residual"], fwd, ws, config=cfg, wgrad_hook=hook)
+        got.update({"qkv": fwd.qkv, "residual": fwd.residual, "x": grads[0].x, "z": grads[0].z})
+        for b, g in enumerate(grads):
+            got.update({f"{k}.{b}": getattr(g, k) for k in FS.WGRADS + FS.GAINS})
+    else:
+        fwd = cd.layer_forward(acts["x"], acts["z"], ws, cos, sin, config=cfg)
+        bwd = cd.layer_backward(acts["grad_qkv"], fwd.tape, ws, grad_residual=acts["grad_residual"], config=cfg,
+                                wgrad_hook=hook)
+        got = {"qkv": fwd.qkv, "residual": fwd.residual}
+        got.update({k: getattr(bwd, k) for k in O.GRAD_KEYS})
     torch.cuda.synchronize()
-    got = {"qkv": fwd.qkv, "residual": fwd.residual}
-    got.update({k: getattr(bwd, k) for k in O.GRAD_KEYS})
     out = {}
-    for k in FS.OUTPUTS:
+    for k in got:
         t = got[k].tensor
-        if k.startswith("gamma"):
+        if f"{k}__full" in z.files:
             out[k] = FS.compare(k, t.double().cpu().numpy(), {"full": z[f"{k}__full"]})
             continue
-        fp = {"sketch": z[f"{k}__sketch"], "rows": z[f"{k}__rows"].astype(np.float64), "row_idx": z[f"{k}__row_idx"]}
-        S = torch.from_numpy(FS.sketch_matrix(k, t.shape[0])).to(dev, torch.float64)
+        fp = {"sketch": z[f"{k}__sketch"].astype(np.float64), "rows": z[f"{k}__rows"].astype(np.float64),
+              "row_idx": z[f"{k}__row_idx"]}
+        S = torch.from_numpy(FS.sketch_matrix(k, t.shape[0], fp["sketch"].shape[0])).to(dev, torch.float64)
         gs = (S @ t.double()).cpu().numpy()
         gr = t[torch.from_numpy(fp["row_idx"]).to(dev)].double().cpu().numpy()
         out[k] = FS.compare(k, None, fp, got_sketch=gs, got_rows=gr)

@@ -39,7 +39,9 @@ CONFIGS = {
     "c1": (128, 256, 1024),
     "c3": (8192, 2048, 8192),
     "c4": (16384, 4096, 14336),
+    "c5": (8192, 4096, 14336),     # per block of the 4-block stack, 8192 tokens per GPU
 }
+BLOCKS = {"c5": 4}
 
 # order of the generated tensors (stream index = position)
 TENSORS = ("w_out", "gamma_ffn", "w_gate_up", "w_down", "gamma_qkv", "w_qkv", "x", "z", "grad_qkv",
@@ -56,7 +58,20 @@ def _normal(seed: int, idx: int, shape, scale: float) -> np.ndarray:
     return a
 
 
-def make_inputs(name: str, seed: int = 0, mode: str = O.SIMBF16, scale: float = 0.02) -> dict:
+def make_stack_inputs(name: str, seed: int = 0, mode: str = O.SIMBF16, scale: float = 0.02) -> tuple[list, dict]:
+    """Per-block weights (stream indices offset by 10 per block) and the stack's activations."""
+    m, d, inter = CONFIGS[name]
+    blocks = BLOCKS.get(name, 1)
+    base = make_inputs(name, seed, mode, scale)
+    ws = [weights_of(base)]
+    for b in range(1, blocks):
+        ws.append(weights_of(make_inputs(name, seed, mode, scale, stream_offset=10 * b, weights_only=True)))
+    acts = {k: base[k] for k in ("x", "z", "grad_qkv", "grad_residual")}
+    return ws, acts
+
+
+def make_inputs(name: str, seed: int = 0, mode: str = O.SIMBF16, scale: float = 0.02, stream_offset: int = 0,
+                weights_only: bool = False) -> dict:
     """Weights N(0, scale^2) with gains 1 + 0.1 N(0,1) (kernels.py:750-767 draw rules; per-tensor
     streams instead of one sequential stream), activations and incoming gradients N(0, 1), all
     quantized to the storage grid of `mode`.  Float32 arrays (every grid value is exact in f32)."""
@@ -66,10 +81,12 @@ def make_inputs(name: str, seed: int = 0, mode: str = O.SIMBF16, scale: float = 
               "w_qkv": (d, 3 * d), "x": (m, d), "z": (m, d), "grad_qkv": (m, 3 * d), "grad_residual": (m, d)}
     out = {}
     for i, key in enumerate(TENSORS):
+        if weights_only and not (key.startswith("w_") or key.startswith("gamma")):
+            continue
         if key.startswith("gamma"):
-            a = 1.0 + 0.1 * _normal(seed, i, shapes[key], 1.0)
+            a = 1.0 + 0.1 * _normal(seed, i + stream_offset, shapes[key], 1.0)
         else:
-            a = _normal(seed, i, shapes[key], scale if key.startswith("w_") else 1.0)
+            a = _normal(seed, i + stream_offset, shapes[key], scale if key.startswith("w_") else 1.0)
         out[key] = _grid(a, mode)
     return out
 
@@ -161,6 +178,50 @@ def run_layer_chunked(inp: dict, mode: str = O.SIMBF16, chunk: int = 1024, eps: 
     return res
 
 
+def run_stack_chunked(ws: list, acts: dict, mode: str = O.SIMBF16, chunk: int = 1024, eps: float = 1e-6,
+                      on_rows=None) -> dict:
+    """The identity-attention block stack (paper_2605_19269_b200/stack.py glue: x_{l+1} = V span
+    of qkv_l, z_{l+1} = residual_l; backward feeds grad_qkv = [0 | 0 | grad_x_l], grad_residual =
+    grad_z_l) token-chunked like run_layer_chunked -- every block is row-local in the same way.
+    Returns per-block reduced gradients under keys "<name>.<block>"; `on_rows` receives the
+    final qkv / residual and block 0's x / z gradients per chunk."""
+    if chunk % 128:
+        raise ValueError("chunk must be a multiple of the 128-row tile")
+    m, d = acts["x"].shape
+    nb = len(ws)
+    acc = {(k, b): None for k in WGRADS for b in range(nb)}
+    gparts = {(k, b): [] for k in GAINS for b in range(nb)}
+    for r0 in range(0, m, chunk):
+        r1 = min(m, r0 + chunk)
+        cos, sin = O.qkv_rope_tables(r1 - r0, d, mode, start=r0)
+        x, z = acts["x"][r0:r1], acts["z"][r0:r1]
+        tapes = []
+        for w in ws:
+            f = O.layer_forward(x, z, w, cos, sin, mode, eps=eps)
+            tapes.append(f)
+            x, z = f["qkv"][:, 2 * d:3 * d], f["residual"]
+        gq, gr = acts["grad_qkv"][r0:r1], acts["grad_residual"][r0:r1]
+        for b in range(nb - 1, -1, -1):
+            parts = _backward_parts(gq, tapes[b], ws[b], mode, gr)
+            for k in WGRADS:
+                p = np.asarray(parts[k], dtype=np.float64)
+                acc[(k, b)] = p if acc[(k, b)] is None else acc[(k, b)] + p
+            for k in GAINS:
+                gparts[(k, b)].append(parts[k])
+            if b > 0:
+                gq = np.concatenate([np.zeros((r1 - r0, 2 * d)), parts["x"]], axis=1)
+                gr = parts["z"]
+        if on_rows is not None:
+            on_rows(r0, r1, {"qkv": tapes[-1]["qkv"], "residual": tapes[-1]["residual"], "x": parts["x"],
+                             "z": parts["z"]})
+    res = {}
+    for (k, b), v in acc.items():
+        res[f"{k}.{b}"] = O.q(v, mode)
+    for (k, b), v in gparts.items():
+        res[f"{k}.{b}"] = O.reduce_row_partials((np.concatenate(v, axis=0), None), mode)
+    return res
+
+
 # ----------------------------------------------------------------------------- sketches
 
 
@@ -168,34 +229,43 @@ SKETCH_ROWS = 6
 SAMPLE_ROWS = 4
 
 
+def _output_index(name: str) -> int:
+    """OUTPUTS index; per-block stack outputs "<name>.<b>" get their own streams."""
+    base, _, blk = name.partition(".")
+    return OUTPUTS.index(base) + (100 * (int(blk) + 1) if blk else 0)
+
+
 def sketch_matrix(name: str, rows: int, k: int = SKETCH_ROWS, seed: int = 1234) -> np.ndarray:
     """Gaussian JL sketch S (k, rows), float32, deterministic per output name."""
-    idx = OUTPUTS.index(name)
+    idx = _output_index(name)
     return np.random.default_rng([seed, 99, idx]).standard_normal((k, rows), dtype=np.float32)
 
 
 def sample_rows(name: str, rows: int, k: int = SAMPLE_ROWS, seed: int = 1234) -> np.ndarray:
     """First, last and k-2 seeded interior rows (sorted)."""
-    idx = OUTPUTS.index(name)
+    idx = _output_index(name)
     inner = np.random.default_rng([seed, 77, idx]).choice(np.arange(1, rows - 1), size=k - 2, replace=False)
     return np.sort(np.concatenate([[0, rows - 1], inner])).astype(np.int64)
 
 
-def fingerprint(name: str, full: np.ndarray) -> dict:
-    """Sketch, Frobenius norm and sampled rows of one full output (vectors are kept whole)."""
+def fingerprint(name: str, full: np.ndarray, k: int = SKETCH_ROWS, rows: int = SAMPLE_ROWS) -> dict:
+    """Sketch (k rows), Frobenius norm and `rows` sampled rows of one full output (vectors are
+    kept whole)."""
     a = np.asarray(full, dtype=np.float64)
     if a.ndim == 1:
         return {"full": a, "norm": float(np.linalg.norm(a))}
-    S = sketch_matrix(name, a.shape[0]).astype(np.float64)
-    ri = sample_rows(name, a.shape[0])
+    S = sketch_matrix(name, a.shape[0], k).astype(np.float64)
+    ri = sample_rows(name, a.shape[0], rows)
     return {"sketch": S @ a, "norm": float(np.linalg.norm(a)), "rows": a[ri], "row_idx": ri}
 
 
 class RowLocalSketcher:
     """Accumulates fingerprints of the row-local outputs chunk by chunk (run_layer_chunked on_rows)."""
 
-    def __init__(self, m: int):
+    def __init__(self, m: int, k: int = SKETCH_ROWS, rows: int = SAMPLE_ROWS):
         self.m = m
+        self.k = k
+        self.rows = rows
         self.acc: dict = {}
 
     def __call__(self, r0: int, r1: int, outs: dict) -> None:
@@ -203,8 +273,9 @@ class RowLocalSketcher:
             a = np.asarray(v, dtype=np.float64)
             st = self.acc.get(k)
             if st is None:
-                st = self.acc[k] = {"sketch": 0.0, "sq": 0.0, "rows": {}, "row_idx": sample_rows(k, self.m)}
-            S = sketch_matrix(k, self.m)[:, r0:r1].astype(np.float64)
+                st = self.acc[k] = {"sketch": 0.0, "sq": 0.0, "rows": {},
+                                    "row_idx": sample_rows(k, self.m, self.rows)}
+            S = sketch_matrix(k, self.m, self.k)[:, r0:r1].astype(np.float64)
             st["sketch"] = st["sketch"] + S @ a
             st["sq"] += float(np.sum(a * a))
             for r in st["row_idx"]:
@@ -231,7 +302,7 @@ def compare(name: str, got: np.ndarray | None, fp: dict, *, got_sketch=None, got
                 "max_ref": float(np.max(np.abs(o))), "exact": True}
     if got_sketch is None:
         g = np.asarray(got, dtype=np.float64)
-        got_sketch = sketch_matrix(name, g.shape[0]).astype(np.float64) @ g
+        got_sketch = sketch_matrix(name, g.shape[0], fp["sketch"].shape[0]).astype(np.float64) @ g
         got_rows = g[fp["row_idx"]]
     rel = float(np.linalg.norm(got_sketch - fp["sketch"]) / np.linalg.norm(fp["sketch"]))
     dif = np.abs(np.asarray(got_rows, dtype=np.float64) - fp["rows"])

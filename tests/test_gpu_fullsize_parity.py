@@ -68,6 +68,16 @@ def test_fullsize_block_vs_oracle(cuda_ready, name):
     _check(run_fullsize(name), f"{name} full block vs chunked fused-order oracle ({time.time() - t0:.0f}s)")
 
 
+def test_fullsize_c5_stack_vs_oracle(cuda_ready):
+    """BASELINE config 5's per-GPU work: the 4-block LLaMA-3-8B stack over 8192 tokens (stack.py
+    glue), every block's weight and gain gradients, block 0's activation gradients and the last
+    block's outputs, against the chunked oracle stack (tests/golden/fullsize_c5.npz)."""
+    if not (GOLDEN / "fullsize_c5.npz").exists():
+        pytest.skip("fixture not generated")
+    t0 = time.time()
+    _check(run_fullsize("c5"), f"c5 4-block stack vs chunked fused-order oracle ({time.time() - t0:.0f}s)")
+
+
 def test_fullsize_c4_f32_wgrads_vs_oracle(cuda_ready):
     """The data-parallel precision path (unrounded f32 weight gradients, one rounding after
     the (here world-size-1) reduction) at full C4 size."""

@@ -78,3 +78,30 @@ def test_fixture_format(name):
         else:
             assert z[f"{k}__sketch"].shape[0] == FS.SKETCH_ROWS
             assert z[f"{k}__rows"].shape[0] == FS.SAMPLE_ROWS
+
+
+def test_stack_chunked_equals_chained_oracle():
+    """The chunked stack driver reproduces the block-by-block chained oracle (stack.py glue)."""
+    FS.CONFIGS["_s"] = (256, 64, 128)
+    FS.BLOCKS["_s"] = 3
+    try:
+        ws, acts = FS.make_stack_inputs("_s", seed=4, scale=0.2)
+    finally:
+        del FS.CONFIGS["_s"], FS.BLOCKS["_s"]
+    mode = O.SIMBF16
+    m, d = acts["x"].shape
+    res = FS.run_stack_chunked(ws, acts, mode, chunk=128)
+    cos, sin = O.qkv_rope_tables(m, d, mode)
+    x, z, tapes = acts["x"], acts["z"], []
+    for w in ws:
+        f = O.layer_forward(x, z, w, cos, sin, mode)
+        tapes.append(f)
+        x, z = f["qkv"][:, 2 * d:], f["residual"]
+    gq, gr = acts["grad_qkv"], acts["grad_residual"]
+    for b in range(len(ws) - 1, -1, -1):
+        g = O.layer_backward(gq, tapes[b], ws[b], mode, grad_residual=gr)
+        for k in FS.GAINS:
+            assert np.array_equal(res[f"{k}.{b}"], g[k]), (k, b)
+        for k in FS.WGRADS:
+            assert O.rel_error(res[f"{k}.{b}"], g[k]) < 2e-3, (k, b)
+        gq, gr = np.concatenate([np.zeros((m, 2 * d)), g["x"]], axis=1), g["z"]
