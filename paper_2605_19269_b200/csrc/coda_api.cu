@@ -217,6 +217,7 @@ struct Options {
     int prefetch = 0;     // [experiments] L2 prefetch distance (k-blocks beyond the smem ring)
     int ablate = 0;       // [experiments] epilogue ablations (results invalid)
     int ring = 0;         // [experiments] operand ring stages in use (0 = the compiled depth)
+    int side_ldg = 0;     // [experiments] residual side loads by global loads (no smem staging)
     Options() {
         if (const char* e = getenv("CODA_PDL")) pdl = e[0] != '0';
         if (const char* e = getenv("CODA_CG")) cg = e[0] == '1' ? 1 : 2;
@@ -465,6 +466,7 @@ int coda_set_option(const char* name, int value) {
 #ifdef CODA_EXPERIMENTS
     else if (n == "ablate") opts().ablate = value;
     else if (n == "ring") opts().ring = value;
+    else if (n == "side_ldg") opts().side_ldg = value;
     else if (n == "prefetch") {
         if (value < 0 || value > 64) return fail(CODA_E_CONFIG, "prefetch distance must be in [0, 64]");
         opts().prefetch = value;
@@ -684,6 +686,7 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         F.acc_in = P.acc_in;
         F.ld_acc = P.ld_acc;
         F.ablate = opts().ablate;
+        F.side_ldg = opts().side_ldg;
         F.rope_sign = 1.0f;
         const void* rope_c = nullptr;
         const void* rope_s = nullptr;

@@ -92,6 +92,7 @@ struct FastParams {
     float* ws;
     int* flags;
     int ablate;   // measurement-only ablations (results invalid): 1 = no side loads, 2 = no TMA stores
+    int side_ldg; // [experiments] residual side operand by L1-bypassing global loads instead of TMA + smem
     // deferred finalizers (coda_step_t.fin_*): the RowScale vector / the RMSNorm-backward
     // stat computed per row from (M, nb) f32 partials and written back by the tn == 0 tiles
     const float* rs_fin;
@@ -394,7 +395,9 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         const int rope_h = (FL & F_ROPE) ? P.rope_h : 0;
         // does the chunk starting at global column x load side operands?  (issue and wait
         // sides evaluate the same predicate)
-        auto side_needed = [&](int x) { return !no_side && !(rope_h > 0 && x >= 2 * rope_h); };
+        constexpr bool RES_ONLY = (FL & F_RESIDUAL) && !(FL & (F_ROPE | F_SWIGLU_BWD | F_RMSBWD | F_ROWDOT));
+        const bool ldg_res = RES_ONLY && P.side_ldg != 0;
+        auto side_needed = [&](int x) { return !no_side && !ldg_res && !(rope_h > 0 && x >= 2 * rope_h); };
         auto side_issue = [&](int tm_, int tn_, int c_) {
             const int y = tm_ * G::TILE_M + rank * BM + q * 32;
             const int x = tn_ * BN + h * 128 + c_ * 32;
@@ -605,8 +608,31 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     for (int i = 0; i < 32; ++i) v[i] *= rsc;
                 }
                 if constexpr ((FL & F_RESIDUAL) != 0) {
+                    if (ldg_res) {
+                        if (row_ok && edge) {
+                            float x[32];
+                            fload<TS, 32>(static_cast<const TS*>(P.residual) + row * P.ld_res, gcol0, N, true, x);
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] += sd0[i];
+                            for (int i = 0; i < 32; ++i) v[i] += x[i];
+                        } else if (row_ok) {
+                            const __nv_bfloat16* rp = static_cast<const __nv_bfloat16*>(P.residual) + row * P.ld_res + gcol0;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                uint4 u;
+                                asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                             : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "l"(rp + 8 * j));
+                                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    v[8 * j + 2 * e] += __uint_as_float(w4[e] << 16);
+                                    v[8 * j + 2 * e + 1] += __uint_as_float(w4[e] & 0xFFFF0000u);
+                                }
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] += sd0[i];
+                    }
                 }
                 if (FL & F_AUX) staged_store<TS, 32>(sg, &tma_aux, gcol0, m0 + q * 32, v, lane);
                 if (FL & F_SUMSQ) {
