@@ -15,9 +15,10 @@ from . import errors
 
 import os
 
-# CODA_LIB=exp selects the experiment build (tools/ only: measurement knobs, see coda.h)
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / (
-    "libcoda_exp.so" if os.environ.get("CODA_LIB") == "exp" else "libcoda.so")
+# CODA_LIB=exp selects the experiment build, CODA_LIB=<variant> an experiment variant
+# (_build.VARIANTS) -- tools/ only: measurement knobs, see coda.h
+_LIB_NAME = os.environ.get("CODA_LIB", "")
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / (f"libcoda_{_LIB_NAME}.so" if _LIB_NAME else "libcoda.so")
 
 # ---- constants mirrored from include/coda.h ----
 BF16, F32, I64, I32 = 0, 1, 2, 3

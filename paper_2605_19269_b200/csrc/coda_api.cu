@@ -217,7 +217,6 @@ struct Options {
     int prefetch = 0;     // [experiments] L2 prefetch distance (k-blocks beyond the smem ring)
     int ablate = 0;       // [experiments] epilogue ablations (results invalid)
     int ring = 0;         // [experiments] operand ring stages in use (0 = the compiled depth)
-    int side_ldg = 0;     // [experiments] residual side loads by global loads (no smem staging)
     Options() {
         if (const char* e = getenv("CODA_PDL")) pdl = e[0] != '0';
         if (const char* e = getenv("CODA_CG")) cg = e[0] == '1' ? 1 : 2;
@@ -466,7 +465,6 @@ int coda_set_option(const char* name, int value) {
 #ifdef CODA_EXPERIMENTS
     else if (n == "ablate") opts().ablate = value;
     else if (n == "ring") opts().ring = value;
-    else if (n == "side_ldg") opts().side_ldg = value;
     else if (n == "prefetch") {
         if (value < 0 || value > 64) return fail(CODA_E_CONFIG, "prefetch distance must be in [0, 64]");
         opts().prefetch = value;
@@ -686,7 +684,6 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         F.acc_in = P.acc_in;
         F.ld_acc = P.ld_acc;
         F.ablate = opts().ablate;
-        F.side_ldg = opts().side_ldg;
         F.rope_sign = 1.0f;
         const void* rope_c = nullptr;
         const void* rope_s = nullptr;
@@ -734,6 +731,8 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
                     rope_c = o[cs.arg[3] - 1].ptr; ld_rope_c = o[cs.arg[3] - 1].ld;
                     rope_s = o[cs.arg[4] - 1].ptr; ld_rope_s = o[cs.arg[4] - 1].ld;
                     F.rope_h = cs.arg[5];
+                    F.rope_cc = rope_c; F.ld_rope_cc = ld_rope_c;
+                    F.rope_sc = rope_s; F.ld_rope_sc = ld_rope_s;
                 }
                 break;
             case CODA_OP_SWIGLU_BWD:

@@ -19,7 +19,10 @@ import os  # noqa: E402
 os.environ.setdefault("CODA_LIB", "exp")   # measurement knobs live in the experiment build
 from paper_2605_19269_b200 import _build  # noqa: E402
 
-_build.build(experiments=True)
+if os.environ["CODA_LIB"] == "exp":
+    _build.build(experiments=True)
+else:
+    _build.build(variant=os.environ["CODA_LIB"])
 
 import bench  # noqa: E402
 import paper_2605_19269_b200 as cd  # noqa: E402
