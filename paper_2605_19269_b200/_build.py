@@ -46,27 +46,8 @@ def needs_build(lib: Path = LIB) -> bool:
     return any(s.exists() and s.stat().st_mtime > t for s in srcs)
 
 
-# experiment variants: name -> extra nvcc defines (built as _lib/libcoda_<name>.so, selected
-# with CODA_LIB=<name>; tools/ only)
-VARIANTS = {"ldg": ["-DCODA_EXPERIMENTS", "-DCODA_SIDE_LDG=1"]}
-
-
-def build(force: bool = False, verbose: bool = False, experiments: bool = False, variant: str = "") -> Path:
-    """Compile libcoda.so (or the experiment build libcoda_exp.so, or a named variant) if missing or stale."""
-    if variant:
-        lib = LIBDIR / f"libcoda_{variant}.so"
-        if not force and not needs_build(lib):
-            return lib
-        LIBDIR.mkdir(parents=True, exist_ok=True)
-        tmp = lib.with_suffix(".so.tmp")
-        cmd = [_nvcc(), *NVCC_FLAGS, *VARIANTS[variant], "-I", str(INCLUDE), "-o", str(tmp),
-               *[str(CSRC / s) for s in SOURCES]]
-        proc = subprocess.run(cmd, capture_output=True, text=True)
-        if proc.returncode != 0:
-            raise RuntimeError(f"nvcc failed ({proc.returncode}):\n{proc.stderr[-4000:]}")
-        (LIBDIR / f"ptxas_{variant}.log").write_text(proc.stderr)
-        os.replace(tmp, lib)
-        return lib
+def build(force: bool = False, verbose: bool = False, experiments: bool = False) -> Path:
+    """Compile libcoda.so (or the experiment build libcoda_exp.so) if missing or stale."""
     lib = LIB_EXP if experiments else LIB
     if not force and not needs_build(lib):
         return lib

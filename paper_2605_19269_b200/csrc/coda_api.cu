@@ -731,8 +731,6 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
                     rope_c = o[cs.arg[3] - 1].ptr; ld_rope_c = o[cs.arg[3] - 1].ld;
                     rope_s = o[cs.arg[4] - 1].ptr; ld_rope_s = o[cs.arg[4] - 1].ld;
                     F.rope_h = cs.arg[5];
-                    F.rope_cc = rope_c; F.ld_rope_cc = ld_rope_c;
-                    F.rope_sc = rope_s; F.ld_rope_sc = ld_rope_s;
                 }
                 break;
             case CODA_OP_SWIGLU_BWD:

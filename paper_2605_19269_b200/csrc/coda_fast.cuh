@@ -107,9 +107,6 @@ struct FastParams {
     // (the q and k spans of the packed projection share angles), columns >= 2h are the
     // identity (cos 1, sin 0) and load nothing.
     int rope_h;
-    const void* rope_cc;   // compact tables (direct side loads)
-    const void* rope_sc;
-    int64_t ld_rope_cc, ld_rope_sc;
 };
 
 // Whole tiles run the program in the unit that computed them; the pieces of a split
@@ -131,17 +128,9 @@ __device__ __forceinline__ int counter_arrive(int* c) {
 constexpr int F_SIDE = F_RESIDUAL | F_ROPE | F_SWIGLU_BWD | F_RMSBWD | F_ROWDOT;
 constexpr int SIDE_BYTES = 4096;
 
-// CODA_SIDE_LDG (experiment builds): side operands by L1-bypassing global loads straight into
-// registers instead of TMA boxes staged through shared memory; frees the side buffers and
-// the ring stage they cost.
-#ifndef CODA_SIDE_LDG
-#define CODA_SIDE_LDG 0
-#endif
-
 template <int CG, int FL>
 struct FastGeom {
-    static constexpr bool SIDE_OPS = (FL & F_SIDE) != 0;             // the program has side operands
-    static constexpr bool SIDE = SIDE_OPS && !CODA_SIDE_LDG;         // ... staged through smem by TMA
+    static constexpr bool SIDE = (FL & F_SIDE) != 0;
     static constexpr int NS = Geom<CG>::NSTAGE - (SIDE ? 1 : 0);
     static constexpr int RING = NS * Geom<CG>::STAGE;
     static constexpr int SIDE_TOTAL = SIDE ? FAST_EPI_WARPS * SIDE_BYTES : 0;
@@ -228,60 +217,6 @@ __device__ __forceinline__ void fload_vec(const float* vp, int64_t c0, int64_t n
         } else {
 #pragma unroll
             for (int e = 0; e < 4; ++e) d[i + e] = (c0 + i + e < n) ? __ldg(vp + c0 + i + e) : 0.0f;
-        }
-    }
-}
-
-// -------------------------------------------------------------- direct side loads
-// One thread's W bf16 values of row `row` from column c0 by L1-bypassing 16-B global loads
-// (zero for !ok rows; masked scalar loads at the right edge).
-template <int W>
-__device__ __forceinline__ void ldg_row(const void* base, int64_t ld, int64_t row, int64_t c0, int64_t ncols,
-                                        bool ok, bool edge, float* d) {
-    if (!ok) {
-#pragma unroll
-        for (int i = 0; i < W; ++i) d[i] = 0.0f;
-        return;
-    }
-    const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(base) + row * ld;
-    if (edge) {
-        fload<__nv_bfloat16, W>(p, c0, ncols, true, d);
-        return;
-    }
-#pragma unroll
-    for (int j = 0; j < W / 8; ++j) {
-        uint4 u;
-        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "l"(p + c0 + 8 * j));
-        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            d[8 * j + 2 * e] = __uint_as_float(w4[e] << 16);
-            d[8 * j + 2 * e + 1] = __uint_as_float(w4[e] & 0xFFFF0000u);
-        }
-    }
-}
-// 16 compact-table angles of a row from pair index pc, each duplicated for its two columns.
-__device__ __forceinline__ void ldg_pairs(const void* base, int64_t ld, int64_t row, int64_t pc, bool ok, float* d) {
-    if (!ok) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) d[i] = 0.0f;
-        return;
-    }
-    const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(base) + row * ld + pc;
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        uint4 u;
-        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "l"(p + 8 * j));
-        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float lo = __uint_as_float(w4[e] << 16), hi = __uint_as_float(w4[e] & 0xFFFF0000u);
-            d[16 * j + 4 * e] = lo;
-            d[16 * j + 4 * e + 1] = lo;
-            d[16 * j + 4 * e + 2] = hi;
-            d[16 * j + 4 * e + 3] = hi;
         }
     }
 }
@@ -603,7 +538,7 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 }
                 // side operands of this chunk: wait for the TMA load, pull this thread's row
                 // into registers, then reuse the buffer for the next chunk's load
-                float sd0[FG::SIDE_OPS ? ((FL & F_SWIGLU_BWD) ? 64 : 32) : 1];
+                float sd0[FG::SIDE ? ((FL & F_SWIGLU_BWD) ? 64 : 32) : 1];
                 float sd1[(FL & (F_ROPE | F_RMSBWD_ACC)) ? 32 : 1];
                 if constexpr (FG::SIDE) {
                     const int xcol = n0 + h * 128 + c * 32;
@@ -646,36 +581,6 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 const int gcol0 = n0 + h * 128 + c * 32;
                 if (gcol0 >= N) continue;   // uniform for the 4 warps of this half
                 const bool edge = gcol0 + 32 > N;
-                if constexpr (FG::SIDE_OPS && CODA_SIDE_LDG) {
-                    if constexpr ((FL & F_ROPE) != 0) {
-                        if (rope_h > 0) {
-                            if (gcol0 < 2 * rope_h) {
-                                const int64_t pc = (gcol0 % rope_h) / 2;
-                                ldg_pairs(P.rope_cc, P.ld_rope_cc, row, pc, row_ok, sd0);
-                                ldg_pairs(P.rope_sc, P.ld_rope_sc, row, pc, row_ok, sd1);
-                            } else {
-#pragma unroll
-                                for (int e = 0; e < 32; ++e) {
-                                    sd0[e] = 1.0f;
-                                    sd1[e] = 0.0f;
-                                }
-                            }
-                        } else {
-                            ldg_row<32>(P.cosp, P.ld_cos, row, gcol0, N, row_ok, edge, sd0);
-                            ldg_row<32>(P.sinp, P.ld_sin, row, gcol0, N, row_ok, edge, sd1);
-                        }
-                    } else if constexpr ((FL & F_SWIGLU_BWD) != 0) {
-                        ldg_row<64>(P.preact2, P.ld_pre2, row, 2 * (int64_t)gcol0, 2 * (int64_t)N, row_ok, edge, sd0);
-                    } else if constexpr ((FL & F_RMSBWD) != 0) {
-                        ldg_row<32>(P.pre, P.ld_pre, row, gcol0, N, row_ok, edge, sd0);
-                        if constexpr ((FL & F_RMSBWD_ACC) != 0)
-                            ldg_row<32>(P.grad_in, P.ld_gin, row, gcol0, N, row_ok, edge, sd1);
-                    } else if constexpr ((FL & F_ROWDOT) != 0) {
-                        ldg_row<32>(P.rowdot_x, P.ld_rowdot_x, row, gcol0, N, row_ok, edge, sd0);
-                    } else {
-                        ldg_row<32>(P.residual, P.ld_res, row, gcol0, N, row_ok, edge, sd0);
-                    }
-                }
                 if (P.acc_in != nullptr) {
                     float x[32];
                     fload<float, 32>(P.acc_in + row * P.ld_acc, gcol0, N, row_ok, x);

@@ -19,10 +19,7 @@ import os  # noqa: E402
 os.environ.setdefault("CODA_LIB", "exp")   # measurement knobs live in the experiment build
 from paper_2605_19269_b200 import _build  # noqa: E402
 
-if os.environ["CODA_LIB"] == "exp":
-    _build.build(experiments=True)
-else:
-    _build.build(variant=os.environ["CODA_LIB"])
+_build.build(experiments=True)
 
 import bench  # noqa: E402
 import paper_2605_19269_b200 as cd  # noqa: E402
