@@ -1,0 +1,47 @@
+"""bench.py's JSON contract on the GPU: one line with every key the driver reads, for the fp32
+parity config (fast) and a reduced-token C4 run (the default workload's code path)."""
+
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+REQUIRED = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+            "vs_baseline", "dtype", "data", "config", "clocks", "e2e", "gpu_launches", "roofline", "cpu_baseline")
+
+
+def _bench(*args):
+    p = subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], capture_output=True, text=True, timeout=600,
+                       cwd=str(ROOT))
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_bench_line_c1(cuda_ready):
+    out = _bench("--config", "c1", "--steps", "3", "--warmup", "3", "--cpu-sample", "128")
+    for k in REQUIRED:
+        assert k in out, k
+    assert out["n_gpus"] == 1 and out["steps"] == 3 and out["warmup"] == 3
+    assert out["dtype"] == "f32" and out["higher_is_better"] is True
+    assert out["gpu_launches"] > 0 and out["value"] > 0
+    assert out["e2e"]["h2d_bytes_per_step"] > 0 and out["e2e"]["d2h_bytes_per_step"] > 0
+    assert out["cpu_baseline"]["kind"] == "port" and out["cpu_baseline"]["cores"] >= 1
+    assert out["parity"]["rel_err_max"] <= 1e-5
+
+
+def test_bench_line_c4_reduced(cuda_ready):
+    out = _bench("--tokens", "2048", "--steps", "3", "--warmup", "3", "--no-cpu", "--ab-rounds", "2")
+    for k in REQUIRED:
+        assert k in out, k
+    assert out["dtype"] == "bf16" and out["config"]["tokens_per_gpu"] == 2048
+    assert out["roofline"]["bound"] == "tensor" and 0 < out["roofline"]["frac"] < 1.5
+    assert out["gpu_launches"] == 3 * 15          # 15 kernels per block step (deferred finalizers)
+    ab = out["fold_gamma_ab"]
+    assert ab["ms_reference_schedule"] > 0 and ab["ms_gamma_folded"] > 0
