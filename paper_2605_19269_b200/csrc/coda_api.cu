@@ -217,6 +217,7 @@ struct Options {
     int prefetch = 0;     // [experiments] L2 prefetch distance (k-blocks beyond the smem ring)
     int ablate = 0;       // [experiments] epilogue ablations (results invalid)
     int ring = 0;         // [experiments] operand ring stages in use (0 = the compiled depth)
+    int rope_u = 0;       // [experiments] rope_backward_stat: 0 auto, 3 / 6 deep-load sweeps, 1 plain compact
     Options() {
         if (const char* e = getenv("CODA_PDL")) pdl = e[0] != '0';
         if (const char* e = getenv("CODA_CG")) cg = e[0] == '1' ? 1 : 2;
@@ -465,6 +466,7 @@ int coda_set_option(const char* name, int value) {
 #ifdef CODA_EXPERIMENTS
     else if (n == "ablate") opts().ablate = value;
     else if (n == "ring") opts().ring = value;
+    else if (n == "rope_u") opts().rope_u = value;
     else if (n == "prefetch") {
         if (value < 0 || value > 64) return fail(CODA_E_CONFIG, "prefetch distance must be in [0, 64]");
         opts().prefetch = value;
@@ -903,9 +905,14 @@ int coda_rope_backward_stat_compact(const coda_tensor_t* grad, const coda_tensor
     DeviceGuard dg;
     if ((rc = bind_device(grad->ptr, dg))) return rc;
     // deep-load variant when rows split into whole 6 (or 3) x 2048-column sweeps (16-B aligned rows)
-    const int U = grad->cols % (6 * 2048) == 0 ? 6 : 3;
-    const bool deep = grad->cols % (U * 2048) == 0 && grad->ld % 8 == 0 && rotated->ld % 8 == 0 &&
-                      grad_z->ld % 8 == 0 && cos_c->ld % 4 == 0 && sin_c->ld % 4 == 0;
+    int U = grad->cols % (6 * 2048) == 0 ? 6 : 3;
+    bool deep = true;
+#ifdef CODA_EXPERIMENTS
+    if (opts().rope_u == 1) deep = false;
+    else if (opts().rope_u == 3 || opts().rope_u == 6) U = opts().rope_u;
+#endif
+    deep = deep && grad->cols % (U * 2048) == 0 && grad->ld % 8 == 0 && rotated->ld % 8 == 0 &&
+           grad_z->ld % 8 == 0 && cos_c->ld % 4 == 0 && sin_c->ld % 4 == 0;
     if (deep) {
         const int64_t items = grad->rows * (grad->cols / (U * 2048));
         const unsigned g = (unsigned)std::min<int64_t>(items, (int64_t)num_sms() * 8);
