@@ -218,6 +218,7 @@ struct Options {
     int ablate = 0;       // [experiments] epilogue ablations (results invalid)
     int ring = 0;         // [experiments] operand ring stages in use (0 = the compiled depth)
     int rope_u = 0;       // [experiments] rope_backward_stat: 0 auto, 3 / 6 deep-load sweeps, 1 plain compact
+    int persist = 1;      // [experiments] 0: one tile per cluster (non-persistent, hardware dispatch order)
     Options() {
         if (const char* e = getenv("CODA_PDL")) pdl = e[0] != '0';
         if (const char* e = getenv("CODA_CG")) cg = e[0] == '1' ? 1 : 2;
@@ -342,7 +343,10 @@ int launch_fast_fl(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorM
             if (e != cudaSuccess) cudaGetLastError();
         }
     }
-    const int grid = (P.mp.nitems < units ? P.mp.nitems : units) * CG;
+    int grid = (P.mp.nitems < units ? P.mp.nitems : units) * CG;
+#ifdef CODA_EXPERIMENTS
+    if (opts().persist == 0 && P.mp.split <= 1) grid = P.mp.nitems * CG;   // one tile per cluster, hardware order
+#endif
     return launch_pdl(kern, dim3((unsigned)grid), dim3(coda::FAST_THREADS), smem, st, CG, "coda_gemm_fast launch",
                       ma, mb, mm, mx, s0, s1, P);
 }
@@ -467,6 +471,7 @@ int coda_set_option(const char* name, int value) {
     else if (n == "ablate") opts().ablate = value;
     else if (n == "ring") opts().ring = value;
     else if (n == "rope_u") opts().rope_u = value;
+    else if (n == "persist") opts().persist = value;
     else if (n == "prefetch") {
         if (value < 0 || value > 64) return fail(CODA_E_CONFIG, "prefetch distance must be in [0, 64]");
         opts().prefetch = value;

@@ -21,6 +21,13 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import pynvml  # noqa: E402
 import torch  # noqa: E402
 
+import os  # noqa: E402
+
+if "--persist" in sys.argv:
+    os.environ.setdefault("CODA_LIB", "exp")   # the persist option lives in the experiment build
+    from paper_2605_19269_b200 import _build  # noqa: E402
+
+    _build.build(experiments=True)
 import paper_2605_19269_b200 as cd  # noqa: E402
 
 SHAPES = {  # name: (m, n, k, trans_a, trans_b) — C4 launch shapes + a square one
@@ -28,12 +35,15 @@ SHAPES = {  # name: (m, n, k, trans_a, trans_b) — C4 launch shapes + a square 
     "K9a 16384x4096x28672 NT": (16384, 4096, 28672, False, True),
     "wgrad_gu 4096x28672x16384 TN": (4096, 28672, 16384, True, False),
     "square 8192^3 NN": (8192, 8192, 8192, False, False),
+    "K10 16384x14336x4096 NT": (16384, 14336, 4096, False, True),
+    "K4a 16384x4096x4096 NN": (16384, 4096, 4096, False, False),
+    "wgrad_down 14336x4096x16384 TN": (14336, 4096, 16384, True, False),
 }
 
 
 class Sampler:
     def __init__(self, h):
-        self.h, self.clk, self.pw = h, [], []
+        self.h, self.clk, self.pw, self.reasons = h, [], [], 0
         self._stop = threading.Event()
 
     def __enter__(self):
@@ -42,6 +52,7 @@ class Sampler:
                 try:
                     self.clk.append(pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM))
                     self.pw.append(pynvml.nvmlDeviceGetPowerUsage(self.h) / 1e3)
+                    self.reasons |= pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 except Exception:
                     pass
                 self._stop.wait(0.01)
@@ -62,7 +73,10 @@ def main():
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--seconds", type=float, default=1.5)
     ap.add_argument("--shape", action="append", help="subset of SHAPES keys (prefix match)")
+    ap.add_argument("--raster", type=int, action="append", help="also run CODA with these raster groups")
+    ap.add_argument("--persist", action="store_true", help="also run CODA non-persistent (experiment build)")
     args = ap.parse_args()
+    from paper_2605_19269_b200 import _native
     pynvml.nvmlInit()
     h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
     P = cd.PrecisionMode.SIMBF16
@@ -86,7 +100,18 @@ def main():
 
         per = {}
         graphs = {}
-        for label, fn in (("coda", coda), ("cublas", cublas)):
+        def coda_np():
+            _native.set_option("persist", 0)
+            cd.run_gemm(prob, a, b)
+            _native.set_option("persist", 1)
+
+        variants = [("coda", coda, 8)] + [(f"coda_r{g}", coda, g) for g in (args.raster or [])] + \
+                   ([("coda_nonpersist", coda_np, 8)] if args.persist else []) + [("cublas", cublas, None)]
+        cap = torch.cuda.Stream()
+        _native.prepare_stream_workspace(torch.device("cuda", torch.cuda.current_device()), cap)
+        for label, fn, raster in variants:
+            if raster is not None:
+                _native.set_option("raster", raster)
             for _ in range(3):
                 fn()
             torch.cuda.synchronize()
@@ -97,11 +122,12 @@ def main():
             torch.cuda.synchronize()
             reps = max(4, int(args.seconds * 1e3 / max(e0.elapsed_time(e1), 1e-3)))
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, stream=cap):     # own split-K workspace inside the graph
                 for _ in range(reps):
                     fn()
             graphs[label] = (g, reps)
             per[label] = []
+        _native.set_option("raster", 8)
         for _ in range(args.rounds):
             for label, (g, reps) in graphs.items():
                 torch.cuda.synchronize()
@@ -115,12 +141,15 @@ def main():
                 per[label].append({"tflops": flops / ms / 1e9, "ms": ms,
                                    "sm_mhz": statistics.median(s.clk) if s.clk else None,
                                    "watts": statistics.median(s.pw) if s.pw else None,
-                                   "j_per_pflop": s.joules / (flops * reps / 1e15)})
+                                   "j_per_pflop": s.joules / (flops * reps / 1e15),
+                                   "reasons": hex(s.reasons)})
         res = {"shape": name}
         for label, runs in per.items():
             best = max(runs, key=lambda r: r["tflops"])
             res[label] = {kk: round(v, 3) if isinstance(v, float) else v for kk, v in best.items()}
-        res["coda/cublas"] = round(res["coda"]["tflops"] / res["cublas"]["tflops"], 4)
+        for label in per:
+            if label.startswith("coda"):
+                res[f"{label}/cublas"] = round(res[label]["tflops"] / res["cublas"]["tflops"], 4)
         print(json.dumps(res), flush=True)
 
 
