@@ -219,6 +219,7 @@ struct Options {
     int ring = 0;         // [experiments] operand ring stages in use (0 = the compiled depth)
     int rope_u = 0;       // [experiments] rope_backward_stat: 0 auto, 3 / 6 deep-load sweeps, 1 plain compact
     int persist = 1;      // [experiments] 0: one tile per cluster (non-persistent, hardware dispatch order)
+    int wave_sync = 0;    // [experiments] soft wave barrier milestone in % of a tile's k-blocks (0 = off)
     Options() {
         if (const char* e = getenv("CODA_PDL")) pdl = e[0] != '0';
         if (const char* e = getenv("CODA_CG")) cg = e[0] == '1' ? 1 : 2;
@@ -472,6 +473,7 @@ int coda_set_option(const char* name, int value) {
     else if (n == "ring") opts().ring = value;
     else if (n == "rope_u") opts().rope_u = value;
     else if (n == "persist") opts().persist = value;
+    else if (n == "wave_sync") opts().wave_sync = value;
     else if (n == "prefetch") {
         if (value < 0 || value > 64) return fail(CODA_E_CONFIG, "prefetch distance must be in [0, 64]");
         opts().prefetch = value;
@@ -678,7 +680,7 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
             const int64_t tile_bytes = (int64_t)cg * coda::BM * coda::BN * 4;
             // every piece dumps its partial tile; one arrival counter per (tail tile, rank, warp)
             while (sp >= 2 && (int64_t)r * sp * tile_bytes > pr->workspace_bytes - (64 << 10)) --sp;
-            if ((int64_t)r * cg * 4 > (64 << 10)) sp = 0;   // one arrival counter per (tail tile, rank)
+            if ((int64_t)r * cg * 4 > (32 << 10)) sp = 0;   // one arrival counter per (tail tile, rank)
             if (sp >= 2) {
                 F.mp.full_tiles = ntiles - r;
                 F.mp.tail = r;
@@ -688,6 +690,16 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
                 F.ws = reinterpret_cast<float*>(static_cast<char*>(pr->workspace) + (64 << 10));
             }
         }
+#ifdef CODA_EXPERIMENTS
+        // soft wave barrier: counters live in the second half of the workspace's counter region
+        if (opts().wave_sync > 0 && pr->workspace && K >= opts().split_min_k) {
+            const int nw = (F.mp.nitems + units - 1) / units;
+            if ((nw + 1) * 4 <= (32 << 10)) {
+                F.mp.wave_pct = opts().wave_sync;
+                F.mp.wave_ctr = reinterpret_cast<int*>(static_cast<char*>(pr->workspace) + (32 << 10));
+            }
+        }
+#endif
         F.acc_in = P.acc_in;
         F.ld_acc = P.ld_acc;
         F.ablate = opts().ablate;

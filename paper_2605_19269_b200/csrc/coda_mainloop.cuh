@@ -50,6 +50,14 @@ struct MainParams {
     int full_tiles, tail, split, nitems;
     int prefetch;               // L2 prefetch distance in k-blocks beyond the load (0 = off)
     int ns;                     // ring stages in use (<= the compiled ring depth; 0 = all)
+#ifdef CODA_EXPERIMENTS
+    // Soft wave barrier (0 = off): a producer arrives on the wave's counter once its tile
+    // has issued `wave_pct` % of its k-blocks, and holds the next wave's first load until
+    // every producer of the launch has arrived (bounded wait: a hint, never a dependency),
+    // keeping the CTAs that share operand panels within a tile of each other in K.
+    int wave_pct;
+    int* wave_ctr;              // [waves] counters + a finish counter, zero between launches
+#endif
 };
 
 // One unit of scheduled work: a whole tile (piece = -1) or piece `piece` of tail tile `tail_idx`.
@@ -125,16 +133,41 @@ __device__ __forceinline__ void producer_loop(const MainParams& mp, const CUtens
         for (int kb = w.kb0 + nst; kb < w.kb1 && kb < w.kb0 + nst + pf; ++kb) boxes(prefetch, m0, nb0, kb);
     }
     __syncwarp();
+#ifdef CODA_EXPERIMENTS
+    const bool wsync = mp.wave_pct > 0 && mp.wave_ctr != nullptr;
+    const int producers = nunits * CG;
+#endif
     for (int i = unit; i < mp.nitems; i += nunits) {
         const Work w = work_item(mp, i);
         const int m0 = w.tm * G::TILE_M + rank * BM;
         const int nb0 = w.tn * BN + rank * G::B_COLS;
+#ifdef CODA_EXPERIMENTS
+        const int wave = (i - unit) / nunits;
+        if (wsync && wave > 0 && w.piece < 0) {
+            // bounded wait for every producer to pass the previous wave's milestone
+            if (elect_one()) {
+                const int* c = mp.wave_ctr + (wave - 1);
+                for (int it = 0; it < 400; ++it) {
+                    int v;
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+                    if (v >= producers) break;
+                    __nanosleep(64);
+                }
+            }
+            __syncwarp();
+        }
+        const int milestone = w.kb0 + (int)((int64_t)(w.kb1 - w.kb0) * mp.wave_pct / 100);
+#endif
         // the item after this one (prefetch target once this item's k-blocks run out)
         const bool has_next = i + nunits < mp.nitems;
         Work wn = w;
         if (pf > 0 && has_next) wn = work_item(mp, i + nunits);
         const int m0n = wn.tm * G::TILE_M + rank * BM, nb0n = wn.tn * BN + rank * G::B_COLS;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
+#ifdef CODA_EXPERIMENTS
+            if (wsync && w.piece < 0 && kb == milestone && elect_one())
+                atomicAdd(mp.wave_ctr + wave, 1);
+#endif
             mbar_wait(&empty[stage], phase ^ 1);
             if (elect_one()) {
                 if (rank == 0) mbar_arrive_expect_tx(&full[stage], G::STAGE * CG);
@@ -158,6 +191,18 @@ __device__ __forceinline__ void producer_loop(const MainParams& mp, const CUtens
             if (++stage == nst) { stage = 0; phase ^= 1; }
         }
     }
+#ifdef CODA_EXPERIMENTS
+    if (wsync && elect_one()) {
+        // the last producer to finish clears the counters for the next launch
+        const int nw = (mp.nitems + nunits - 1) / nunits;
+        int* fin = mp.wave_ctr + nw;
+        if (atomicAdd(fin, 1) == producers - 1) {
+            for (int k = 0; k <= nw; ++k) mp.wave_ctr[k] = 0;
+            __threadfence();
+        }
+    }
+    __syncwarp();
+#endif
 }
 
 // MMA issuer (one warp; for CG = 2 only in the leader CTA; one elected lane issues):

@@ -25,4 +25,8 @@ for _ in range(2):
     _native.set_option("persist", 0)
     cd.run_gemm(prob, a, b)
     _native.set_option("persist", 1)
+    for pct in (50, 90):
+        _native.set_option("wave_sync", pct)
+        cd.run_gemm(prob, a, b)
+        _native.set_option("wave_sync", 0)
 torch.cuda.synchronize()

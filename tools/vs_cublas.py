@@ -23,7 +23,7 @@ import torch  # noqa: E402
 
 import os  # noqa: E402
 
-if "--persist" in sys.argv:
+if "--persist" in sys.argv or "--wave-sync" in sys.argv:
     os.environ.setdefault("CODA_LIB", "exp")   # the persist option lives in the experiment build
     from paper_2605_19269_b200 import _build  # noqa: E402
 
@@ -75,6 +75,7 @@ def main():
     ap.add_argument("--shape", action="append", help="subset of SHAPES keys (prefix match)")
     ap.add_argument("--raster", type=int, action="append", help="also run CODA with these raster groups")
     ap.add_argument("--persist", action="store_true", help="also run CODA non-persistent (experiment build)")
+    ap.add_argument("--wave-sync", type=int, action="append", help="also run CODA with this soft wave barrier %%")
     args = ap.parse_args()
     from paper_2605_19269_b200 import _native
     pynvml.nvmlInit()
@@ -105,8 +106,16 @@ def main():
             cd.run_gemm(prob, a, b)
             _native.set_option("persist", 1)
 
+        def coda_ws(pct):
+            def fn():
+                _native.set_option("wave_sync", pct)
+                cd.run_gemm(prob, a, b)
+                _native.set_option("wave_sync", 0)
+            return fn
+
         variants = [("coda", coda, 8)] + [(f"coda_r{g}", coda, g) for g in (args.raster or [])] + \
-                   ([("coda_nonpersist", coda_np, 8)] if args.persist else []) + [("cublas", cublas, None)]
+                   ([("coda_nonpersist", coda_np, 8)] if args.persist else []) + \
+                   [(f"coda_ws{p}", coda_ws(p), 8) for p in (args.wave_sync or [])] + [("cublas", cublas, None)]
         cap = torch.cuda.Stream()
         _native.prepare_stream_workspace(torch.device("cuda", torch.cuda.current_device()), cap)
         for label, fn, raster in variants:
