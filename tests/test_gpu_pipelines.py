@@ -171,14 +171,17 @@ def _run_layer(case, cfg, hook=None):
     return fwd, bwd
 
 
-def test_folded_layer_vs_oracle(cuda_ready):
+@pytest.mark.parametrize("shape", [(384, 256, 1024), (300, 192, 640)])
+def test_folded_layer_vs_oracle(cuda_ready, shape):
     """The gain-folded block (K4 without RowVecMul / gained store, folded K6/K7/K9, wgrad gain
-    epilogue) matches the reference's unfolded fused-order algorithm within the bf16 bar."""
+    epilogue) matches the reference's unfolded fused-order algorithm within the bf16 bar
+    (aligned shape: specialised kernels; ragged shape: generic interpreter for the gain epilogue)."""
     import torch
 
     cd = _cd()
     P = cd.PrecisionMode.SIMBF16
-    case = _layer_case(P)
+    m, d, ffn = shape
+    case = _layer_case(P, m=m, d=d, ffn=ffn)
     cfg = cd.PipelineConfig(hidden=case["d"], ffn=case["ffn"], precision=P, fold_gamma=True)
     fwd, bwd = _run_layer(case, cfg)
     torch.cuda.synchronize()
@@ -305,8 +308,9 @@ def test_graph_capture_workspace(cuda_ready):
 # ----------------------------------------------------------------------------- deferred finalizers
 
 
+@pytest.mark.parametrize("shape", [(384, 256, 1024), (300, 192, 640)])
 @pytest.mark.parametrize("prec", ["SIMBF16", "SIM32"])
-def test_deferred_finalizers_bit_identical(cuda_ready, prec):
+def test_deferred_finalizers_bit_identical(cuda_ready, prec, shape):
     """finalize_rms / finalize_rowdot folded into the consuming GEMM epilogues (VERDICT r01
     next #6) give the same bits as their standalone kernels, including the tape's r vectors,
     and the SIMBF16 block runs in 15 launches instead of 19."""
@@ -316,7 +320,8 @@ def test_deferred_finalizers_bit_identical(cuda_ready, prec):
     from paper_2605_19269_b200 import _native, reductions
 
     P = getattr(cd.PrecisionMode, prec)
-    case = _layer_case(P, m=384)
+    m, d, ffn = shape
+    case = _layer_case(P, m=m, d=d, ffn=ffn)
     cfg = cd.PipelineConfig(hidden=case["d"], ffn=case["ffn"], precision=P)
 
     def run():
@@ -333,7 +338,7 @@ def test_deferred_finalizers_bit_identical(cuda_ready, prec):
     for i, (x, y) in enumerate(zip(deferred, eager)):
         assert np.array_equal(x, y), i
     assert n_eager - n_def == 4
-    if P is cd.PrecisionMode.SIMBF16:
+    if P is cd.PrecisionMode.SIMBF16 and shape == (384, 256, 1024):
         assert (n_eager, n_def) == (19, 15)
 
 
