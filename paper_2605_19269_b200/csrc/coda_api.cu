@@ -220,6 +220,7 @@ struct Options {
     int rope_u = 0;       // [experiments] rope_backward_stat: 0 auto, 3 / 6 deep-load sweeps, 1 plain compact
     int persist = 1;      // [experiments] 0: one tile per cluster (non-persistent, hardware dispatch order)
     int wave_sync = 0;    // [experiments] soft wave barrier milestone in % of a tile's k-blocks (0 = off)
+    int backoff = 0;      // [experiments] epilogue accumulator-wait sleep (ns)
     Options() {
         if (const char* e = getenv("CODA_PDL")) pdl = e[0] != '0';
         if (const char* e = getenv("CODA_CG")) cg = e[0] == '1' ? 1 : 2;
@@ -474,6 +475,7 @@ int coda_set_option(const char* name, int value) {
     else if (n == "rope_u") opts().rope_u = value;
     else if (n == "persist") opts().persist = value;
     else if (n == "wave_sync") opts().wave_sync = value;
+    else if (n == "backoff") opts().backoff = value;
     else if (n == "prefetch") {
         if (value < 0 || value > 64) return fail(CODA_E_CONFIG, "prefetch distance must be in [0, 64]");
         opts().prefetch = value;
@@ -703,6 +705,7 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         F.acc_in = P.acc_in;
         F.ld_acc = P.ld_acc;
         F.ablate = opts().ablate;
+        F.backoff = opts().backoff;
         F.rope_sign = 1.0f;
         const void* rope_c = nullptr;
         const void* rope_s = nullptr;

@@ -92,6 +92,7 @@ struct FastParams {
     float* ws;
     int* flags;
     int ablate;   // measurement-only ablations (results invalid): 1 = no side loads, 2 = no TMA stores
+    int backoff;  // [experiments] epilogue accumulator wait: ns of sleep between polls (0 = plain try_wait loop)
     // deferred finalizers (coda_step_t.fin_*): the RowScale vector / the RMSNorm-backward
     // stat computed per row from (M, nb) f32 partials and written back by the tn == 0 tiles
     const float* rs_fin;
@@ -500,6 +501,10 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             // CTA-scope wait: the accumulator is read through tcgen05.ld after the fence below;
             // a cluster-scope acquire would emit an L1 invalidate (CCTL.IVALL) on every poll.
             if (!piece) {
+#ifdef CODA_EXPERIMENTS
+                if (P.backoff > 0) mbar_wait_backoff(&tfull[acc], acc_phase, P.backoff);
+                else
+#endif
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
             }

@@ -32,6 +32,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     while (!mbar_try_wait(a, parity)) { }
 }
+// Wait with a sleep between polls (long waits of otherwise idle warps).
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, int ns) {
+    const uint32_t a = smem_u32(bar);
+    while (!mbar_try_wait(a, parity)) __nanosleep(ns);
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
 }

@@ -23,7 +23,7 @@ import torch  # noqa: E402
 
 import os  # noqa: E402
 
-if "--persist" in sys.argv or "--wave-sync" in sys.argv:
+if "--persist" in sys.argv or "--wave-sync" in sys.argv or "--backoff" in sys.argv:
     os.environ.setdefault("CODA_LIB", "exp")   # the persist option lives in the experiment build
     from paper_2605_19269_b200 import _build  # noqa: E402
 
@@ -76,6 +76,7 @@ def main():
     ap.add_argument("--raster", type=int, action="append", help="also run CODA with these raster groups")
     ap.add_argument("--persist", action="store_true", help="also run CODA non-persistent (experiment build)")
     ap.add_argument("--wave-sync", type=int, action="append", help="also run CODA with this soft wave barrier %%")
+    ap.add_argument("--backoff", type=int, action="append", help="also run CODA with this epilogue wait sleep (ns)")
     args = ap.parse_args()
     from paper_2605_19269_b200 import _native
     pynvml.nvmlInit()
@@ -113,7 +114,15 @@ def main():
                 _native.set_option("wave_sync", 0)
             return fn
 
-        variants = [("coda", coda, 8)] + [(f"coda_r{g}", coda, g) for g in (args.raster or [])] + \
+        def coda_bo(ns):
+            def fn():
+                _native.set_option("backoff", ns)
+                cd.run_gemm(prob, a, b)
+                _native.set_option("backoff", 0)
+            return fn
+
+        variants = [(f"coda_bo{n}", coda_bo(n), 8) for n in (args.backoff or [])] + \
+                   [("coda", coda, 8)] + [(f"coda_r{g}", coda, g) for g in (args.raster or [])] + \
                    ([("coda_nonpersist", coda_np, 8)] if args.persist else []) + \
                    [(f"coda_ws{p}", coda_ws(p), 8) for p in (args.wave_sync or [])] + [("cublas", cublas, None)]
         cap = torch.cuda.Stream()
