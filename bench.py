@@ -775,7 +775,10 @@ def coda_arm(args, rank, world, local_rank):
     if prof:
         top = max(prof.values(), key=lambda r: r["total_ms"])
         achieved = top["flops"] / (top["avg_ms"] / 1e3) / 1e12
-        peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+        # the sustained (power-capped) peak when the timed region ran under the power cap,
+        # the burst peak when it did not (short steps, e.g. C3/C1, finish before the cap)
+        capped = "sw_power_cap" in (clocks.summary() or {}).get("reasons", ["sw_power_cap"])
+        peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) if capped else pk["bf16_tflops"]
         traffic, traffic_src = None, None
         tp = ROOT / "profiles" / "traffic.json"
         if tp.exists():
@@ -787,7 +790,8 @@ def coda_arm(args, rank, world, local_rank):
                                                             if meta else "ncu DRAM bytes of a round-1 build"))
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src, "kernel": top["name"],
-                    "peak_kind": "measured sustained bf16 (MEASURED_PEAKS.json)",
+                    "peak_kind": ("measured sustained bf16 (MEASURED_PEAKS.json; sw_power_cap seen in the timed region)"
+                                  if capped else "measured burst bf16 (MEASURED_PEAKS.json; no power cap in the timed region)"),
                     "share_of_step": top["total_ms"] / sum(r["total_ms"] for r in prof.values())}
     total_flops = flops_per_token(d, inter, kv) * m * nblocks
     block_tflops = total_flops / (ms_step / 1e3) / 1e12

@@ -316,15 +316,20 @@ def launch_count() -> int:
     return _launches
 
 
-def profile_launches(fn, reps: int = 2) -> dict:
+def profile_launches(fn, reps: int = 2, lead: int = 1) -> dict:
     """Run fn() `reps` times recording CUDA events around every launch.
 
     Returns {tag: {name, count, avg_ms, total_ms, flops}} (flops per launch).
-    Events are recorded on the launching (current) stream.
+    Events are recorded on the launching (current) stream.  `lead` unrecorded calls
+    are enqueued first, without a sync, so the recorded launches sit behind queued
+    device work: on an idle GPU the first launch's interval would also contain the
+    host time between its start event and the kernel (validation, allocation).
     """
     import torch
 
     global _profile
+    for _ in range(lead):
+        fn()
     _profile = []
     try:
         for _ in range(reps):
