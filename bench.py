@@ -90,7 +90,12 @@ class NvmlClockSampler:
                 try:
                     sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
                     reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                    self.samples.append((sm, reasons))
+                    try:
+                        mem = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_MEM)
+                        power = nv.nvmlDeviceGetPowerUsage(self.h) / 1e3
+                    except Exception:
+                        mem = power = None
+                    self.samples.append((sm, reasons, mem, power))
                 except Exception:
                     pass
                 self._stop.wait(0.02)
@@ -112,9 +117,16 @@ class NvmlClockSampler:
             mx = None
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["unsampled"], "samples": 0}
-        reasons = sorted({name for _, r in self.samples for name, bit in self.BITS.items() if r & bit})
-        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.samples), "sm_mhz_min": min(s for s, _ in self.samples)}
+        reasons = sorted({name for _, r, *_ in self.samples for name, bit in self.BITS.items() if r & bit})
+        out = {"sm_mhz": statistics.median(s[0] for s in self.samples), "sm_max_mhz": mx, "reasons": reasons,
+               "samples": len(self.samples), "sm_mhz_min": min(s[0] for s in self.samples)}
+        mem = [s[2] for s in self.samples if s[2] is not None]
+        power = [s[3] for s in self.samples if s[3] is not None]
+        if mem:
+            out["mem_mhz"] = statistics.median(mem)
+        if power:
+            out["power_w"] = round(statistics.median(power), 1)
+        return out
 
 
 def clock_sampler(index: int):
