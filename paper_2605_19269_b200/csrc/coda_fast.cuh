@@ -87,8 +87,8 @@ struct FastParams {
     float* target;
     const float* xent_lse;  // F_XENT_BWD: per-row log-sum-exp
     float xent_scale;
-    // tail-split workspace: f32 partial accumulators [tail][piece < split-1][rank][128][256]
-    // and one flag per (tail, piece, rank, epilogue warp), zero between launches
+    // tail-split workspace: f32 partial accumulators [tail tile][piece < split][rank][128 x 256]
+    // and one arrival counter per (tail tile, rank), zero between launches
     float* ws;
     int* flags;
     int ablate;   // measurement-only ablations (results invalid): 1 = no side loads, 2 = no TMA stores
@@ -434,7 +434,9 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             // launch needs no co-residency of its clusters.  The decision is per CTA (not per
             // warp) because the program's column reductions synchronise the warps of a half.
             const bool piece = w.piece >= 0;
-            const int64_t ws_region = (int64_t)(q * 32 + lane) * BN + h * 128;
+            // dump layout of a warp's 32 x 128 region: float4 k of lane l at (k * 32 + l) * 4,
+            // so every warp-wide store / load covers 512 contiguous bytes (4 full lines)
+            const int64_t ws_region = (int64_t)(q * 2 + h) * (32 * 128) + lane * 4;
             if (piece) {
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
@@ -446,7 +448,8 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     tmem_ld32(tb + c * 32, v);
 #pragma unroll
                     for (int e = 0; e < 32; e += 4)
-                        __stcg(reinterpret_cast<float4*>(dst + c * 32 + e), make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]));
+                        __stcg(reinterpret_cast<float4*>(dst + (c * 8 + e / 4) * 128),
+                               make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]));
                 }
                 tc_fence_before();
                 __threadfence();
@@ -530,10 +533,10 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     for (int e = 0; e < 32; ++e) v[e] = 0.0f;
                     for (int pc = 0; pc < split; ++pc) {
                         const float* src = P.ws + ((int64_t)(w.tail_idx * split + pc) * CG + rank) * (BM * BN) +
-                                           ws_region + c * 32;
+                                           ws_region + c * 8 * 128;
 #pragma unroll
                         for (int e = 0; e < 32; e += 4) {
-                            const float4 u = __ldcg(reinterpret_cast<const float4*>(src + e));
+                            const float4 u = __ldcg(reinterpret_cast<const float4*>(src + (e / 4) * 128));
                             v[e] += u.x;
                             v[e + 1] += u.y;
                             v[e + 2] += u.z;

@@ -215,16 +215,13 @@ np.savez(sys.argv[1], *outs)
             assert O.rel_error(x, y) < 1e-5 if np.linalg.norm(y) else np.all(x == y)
 
 
-def test_tail_split_matches_unsplit(cuda_ready):
-    """Wave-tail split-K (partial last wave folded in fixed order) equals the unsplit launch."""
+def _split_programs(cd, m, k, n, seed=8):
+    """Every fast-path program family (K4, K6, K7, K9 + grad_in, K10, K8, a TN plain GEMM) on
+    one set of seeded operands; returns a function that runs them and returns the outputs."""
     import torch
 
-    cd = _mods()
-    from paper_2605_19269_b200 import _native
-
-    rng = np.random.default_rng(8)
+    rng = np.random.default_rng(seed)
     P = cd.PrecisionMode.SIMBF16
-    m, k, n = 1000, 2048, 1536          # 4 x 6 = 24 pair tiles < 74 units -> every tile split
     M = lambda a: cd.DenseMatrix.from_array(a, P)  # noqa: E731
     a, b = M(rng.standard_normal((m, k)) / 40), M(rng.standard_normal((k, n)) / 40)
     bt = M(rng.standard_normal((n, k)) / 40)
@@ -255,6 +252,15 @@ def test_tail_split_matches_unsplit(cuda_ready):
         torch.cuda.synchronize()
         return outs
 
+    return run
+
+
+def test_tail_split_matches_unsplit(cuda_ready):
+    """Wave-tail split-K (partial last wave folded in fixed order) equals the unsplit launch."""
+    cd = _mods()
+    from paper_2605_19269_b200 import _native
+
+    run = _split_programs(cd, 1000, 2048, 1536)    # 4 x 6 = 24 pair tiles < 74 units -> every tile split
     try:
         _native.set_option("split_min_k", 0)     # split every eligible launch of this test
         _native.set_option("split", 0)

@@ -38,8 +38,11 @@ def main():
     ap.add_argument("--config", default="c4", choices=tuple(bench.CONFIGS))
     ap.add_argument("--rounds", type=int, default=12)
     ap.add_argument("--variant", action="append", required=True, help="e.g. cg=2,pdl=1")
+    ap.add_argument("--tokens", type=int, default=0, help="override the config's token count (per-rank shape proxies)")
     args = ap.parse_args()
     d, inter, m, label = bench.CONFIGS[args.config]
+    if args.tokens:
+        m, label = args.tokens, f"{label} at {args.tokens} tokens"
     dev = torch.device("cuda", 0)
     cfg = cd.PipelineConfig(hidden=d, ffn=2 * inter, precision=cd.PrecisionMode.SIMBF16)
     weights, acts, cos, sin = bench.make_workload(cd, d, inter, m, 0, dev, blocks=bench.BLOCKS.get(args.config, 1))
@@ -55,9 +58,11 @@ def main():
         for _ in range(3):
             run(i)
     torch.cuda.synchronize()
-    for _ in range(args.rounds):
-        for i in range(len(variants)):
+    nv = len(variants)
+    for rnd in range(args.rounds):
+        for i in [(rnd + j) % nv for j in range(nv)]:     # rotated order
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            run(i)          # untimed lead step: the timed one starts behind queued device work
             e0.record()
             run(i)
             e1.record()

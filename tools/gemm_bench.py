@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--shape", action="append", required=True, help="m,n,k[,ta,tb]")
     ap.add_argument("--variant", action="append", required=True)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--inner", type=int, default=10, help="launches per captured graph (one timed replay)")
     ap.add_argument("--pad", type=int, default=0, help="extra elements per row of A and B (row-pitch experiment)")
     args = ap.parse_args()
     P = cd.PrecisionMode.SIMBF16
@@ -53,19 +54,22 @@ def main():
                 cd.run_gemm(prob, a, b)
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                for _ in range(10):
+            cap = torch.cuda.Stream()
+            _native.prepare_stream_workspace(torch.device("cuda", 0), cap)   # split-K tail inside the graph
+            with torch.cuda.graph(g, stream=cap):
+                for _ in range(args.inner):
                     cd.run_gemm(prob, a, b)
             graphs.append((v, g))
         times = {v: [] for v, _ in graphs}
-        for _ in range(args.reps):
-            for v, g in graphs:
+        for rep in range(args.reps):
+            # rotate the variant order every rep: no variant always runs first after the sync
+            for v, g in graphs[rep % len(graphs):] + graphs[:rep % len(graphs)]:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 g.replay()
                 e1.record()
                 torch.cuda.synchronize()
-                times[v].append(e0.elapsed_time(e1) / 10)
+                times[v].append(e0.elapsed_time(e1) / args.inner)
         res = {v: statistics.median(t) for v, t in times.items()}
         print(json.dumps({"shape": spec, **{v: {"ms": t, "tflops": 2 * m * n * k / t / 1e9} for v, t in res.items()}}),
               flush=True)
