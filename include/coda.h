@@ -66,6 +66,7 @@ extern "C" {
 #define CODA_MAX_OPERANDS    16
 #define CODA_MAX_STORES      16
 #define CODA_MAX_ROW_STREAMS  4
+#define CODA_MAX_PEERS        8
 #define CODA_FIN_RMS          1   /* coda_step_t.fin_kind: finalize_rms    reductions.py:64-80 */
 #define CODA_FIN_ROWDOT       2   /*                       finalize_rowdot reductions.py:83-98 */   /* row-directed partial streams (sum / row-dot / LSE) per program */
 
@@ -243,6 +244,35 @@ int coda_convert_f32_bf16(const coda_tensor_t* src, coda_tensor_t* dst, void* st
  * producing launch (gemm_residual_partial_rms, kernels.py:325-360) no longer
  * multiplies by gamma nor stores the gained copy of its output. */
 int coda_scale_rows(const coda_tensor_t* src, const float* scale, coda_tensor_t* dst, void* stream);
+
+/* Data-parallel weight gradient with its cross-rank sum fused into the GEMM epilogue
+ * (B200 extension; replaces "wgrad GEMM, then NCCL all-reduce" for the weight gradients
+ * the token-sharded block sums over ranks, reference kernels.py:936-1001).  Every rank
+ * launches the same problem (its own token shard as K).  Output tile t is owned by rank
+ * t % world: each rank dumps its f32 partial of t into slots[owner] (peer memory, e.g.
+ * CUDA IPC over NVLink), then arrives on counters[owner]; the last of the world arrivals
+ * sums the partials in rank order (bitwise deterministic, independent of arrival order),
+ * rounds to bf16 once -- the reference's single store rounding, engine.py:443-447 -- and
+ * writes the tile into out[r] of every rank.  Nothing waits on another rank, so ranks need
+ * no co-scheduling; out[] is complete on all ranks once every rank's launch has finished
+ * (the caller's cross-rank barrier).  Counters must be zero before the first launch and
+ * are left zero; slot and counter buffers may be reused by the next launch only after
+ * that barrier.  Sizes per rank: coda_peer_reduce_sizes. */
+typedef struct {
+    int32_t  world;                      /* ranks, 1 .. CODA_MAX_PEERS */
+    int32_t  rank;                       /* this rank */
+    void*    slots[CODA_MAX_PEERS];      /* per rank: f32 landing buffer (slot_bytes) */
+    int32_t* counters[CODA_MAX_PEERS];   /* per rank: arrival counters (counter_bytes) */
+    void*    out[CODA_MAX_PEERS];        /* per rank: bf16 (m, n) result, row stride ld_out */
+    int64_t  ld_out;
+    int64_t  slot_bytes;                 /* size of every rank's slots / counters buffer */
+    int64_t  counter_bytes;
+} coda_peer_reduce_t;
+
+int coda_peer_reduce_sizes(int64_t m, int64_t n, int32_t world, int64_t* slot_bytes, int64_t* counter_bytes);
+
+int coda_gemm_peer_reduce(const coda_problem_t* problem, const coda_tensor_t* a, const coda_tensor_t* b,
+                          const coda_peer_reduce_t* peer, void* stream);
 
 /* Engine schedule options (defaults from the environment); each variant computes
  * the same program: "pdl" 0/1 programmatic dependent launch, "cg" 1/2 CTA-pair

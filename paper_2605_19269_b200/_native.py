@@ -46,6 +46,7 @@ MAX_STEPS = 16
 MAX_OPERANDS = 16
 MAX_STORES = 16
 MAX_ROW_STREAMS = 4
+MAX_PEERS = 8
 
 # GPU tile geometry of the persistent kernel (csrc/coda_gemm.cuh)
 GPU_TILE_M = 128
@@ -65,6 +66,8 @@ EXPORTS = (
     "coda_split_operand",
     "coda_convert_f32_bf16",
     "coda_scale_rows",
+    "coda_peer_reduce_sizes",
+    "coda_gemm_peer_reduce",
     "coda_num_sms",
     "coda_set_option",
     "coda_version",
@@ -121,6 +124,21 @@ class Store(ctypes.Structure):
     ]
 
 
+class PeerReduce(ctypes.Structure):
+    """coda_peer_reduce_t: the cross-rank weight-gradient sum fused into the GEMM epilogue."""
+
+    _fields_ = [
+        ("world", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("slots", ctypes.c_void_p * MAX_PEERS),
+        ("counters", ctypes.c_void_p * MAX_PEERS),
+        ("out", ctypes.c_void_p * MAX_PEERS),
+        ("ld_out", ctypes.c_int64),
+        ("slot_bytes", ctypes.c_int64),
+        ("counter_bytes", ctypes.c_int64),
+    ]
+
+
 class NativeUnavailable(errors.TileFuseError):
     """The CUDA library could not be loaded (no silent CPU fallback exists)."""
 
@@ -158,6 +176,8 @@ def _declare(lib) -> None:
     lib.coda_split_operand.argtypes = [P(Tensor), i32, i64, P(ctypes.c_int32), P(Tensor), vp]
     lib.coda_convert_f32_bf16.argtypes = [P(Tensor), P(Tensor), vp]
     lib.coda_scale_rows.argtypes = [P(Tensor), vp, P(Tensor), vp]
+    lib.coda_peer_reduce_sizes.argtypes = [i64, i64, ctypes.c_int32, P(i64), P(i64)]
+    lib.coda_gemm_peer_reduce.argtypes = [P(Problem), P(Tensor), P(Tensor), P(PeerReduce), vp]
     lib.coda_num_sms.argtypes = []
     lib.coda_set_option.argtypes = [ctypes.c_char_p, i32]
     lib.coda_version.argtypes = []
@@ -374,3 +394,11 @@ def dtype_of(t) -> int:
     if t.dtype not in m:
         raise errors.BindingError(f"unsupported device dtype {t.dtype}")
     return m[t.dtype]
+
+
+def peer_reduce_sizes(m: int, n: int, world: int) -> tuple[int, int]:
+    """Bytes of the f32 landing buffer and of the counter buffer every rank of a
+    `world`-rank peer-reduced (m, n) weight gradient needs (coda_peer_reduce_sizes)."""
+    sb, cb = ctypes.c_int64(0), ctypes.c_int64(0)
+    check(load().coda_peer_reduce_sizes(int(m), int(n), int(world), ctypes.byref(sb), ctypes.byref(cb)))
+    return int(sb.value), int(cb.value)

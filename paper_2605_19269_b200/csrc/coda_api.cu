@@ -293,6 +293,7 @@ using coda::F_AUX;
 using coda::F_GATHER;
 using coda::F_LSE;
 using coda::F_OUT_F32;
+using coda::F_PEER;
 using coda::F_RESIDUAL;
 using coda::F_RMSBWD;
 using coda::F_RMSBWD_ACC;
@@ -328,7 +329,8 @@ using coda::F_XENT_BWD;
     X(F_ROWSCALE | F_GATHER | F_LSE | F_STORE_MAIN)                   \
     X(F_ROWDOT | F_ROWSCALE | F_STORE_MAIN)                           \
     X(F_ROWSCALE | F_XENT_BWD | F_STORE_MAIN)                         \
-    X(F_ROWDOT | F_ROWSCALE | F_STORE_MAIN | F_OUT_F32)
+    X(F_ROWDOT | F_ROWSCALE | F_STORE_MAIN | F_OUT_F32)              \
+    X(F_PEER)
 
 template <int FL, int CG>
 int launch_fast_fl(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mm, const CUtensorMap& mx,
@@ -488,10 +490,65 @@ int coda_set_option(const char* name, int value) {
     return CODA_OK;
 }
 
+namespace {
+int gemm_impl(const coda_problem_t* pr, const coda_tensor_t* a, const coda_tensor_t* b, const coda_step_t* steps,
+              int nsteps, const coda_tensor_t* operands, int noperands, const coda_store_t* stores, int nstores,
+              const coda_tensor_t* main_out, const coda_tensor_t* acc_in, void* stream,
+              const coda_peer_reduce_t* peer);
+
+int64_t peer_tiles(int64_t m, int64_t n) {
+    const int64_t tile_m = (int64_t)coda::BM * fast_cg();
+    return ((m + tile_m - 1) / tile_m) * ((n + coda::BN - 1) / coda::BN);
+}
+}  // namespace
+
+int coda_peer_reduce_sizes(int64_t m, int64_t n, int32_t world, int64_t* slot_bytes, int64_t* counter_bytes) {
+    if (m <= 0 || n <= 0) return fail(CODA_E_DIMENSION, "peer reduce: dims must be positive");
+    if (world < 1 || world > CODA_MAX_PEERS) return fail(CODA_E_CONFIG, "peer reduce: world must be 1..%d", CODA_MAX_PEERS);
+    if (!slot_bytes || !counter_bytes) return fail(CODA_E_BINDING, "peer reduce: null size outputs");
+    const int64_t owned = (peer_tiles(m, n) + world - 1) / world;
+    *slot_bytes = owned * world * fast_cg() * coda::BM * coda::BN * 4;
+    *counter_bytes = owned * fast_cg() * 4;
+    return 0;
+}
+
+int coda_gemm_peer_reduce(const coda_problem_t* problem, const coda_tensor_t* a, const coda_tensor_t* b,
+                          const coda_peer_reduce_t* peer, void* stream) {
+    if (!problem || !peer) return fail(CODA_E_BINDING, "null problem or peer descriptor");
+    if (problem->storage != CODA_BF16) return fail(CODA_E_CONFIG, "peer reduce: storage must be bf16");
+    if (opts().generic) return fail(CODA_E_CONFIG, "peer reduce runs on the specialised kernels only");
+    int64_t need_slots = 0, need_ctr = 0;
+    int rc = coda_peer_reduce_sizes(problem->m, problem->n, peer->world, &need_slots, &need_ctr);
+    if (rc) return rc;
+    if (peer->rank < 0 || peer->rank >= peer->world) return fail(CODA_E_CONFIG, "peer reduce: bad rank %d", peer->rank);
+    if (peer->slot_bytes < need_slots || peer->counter_bytes < need_ctr)
+        return fail(CODA_E_BINDING, "peer reduce: buffers too small (%lld / %lld bytes, need %lld / %lld)",
+                    (long long)peer->slot_bytes, (long long)peer->counter_bytes, (long long)need_slots,
+                    (long long)need_ctr);
+    if (peer->ld_out < problem->n) return fail(CODA_E_DIMENSION, "peer reduce: ld_out < n");
+    for (int r = 0; r < peer->world; ++r)
+        if (!peer->slots[r] || !peer->counters[r] || !peer->out[r])
+            return fail(CODA_E_BINDING, "peer reduce: null buffer for rank %d", r);
+    coda_problem_t pr = *problem;
+    pr.store_main = 0;
+    pr.out_dtype = CODA_BF16;
+    pr.workspace = nullptr;      // no wave-tail split: every tile is one rank's partial
+    pr.workspace_bytes = 0;
+    return gemm_impl(&pr, a, b, nullptr, 0, nullptr, 0, nullptr, 0, nullptr, nullptr, stream, peer);
+}
+
 int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const coda_tensor_t* b,
                        const coda_step_t* steps, int nsteps, const coda_tensor_t* operands, int noperands,
                        const coda_store_t* stores, int nstores, const coda_tensor_t* main_out,
                        const coda_tensor_t* acc_in, void* stream) {
+    return gemm_impl(pr, a, b, steps, nsteps, operands, noperands, stores, nstores, main_out, acc_in, stream, nullptr);
+}
+
+namespace {
+int gemm_impl(const coda_problem_t* pr, const coda_tensor_t* a, const coda_tensor_t* b, const coda_step_t* steps,
+              int nsteps, const coda_tensor_t* operands, int noperands, const coda_store_t* stores, int nstores,
+              const coda_tensor_t* main_out, const coda_tensor_t* acc_in, void* stream,
+              const coda_peer_reduce_t* peer) {
     if (!pr) return fail(CODA_E_BINDING, "null problem");
     const int64_t M = pr->m, N = pr->n, K = pr->k;
     if (M <= 0 || N <= 0 || K <= 0) return fail(CODA_E_DIMENSION, "problem dims must be positive");
@@ -659,7 +716,7 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
 
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
 
-    const int fl = match_fast(pr, steps, nsteps, stores);
+    const int fl = peer ? (int)coda::F_PEER : match_fast(pr, steps, nsteps, stores);
     if (fl >= 0) {
         const int cg = fast_cg();
         coda::FastParams F;
@@ -674,7 +731,7 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
         const int r = units > 0 ? ntiles % units : 0;
         // only long-K launches: the dump / fixed-order fold costs ~10-20 us, which a split of a
         // short mainloop cannot repay (tools/gemm_bench.py: +9 % at K=16384, -8 % at K=4096)
-        if (opts().split && r > 0 && K >= opts().split_min_k && pr->workspace &&
+        if (!peer && opts().split && r > 0 && K >= opts().split_min_k && pr->workspace &&
             pr->workspace_bytes > (64 << 10)) {
             int sp = units / r;
             if (sp > P.nk / 4) sp = P.nk / 4;
@@ -702,6 +759,16 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
             }
         }
 #endif
+        if (peer) {
+            F.peer_world = peer->world;
+            F.peer_rank = peer->rank;
+            for (int r = 0; r < peer->world; ++r) {
+                F.peer_slots[r] = static_cast<float*>(peer->slots[r]);
+                F.peer_ctr[r] = peer->counters[r];
+                F.peer_out[r] = static_cast<__nv_bfloat16*>(peer->out[r]);
+            }
+            F.ld_peer_out = peer->ld_out;
+        }
         F.acc_in = P.acc_in;
         F.ld_acc = P.ld_acc;
         F.ablate = opts().ablate;
@@ -829,6 +896,7 @@ int coda_gemm_epilogue(const coda_problem_t* pr, const coda_tensor_t* a, const c
     if (sdt == CODA_BF16) return launch_gemm<__nv_bfloat16>(ma, mb, P, st, pr->sm_limit);
     return launch_gemm<float>(ma, mb, P, st, pr->sm_limit);
 }
+}  // namespace
 
 int coda_finalize_rms(const float* p, int64_t m, int64_t nb, int64_t ld, int64_t d, float eps, float* r,
                       void* stream) {

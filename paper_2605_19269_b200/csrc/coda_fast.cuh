@@ -46,7 +46,10 @@ enum FastFlags : int {
     F_LSE = 1 << 13,        // OnlineLse: (max, scaled sum) pairs per piece (rowpart holds pairs)
     F_ROWDOT = 1 << 14,     // PartialRowDot against a side tile, before RowScale (rowpart = row sums)
     F_XENT_BWD = 1 << 15,   // CrossEntropyBackward: grad = (exp(x - lse) - onehot) * scale, rowpart = sum x*grad
+    F_PEER = 1 << 16,       // data-parallel weight gradient: cross-rank sum over peer memory (no main store)
 };
+
+constexpr int MAX_PEERS = 8;
 
 constexpr int FAST_EPI_WARPS = 8;
 constexpr int FAST_THREADS = 64 + 32 * FAST_EPI_WARPS;
@@ -87,6 +90,18 @@ struct FastParams {
     float* target;
     const float* xent_lse;  // F_XENT_BWD: per-row log-sum-exp
     float xent_scale;
+    // F_PEER: `peer_world` ranks each run this launch on their own token shard.  Tile t is
+    // owned by rank t % world; every rank dumps its f32 partial of t into the owner's
+    // landing buffer peer_slots[owner] at slot ((t / world) * world + peer_rank) and
+    // arrives on the owner's counter peer_ctr[owner][(t / world) * CG + cta rank]; the
+    // last arrival sums the world slots in rank order, rounds to bf16 once and stores the
+    // tile into every rank's output peer_out[r] (row stride ld_peer_out).  Pointers are
+    // peer-mapped (CUDA IPC / NVLink P2P); counters are zero between launches.
+    int peer_world, peer_rank;
+    float* peer_slots[MAX_PEERS];
+    int* peer_ctr[MAX_PEERS];
+    __nv_bfloat16* peer_out[MAX_PEERS];
+    int64_t ld_peer_out;
     // tail-split workspace: f32 partial accumulators [tail tile][piece < split][rank][128 x 256]
     // and one arrival counter per (tail tile, rank), zero between launches
     float* ws;
@@ -122,6 +137,12 @@ __device__ __forceinline__ int counter_arrive(int* c) {
     asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(c) : "memory");
     return old;
 }
+// The same at system scope, for counters in another GPU's memory (F_PEER).
+__device__ __forceinline__ int counter_arrive_sys(int* c) {
+    int old;
+    asm volatile("atom.add.acq_rel.sys.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(c) : "memory");
+    return old;
+}
 
 // Side operands (residual, cos/sin, preact, pre_norm/grad_in) are TMA-loaded per
 // epilogue warp into a 4 KiB swizzled buffer, one 32-row chunk ahead; kernels that
@@ -141,6 +162,85 @@ struct FastGeom {
                                      : (FL & F_RMSBWD) ? ((FL & F_RMSBWD_ACC) ? 4096 : 2048)
                                      : (FL & (F_RESIDUAL | F_ROWDOT)) ? 2048 : 0;
 };
+
+// F_PEER epilogue of one tile (see FastParams): dump, arrive on the owner's counter, and
+// -- last arrival only -- fold the world partials in rank order and store bf16 everywhere.
+// Each epilogue warp owns a 32-row x 128-column region; the dump is lane-contiguous
+// (float4 k of lane l at (32 k + l) * 16 B) so every warp access covers four whole lines.
+template <int CG>
+__device__ __forceinline__ void peer_tile(const FastParams& P, int t, int m0, int n0, int rank, int q, int h,
+                                          int ew, int lane, uint32_t tmem_base, int& acc, uint32_t& acc_phase,
+                                          uint64_t* tfull, uint64_t* tempty, uint32_t* tmem_slot) {
+    const int world = P.peer_world;
+    const int own = t % world, j = t / world;
+    const int64_t region = (int64_t)(q * 2 + h) * (32 * 128) + lane * 4;
+    mbar_wait(&tfull[acc], acc_phase);
+    tc_fence_after();
+    const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + h * 128);
+    float* dst = P.peer_slots[own] + ((int64_t)(j * world + P.peer_rank) * CG + rank) * (BM * BN) + region;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+        float v[32];
+        tmem_ld32(tb + c * 32, v);
+#pragma unroll
+        for (int e = 0; e < 32; e += 4)
+            __stcg(reinterpret_cast<float4*>(dst + (c * 8 + e / 4) * 128), make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]));
+    }
+    tc_fence_before();
+    __threadfence_system();
+    __syncwarp();
+    if (lane == 0) {
+        if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
+        else mbar_arrive_leader(&tempty[acc]);
+    }
+    acc ^= 1;
+    if (acc == 0) acc_phase ^= 1;
+    named_bar_sync(4, 32 * FAST_EPI_WARPS);          // every region of this CTA is dumped
+    if (ew == 0 && lane == 0) {
+        int* cnt = P.peer_ctr[own] + j * CG + rank;
+        const int old = counter_arrive_sys(cnt);
+        if (old == world - 1) *cnt = 0;               // every rank is in: reset for the next launch
+        tmem_slot[1] = old == world - 1 ? 1u : 0u;
+    }
+    named_bar_sync(4, 32 * FAST_EPI_WARPS);
+    if (tmem_slot[1] == 0u) return;
+    __threadfence_system();
+    const int64_t row = (int64_t)m0 + q * 32 + lane;
+    const bool row_ok = row < P.mp.M;
+    const int N = P.mp.N;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+        float v[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = 0.0f;
+        for (int s = 0; s < world; ++s) {             // rank order: bitwise deterministic
+            const float* src = P.peer_slots[own] + ((int64_t)(j * world + s) * CG + rank) * (BM * BN) + region + c * 8 * 128;
+#pragma unroll
+            for (int e = 0; e < 32; e += 4) {
+                const float4 u = __ldcg(reinterpret_cast<const float4*>(src + (e / 4) * 128));
+                v[e] += u.x;
+                v[e + 1] += u.y;
+                v[e + 2] += u.z;
+                v[e + 3] += u.w;
+            }
+        }
+        const int gcol = n0 + h * 128 + c * 32;
+        if (!row_ok || gcol >= N) continue;
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) pk[e] = pack_bf16x2(v[2 * e], v[2 * e + 1]);
+        for (int r = 0; r < world; ++r) {
+            __nv_bfloat16* o = P.peer_out[r] + row * P.ld_peer_out + gcol;
+            if (gcol + 32 <= N && (P.ld_peer_out & 7) == 0) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    reinterpret_cast<uint4*>(o)[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+            } else {
+                for (int e = 0; e < 32 && gcol + e < N; ++e) o[e] = __float2bfloat16_rn(v[e]);
+            }
+        }
+    }
+}
 
 template <int CG, int FL>
 constexpr size_t fast_smem_bytes() {
@@ -427,6 +527,11 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             const int tm = w.tm, tn = w.tn;
             const int m0 = tm * G::TILE_M + rank * BM;
             const int n0 = tn * BN;
+            if constexpr ((FL & F_PEER) != 0) {
+                peer_tile<CG>(P, tm * mp.ntn + tn, m0, n0, rank, q, h, ew, lane, tmem_base, acc, acc_phase, tfull, tempty,
+                          tmem_slot);
+                continue;
+            }
             // a K piece of a split tail tile: every epilogue warp dumps the raw f32 accumulator
             // of its 32 x 128 region; then the CTA arrives once on the (tail tile, rank) counter.
             // The last of the `split` arrivals sums every dumped piece in fixed piece order and

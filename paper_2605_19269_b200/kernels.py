@@ -681,7 +681,13 @@ def layer_backward(grad_qkv: DenseMatrix, tape: LayerTape, weights: LayerWeights
     prec = config.precision
     f32 = wgrad_hook is not None and prec is PrecisionMode.SIMBF16 and getattr(wgrad_hook, "f32", True)
 
+    # a hook that reduces inside the GEMM epilogue (parallel.PeerWgradReduce) launches the
+    # weight gradients itself; bf16 storage only
+    peer_gemm = getattr(wgrad_hook, "gemm", None) if prec is PrecisionMode.SIMBF16 else None
+
     def wgrad(name, a, b):
+        if peer_gemm is not None:
+            return peer_gemm(name, a, b, precision=prec)
         res = _launch(traffic.K_GEMM, a, b, [], {}, trans_a=True, tile_shape=config.tile_shape,
                       reduction_tile_n=config.reduction_tile_n, precision=prec, ledger=ledger, out_f32=f32)
         if wgrad_hook is not None:

@@ -110,3 +110,102 @@ class WgradAllReduce:
         if self._capped is not None:
             self._capped.__exit__(None, None, None)
             self._capped = None
+
+
+class PeerWgradReduce(WgradAllReduce):
+    """`wgrad_hook` whose weight-gradient GEMMs sum across ranks inside their epilogue.
+
+    Instead of "GEMM, then all-reduce", every rank's launch of a weight gradient
+    (coda_gemm_peer_reduce) writes each f32 output tile into the landing buffer of the
+    tile's owner rank through peer memory (CUDA IPC, NVLink P2P between GPUs); the last
+    rank to deliver a tile sums the partials in rank order, rounds to bf16 once and
+    stores the tile into every rank's result — the reduce-scatter and the all-gather ride
+    on the GEMM's own epilogue, tile by tile, while the mainloop computes the next tile.
+    Bytes per rank on the wire: (P-1)/P of the f32 partial out, (P-1)/P of the bf16 sum
+    in, against 2 (P-1)/P of the f32 gradient for a ring all-reduce.
+
+    Gain gradients (vectors) and the folded-gain weight gradients keep the NCCL path of
+    WgradAllReduce.  `wait()` ends the step with a cross-rank barrier (an NCCL all-reduce
+    of one element, or a host barrier on gloo), after which every rank's results are
+    complete and the landing buffers may be reused.  The returned gradients live in
+    buffers owned by the hook and are overwritten by its next step.
+    """
+
+    def __init__(self, dist, device, reserve_sms: int = 0):
+        super().__init__(dist, device, f32=True, reserve_sms=reserve_sms)
+        self.world = dist.get_world_size()
+        self.rank = dist.get_rank()
+        self.device = device
+        if self.world > 8:
+            raise ValueError(f"peer reduction supports up to 8 ranks, got {self.world}")
+        self._regions: dict = {}
+        self._pending = False
+
+    def _region(self, name: str, m: int, n: int):
+        """Landing / counter / result buffers of one weight gradient, mapped on every rank."""
+        import torch
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        from . import _native as nat
+        from .tensors import alloc_matrix
+
+        key = (name, m, n)
+        reg = self._regions.get(key)
+        if reg is not None:
+            return reg
+        slot_bytes, ctr_bytes = nat.peer_reduce_sizes(m, n, self.world)
+        slots = torch.empty(slot_bytes // 4, dtype=torch.float32, device=self.device)
+        ctr = torch.zeros(ctr_bytes // 4, dtype=torch.int32, device=self.device)
+        out = alloc_matrix(m, n, torch.bfloat16, self.device)
+        torch.cuda.synchronize(self.device)            # zeroed counters before any peer arrives
+        mine = [reduce_tensor(t) for t in (slots, ctr, out)]
+        gathered = [None] * self.world
+        self.dist.all_gather_object(gathered, mine)
+        peers = []
+        for r, objs in enumerate(gathered):
+            peers.append([slots, ctr, out] if r == self.rank else [fn(*args) for fn, args in objs])
+        desc = nat.PeerReduce()
+        desc.world, desc.rank = self.world, self.rank
+        for r, (s, c, o) in enumerate(peers):
+            desc.slots[r], desc.counters[r], desc.out[r] = s.data_ptr(), c.data_ptr(), o.data_ptr()
+        desc.ld_out = out.stride(0)
+        desc.slot_bytes, desc.counter_bytes = slot_bytes, ctr_bytes
+        reg = {"desc": desc, "out": out, "keep": peers}
+        self._regions[key] = reg
+        return reg
+
+    def gemm(self, name: str, a, b, *, precision):
+        """dW = a^T b of this rank's token shard, summed over ranks (bf16, complete after wait())."""
+        import ctypes
+
+        import torch
+
+        from . import _native as nat
+        from .tensors import DenseMatrix
+
+        k, m = a.tensor.shape
+        n = b.tensor.shape[1]
+        reg = self._region(name, m, n)
+        prob = nat.Problem(m, n, k, 1, 0, nat.BF16, nat.BF16, 0, nat.sm_limit(), None, 0)
+        stream = torch.cuda.current_stream(a.tensor.device).cuda_stream
+        nat.call("coda_gemm_peer_reduce", ctypes.byref(prob), ctypes.byref(nat.tensor_desc(a.tensor)),
+                 ctypes.byref(nat.tensor_desc(b.tensor)), ctypes.byref(reg["desc"]), stream,
+                 tag=f"gemm_peer_reduce {m}x{n}x{k} TN", flops=2.0 * m * n * k)
+        self.names.append(name)
+        self._pending = True
+        return DenseMatrix._wrap(reg["out"], precision)
+
+    def wait(self) -> None:
+        super().wait()
+        if not self._pending:
+            return
+        import torch
+
+        # every rank's peer-reduce launches have finished -> all results are complete
+        if self.dist.get_backend() == "nccl":
+            t = torch.zeros(1, device=self.device)
+            self.dist.all_reduce(t)
+        else:
+            torch.cuda.current_stream(self.device).synchronize()
+            self.dist.barrier()
+        self._pending = False

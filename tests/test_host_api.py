@@ -328,3 +328,28 @@ def test_problem_validation():
         cd.GemmProblem(m=4, n=4, k=4, tile_shape=cd.TileShape(0, 4))
     with pytest.raises(cd.ConfigError):
         cd.GemmProblem(m=4, n=4, k=4, reduction_tile_n=0)
+
+
+def test_peer_reduce_descriptor_and_sizes():
+    """coda_peer_reduce_t mirrors include/coda.h; buffer sizes follow the pair-tile grid;
+    malformed descriptors fail in validation, before any device work (no GPU needed)."""
+    assert ctypes.sizeof(nat.PeerReduce) == 8 + 3 * 8 * nat.MAX_PEERS + 3 * 8
+    assert nat.PeerReduce.ld_out.offset == 8 + 3 * 8 * nat.MAX_PEERS
+    tile = 2 * 128 * 256 * 4                                   # one 256 x 256 f32 pair tile
+    for (m, n, world) in ((4096, 28672, 2), (4096, 4096, 8), (300, 520, 3)):
+        tiles = -(-m // 256) * -(-n // 256)
+        owned = -(-tiles // world)
+        assert nat.peer_reduce_sizes(m, n, world) == (owned * world * tile, owned * 2 * 4)
+    with pytest.raises(cd.ConfigError):
+        nat.peer_reduce_sizes(256, 256, 9)
+    lib = nat.load()
+    prob = nat.Problem(256, 256, 64, 1, 0, nat.BF16, nat.BF16, 0, 0, None, 0)
+    assert lib.coda_gemm_peer_reduce(ctypes.byref(prob), None, None, None, None) == -2        # BindingError
+    d = nat.PeerReduce()
+    d.world, d.rank = 2, 2
+    d.slot_bytes, d.counter_bytes = 1 << 30, 1 << 20
+    assert lib.coda_gemm_peer_reduce(ctypes.byref(prob), None, None, ctypes.byref(d), None) == -5   # bad rank
+    d.rank = 0
+    assert lib.coda_gemm_peer_reduce(ctypes.byref(prob), None, None, ctypes.byref(d), None) == -1   # ld_out < n
+    d.ld_out = 256
+    assert lib.coda_gemm_peer_reduce(ctypes.byref(prob), None, None, ctypes.byref(d), None) == -2   # null buffers
