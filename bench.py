@@ -554,8 +554,15 @@ def coda_arm(args, rank, world, local_rank):
     # SMs left to the side-stream all-reduce while a reduction is in flight (the hook caps the
     # persistent GEMMs from the first weight gradient of the backward until wait())
     comm_sms = args.comm_sms if args.comm_sms is not None else (DEFAULT_COMM_SMS if world > 1 else 0)
-    hook = parallel.WgradAllReduce(dist, device, f32=args.wgrad_dtype == "f32",
-                                   reserve_sms=comm_sms) if dist is not None else None
+    if dist is None:
+        hook = None
+    elif args.wgrad_reduce == "peer" and not fp32:
+        # weight gradients summed across ranks inside their GEMM epilogue (peer memory);
+        # only the gain vectors go through NCCL, so no SMs are held back for it
+        comm_sms = 0
+        hook = parallel.PeerWgradReduce(dist, device)
+    else:
+        hook = parallel.WgradAllReduce(dist, device, f32=args.wgrad_dtype == "f32", reserve_sms=comm_sms)
     bwd_sms = 0
 
     def step():
@@ -854,6 +861,7 @@ def coda_arm(args, rank, world, local_rank):
             "fold_gamma_ab": fold_ab,
             "comm_sms": comm_sms if dist is not None else 0,
             "wgrad_allreduce_dtype": args.wgrad_dtype if dist is not None else None,
+            "wgrad_reduce": (type(hook).__name__ if hook is not None else None),
             "fold_gamma": bool(args.fold_gamma),
             "launch_breakdown_ms": {k: round(v["avg_ms"], 4) for k, v in (prof or {}).items()},
         }
@@ -909,6 +917,9 @@ def main(argv=None):
     ap.add_argument("--wgrad-dtype", choices=("f32", "bf16"), default="f32",
                     help="dtype of the data-parallel weight-gradient all-reduce (f32: single rounding, "
                          "the reference's; bf16 halves the bytes)")
+    ap.add_argument("--wgrad-reduce", choices=("allreduce", "peer"), default="allreduce",
+                    help="data-parallel weight gradients: NCCL all-reduce on a side stream, or the sum fused "
+                         "into the weight-gradient GEMM epilogue over peer memory (coda_gemm_peer_reduce)")
     ap.add_argument("--cpu-sample", type=int, default=256)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size oracle parity check (c3/c4)")
