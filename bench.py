@@ -467,7 +467,7 @@ def wgrad_shapes(d, inter, kv=None):
 
 def launcher_check(args, rank, world):
     """--launcher-check: gloo on CPU, no kernels.  Each step all-reduces zero-filled f32 buffers
-    with the block's gradient shapes through the same WgradAllReduce hook the GPU path uses."""
+    with the block's gradient shapes through the same hook class the GPU path uses."""
     import torch
     import torch.distributed as dist
 
@@ -478,7 +478,7 @@ def launcher_check(args, rank, world):
     tokens = args.tokens or tokens
     sh = parallel.shard(tokens, rank, world, args.scaling)
     bufs = [torch.zeros(shape, dtype=torch.float32) for _, shape in wgrad_shapes(d, inter, KV.get(args.config))]
-    hook = parallel.WgradAllReduce(dist)
+    hook = parallel.WgradReduceScatter(dist) if args.wgrad_reduce == "rsag" else parallel.WgradAllReduce(dist)
 
     def step():
         for (name, _), b in zip(wgrad_shapes(d, inter), bufs):
@@ -561,6 +561,8 @@ def coda_arm(args, rank, world, local_rank):
         # only the gain vectors go through NCCL, so no SMs are held back for it
         comm_sms = 0
         hook = parallel.PeerWgradReduce(dist, device)
+    elif args.wgrad_reduce == "rsag" and args.wgrad_dtype == "f32" and not fp32:
+        hook = parallel.WgradReduceScatter(dist, device, reserve_sms=comm_sms)
     else:
         hook = parallel.WgradAllReduce(dist, device, f32=args.wgrad_dtype == "f32", reserve_sms=comm_sms)
     bwd_sms = 0
@@ -603,16 +605,24 @@ def coda_arm(args, rank, world, local_rank):
     barrier()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    graph = None
-    if args.graph:
-        # capture one whole step (19 launches) once; replaying it removes host launch overhead
-        graph = torch.cuda.CUDAGraph()
+
+    def capture(fn):
+        """Capture one call of `fn` (a whole step: its launches, the hook's collectives on
+        the side stream and the join) as a CUDA graph; replaying it costs the host ~10 us
+        instead of the step's Python enqueue (1.3 ms, 3-7 ms with the per-gradient
+        collective calls), which a strong-scaled rank (~2.4 ms of device work at P = 8)
+        cannot hide."""
+        g = torch.cuda.CUDAGraph()
         cap_stream = torch.cuda.Stream(device)
         _native.prepare_stream_workspace(device, cap_stream)   # keep the split-K tail inside the graph
         c0 = _native.launch_count()
-        with torch.cuda.graph(graph, stream=cap_stream):
-            step()
-        per_step_launches = _native.launch_count() - c0
+        with torch.cuda.graph(g, stream=cap_stream):
+            out = fn()
+        return g, _native.launch_count() - c0, out
+
+    graph = None
+    if args.graph:
+        graph, per_step_launches, _ = capture(step)
         for _ in range(2):
             graph.replay()
         barrier()
@@ -666,7 +676,7 @@ def coda_arm(args, rank, world, local_rank):
     # ---- the other reading of the config text: weak scaling (the config's tokens on EVERY rank),
     # reported beside the strong-scaled headline for N > 1
     weak = None
-    if world > 1 and args.scaling == "strong" and graph is None:
+    if world > 1 and args.scaling == "strong":
         ww, wa, wc, wsn = make_workload(cd, d, inter, tokens, rank * tokens, device, blocks=nblocks, fp32=fp32,
                                         kv=kv)
 
@@ -677,18 +687,21 @@ def coda_arm(args, rank, world, local_rank):
 
         for _ in range(2):
             weak_step()
+        weak_graph = capture(weak_step)[0] if graph is not None else None
+        run_weak = weak_graph.replay if weak_graph is not None else weak_step
+        run_weak()
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            weak_step()
+            run_weak()
         e1.record(stream)
         barrier()
         t = torch.tensor([e0.elapsed_time(e1)], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         wms = float(t.item()) / args.steps
         weak = {"tokens_per_gpu": tokens, "global_tokens": world * tokens, "ms_per_step": wms,
-                "value": world * tokens / (wms / 1e3), "unit": "tokens/s"}
-        del ww, wa, wc, wsn
+                "value": world * tokens / (wms / 1e3), "unit": "tokens/s", "cuda_graph": weak_graph is not None}
+        del ww, wa, wc, wsn, weak_graph
 
     # ---- e2e through the public API from pinned host buffers.  Every step copies its
     # inputs H2D and reads its results D2H inside the timed region; the copies run on
@@ -715,6 +728,22 @@ def coda_arm(args, rank, world, local_rank):
             e = torch.cuda.Event(enable_timing=True)
             e.record(st)
             marks.append((what, e))
+
+    # with --graph, each input buffer's step is one captured graph (its launches and the
+    # hook's collectives); the copies and the cross-stream events stay outside, so the copy
+    # of step s+1 still overlaps step s.  The graph's step waits for all of its inputs.
+    e2e_graphs = None
+    if graph is not None:
+        def graph_step(b):
+            a = {k: cd.DenseMatrix.from_tensor(dev_in[b][k], P) for k in dev_in[b]}
+            out = run_step(cd, cfg, weights, a, cos, sin, hook, bwd_sms=bwd_sms)
+            if hook is not None:
+                hook.wait()
+            return out
+
+        for b in range(2):
+            graph_step(b)
+        e2e_graphs = [capture(lambda b=b: graph_step(b)) for b in range(2)]
 
     def e2e_run(nsteps):
         marks = []
@@ -749,13 +778,19 @@ def coda_arm(args, rank, world, local_rank):
             if pending[b] is not None:   # step s-2's results: D2H finished before their blocks are reused
                 stream.wait_event(done[b])
                 pending[b] = None
-            stream.wait_event(copied_f[b])
-            mark(marks, f"step{s} start", stream)
-            a = {k: cd.DenseMatrix.from_tensor(dev_in[b][k], P) for k in dev_in[b]}
-            _, bwd = run_step(cd, cfg, weights, a, cos, sin, hook,
-                              before_backward=lambda: stream.wait_event(copied_b[b]), bwd_sms=bwd_sms)
-            if hook is not None:
-                hook.wait()
+            if e2e_graphs is not None:
+                stream.wait_event(copied_b[b])
+                mark(marks, f"step{s} start", stream)
+                g, _, (_, bwd) = e2e_graphs[b]
+                g.replay()
+            else:
+                stream.wait_event(copied_f[b])
+                mark(marks, f"step{s} start", stream)
+                a = {k: cd.DenseMatrix.from_tensor(dev_in[b][k], P) for k in dev_in[b]}
+                _, bwd = run_step(cd, cfg, weights, a, cos, sin, hook,
+                                  before_backward=lambda: stream.wait_event(copied_b[b]), bwd_sms=bwd_sms)
+                if hook is not None:
+                    hook.wait()
             consumed[b].record(stream)
             mark(marks, f"step{s} end", stream)
             with torch.cuda.stream(d2h_stream):
@@ -837,7 +872,7 @@ def coda_arm(args, rank, world, local_rank):
         line = {
             "metric": "block fwd+bwd tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if args.scaling == "strong" and world > 1 else "weak",
+            "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32" if fp32 else "bf16",
             "data": "synthetic (random-init weights, N(0,1) activations)",
             "config": {"workload": label, "blocks": nblocks, "tokens_per_gpu": m, "global_tokens": world * m,
@@ -849,7 +884,7 @@ def coda_arm(args, rank, world, local_rank):
             "frac_of_bf16_peak": block_tflops / pk["bf16_tflops"],
             "clocks": clocks.summary(),
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h, "cuda_graph": e2e_graphs is not None},
             "gpu_launches": launches,
             "host_enqueue_ms_per_step": host_ms,
             "cuda_graph": bool(args.graph),
@@ -917,14 +952,20 @@ def main(argv=None):
     ap.add_argument("--wgrad-dtype", choices=("f32", "bf16"), default="f32",
                     help="dtype of the data-parallel weight-gradient all-reduce (f32: single rounding, "
                          "the reference's; bf16 halves the bytes)")
-    ap.add_argument("--wgrad-reduce", choices=("allreduce", "peer"), default="allreduce",
-                    help="data-parallel weight gradients: NCCL all-reduce on a side stream, or the sum fused "
-                         "into the weight-gradient GEMM epilogue over peer memory (coda_gemm_peer_reduce)")
+    ap.add_argument("--wgrad-reduce", choices=("rsag", "allreduce", "peer"), default="rsag",
+                    help="data-parallel weight gradients: NCCL reduce-scatter of the f32 sums, bf16 rounding of "
+                         "each rank's slice, all-gather of the bf16 slices (default: the reference's single "
+                         "rounding with 25%% fewer bytes than an f32 all-reduce); NCCL all-reduce; or the sum "
+                         "fused into the weight-gradient GEMM epilogue over peer memory (coda_gemm_peer_reduce)")
     ap.add_argument("--cpu-sample", type=int, default=256)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size oracle parity check (c3/c4)")
     ap.add_argument("--ncu", action="store_true", help="profiling pass only (no timing / JSON line)")
-    ap.add_argument("--graph", action="store_true", help="replay the step as one captured CUDA graph")
+    ap.add_argument("--graph", action="store_true", default=None,
+                    help="replay each step (device-timed, weak-scaling and e2e loops) as one captured CUDA graph "
+                         "(default: on when N > 1, where the host enqueue of a strong-scaled step would "
+                         "otherwise exceed its device time)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the NCCL wgrad all-reduce path even at world size 1 (collective overlap check)")
     ap.add_argument("--launcher-check", action="store_true",
@@ -943,6 +984,8 @@ def main(argv=None):
     if world != args.gpus:
         print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr, flush=True)
         return 2
+    if args.graph is None:
+        args.graph = world > 1
     if args.launcher_check:
         launcher_check(args, rank, world)
     elif args.impl == "reference":

@@ -758,7 +758,16 @@ def layer_backward(grad_qkv: DenseMatrix, tape: LayerTape, weights: LayerWeights
         if wait is not None:
             wait()
     if f32:
-        g_wqkv, g_wdown, g_wgu, g_wout = (to_storage(g, prec) for g in (g_wqkv, g_wdown, g_wgu, g_wout))
+        # a hook that rounds after its own reduction (parallel.WgradReduceScatter) hands back
+        # the bf16 sums; otherwise the reduced f32 sums are rounded here, once
+        reduced = getattr(wgrad_hook, "reduced", None)
+
+        def storage(name, g):
+            t = reduced(name) if reduced is not None else None
+            return DenseMatrix._wrap(t, prec) if t is not None else to_storage(g, prec)
+
+        g_wqkv, g_wdown, g_wgu, g_wout = (storage(n, g) for n, g in (("w_qkv", g_wqkv), ("w_down", g_wdown),
+                                                                       ("w_gate_up", g_wgu), ("w_out", g_wout)))
     return LayerGrads(x=grad_x, z=grad_h1a, w_out=g_wout, gamma_ffn=g_gffn, w_gate_up=g_wgu, w_down=g_wdown,
                       gamma_qkv=g_gqkv, w_qkv=g_wqkv, ledger=ledger)
 

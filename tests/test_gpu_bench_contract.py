@@ -45,3 +45,18 @@ def test_bench_line_c4_reduced(cuda_ready):
     assert out["gpu_launches"] == 3 * 15          # 15 kernels per block step (deferred finalizers)
     ab = out["fold_gamma_ab"]
     assert ab["ms_reference_schedule"] > 0 and ab["ms_gamma_folded"] > 0
+
+
+def test_bench_line_graph_with_collectives(cuda_ready):
+    """The N > 1 defaults on one GPU: a one-rank NCCL group, the reduce-scatter / all-gather
+    weight-gradient hook and every loop (device-timed and e2e) replayed as CUDA graphs; the
+    host enqueue is the graph launch only."""
+    out = _bench("--tokens", "2048", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-parity", "--ab-rounds", "0",
+                 "--force-dist", "--graph")
+    for k in REQUIRED:
+        assert k in out, k
+    assert out["cuda_graph"] is True and out["e2e"]["cuda_graph"] is True
+    assert out["wgrad_reduce"] == "WgradReduceScatter"
+    assert out["host_enqueue_ms_per_step"] < 0.5
+    assert out["gpu_launches"] > 3 * 15            # the block's kernels plus the slice roundings
+    assert out["value"] > 0 and out["e2e"]["value"] > 0

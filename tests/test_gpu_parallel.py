@@ -63,7 +63,7 @@ def _run(rank, world, sl, hook=None, fold=False):
                                               "w_qkv")}
 
 
-def _worker(rank, world, port, out_dir, reserve=0, fold=False):
+def _worker(rank, world, port, out_dir, reserve=0, fold=False, kind="allreduce"):
     sys.path.insert(0, str(ROOT))
     import torch
     import torch.distributed as dist
@@ -75,28 +75,37 @@ def _worker(rank, world, port, out_dir, reserve=0, fold=False):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     m = _inputs()[0]
     sh = parallel.shard(m, rank, world)
-    hook = parallel.WgradAllReduce(dist, torch.device("cuda", 0), reserve_sms=reserve)
+    dev = torch.device("cuda", 0)
+    hook = (parallel.WgradReduceScatter(dist, dev, reserve_sms=reserve) if kind == "rsag"
+            else parallel.WgradAllReduce(dist, dev, reserve_sms=reserve))
     grads = _run(rank, world, slice(sh.start, sh.stop), hook, fold=fold)
     from paper_2605_19269_b200 import _native
 
     assert _native.sm_limit() == 0                   # the cap ends with wait()
     assert set(hook.names) == set(parallel.REDUCED)
+    if kind == "rsag":
+        # the same f32 sums rounded once: bit-identical to the all-reduce path (P = 2 sums commute)
+        ar = _run(rank, world, slice(sh.start, sh.stop), parallel.WgradAllReduce(dist, dev), fold=fold)
+        grads.update({"ar_" + k: v for k, v in ar.items()})
     np.savez(Path(out_dir) / f"rank{rank}.npz", **grads)
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("reserve,fold", [(0, False), (8, False), (8, True)])
-def test_sharded_fused_backward_matches_full_batch(cuda_ready, tmp_path, reserve, fold):
+@pytest.mark.parametrize("reserve,fold,kind", [(0, False, "allreduce"), (8, False, "allreduce"), (8, True, "allreduce"),
+                                               (8, False, "rsag"), (0, True, "rsag")])
+def test_sharded_fused_backward_matches_full_batch(cuda_ready, tmp_path, reserve, fold, kind):
     """reserve > 0: the hook caps the GEMMs' SMs while the all-reduce is in flight; fold: the
     gain-folded block, whose gain gradients come from the weight-gradient epilogue and are
-    all-reduced like the weights."""
+    all-reduced like the weights; kind "rsag": WgradReduceScatter (f32 reduce-scatter, bf16
+    rounding of each rank's slice, bf16 all-gather)."""
     import torch.multiprocessing as mp
 
     from oracle import coda_oracle as O
     from paper_2605_19269_b200 import parallel
 
     world = 2
-    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), reserve, fold), nprocs=world, join=True,
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), reserve, fold, kind), nprocs=world,
+                       join=True,
                        start_method="spawn")
     m = _inputs()[0]
     full = _run(0, 1, slice(0, m), fold=fold)
@@ -108,3 +117,7 @@ def test_sharded_fused_backward_matches_full_batch(cuda_ready, tmp_path, reserve
     for name in parallel.ROW_LOCAL:
         got = np.concatenate([s[name] for s in shards], axis=0)
         assert O.rel_error(got, full[name]) < 1e-2, name
+    if kind == "rsag":
+        for name in parallel.REDUCED:
+            for s in shards:
+                assert np.array_equal(s[name], s["ar_" + name]), name

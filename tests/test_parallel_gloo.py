@@ -37,7 +37,7 @@ def _problem():
     return m, d, w, x, z, gq, gr, mode
 
 
-def _worker(rank, world, port, out_dir, scaling):
+def _worker(rank, world, port, out_dir, scaling, kind="allreduce"):
     sys.path.insert(0, str(ROOT))
     import torch
     import torch.distributed as dist
@@ -54,7 +54,7 @@ def _worker(rank, world, port, out_dir, scaling):
     cos, sin = O.qkv_rope_tables(sh.rows, d, O.EXACT64, start=sh.start)
     fwd = O.layer_ref_forward(x[sl], z[sl], w, cos, sin)
     bwd = O.layer_ref_backward(gq[sl], gr[sl], fwd, x[sl], w, cos, sin)
-    hook = parallel.WgradAllReduce(dist)
+    hook = parallel.WgradReduceScatter(dist) if kind == "rsag" else parallel.WgradAllReduce(dist)
     for name in parallel.REDUCED:
         t = torch.from_numpy(np.ascontiguousarray(bwd[name]))
         hook(name, t)
@@ -64,15 +64,16 @@ def _worker(rank, world, port, out_dir, scaling):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("scaling", ["strong", "weak"])
-def test_token_sharded_grads_match_full_batch(tmp_path, scaling):
+@pytest.mark.parametrize("scaling,kind", [("strong", "allreduce"), ("weak", "allreduce"), ("strong", "rsag")])
+def test_token_sharded_grads_match_full_batch(tmp_path, scaling, kind):
+    """kind "rsag": WgradReduceScatter — reduce-scatter + all-gather in place of the all-reduce."""
     import torch.multiprocessing as mp
 
     from oracle import coda_oracle as O
     from paper_2605_19269_b200 import parallel
 
     world = 2
-    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), scaling), nprocs=world, join=True,
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), scaling, kind), nprocs=world, join=True,
                        start_method="spawn")
     m, d, w, x, z, gq, gr, mode = _problem()
     cos, sin = O.qkv_rope_tables(m, d, O.EXACT64)
