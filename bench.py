@@ -621,10 +621,17 @@ def coda_arm(args, rank, world, local_rank):
         return g, _native.launch_count() - c0, out
 
     graph = None
+    graph_error = None
     if args.graph:
-        graph, per_step_launches, _ = capture(step)
-        for _ in range(2):
-            graph.replay()
+        try:
+            graph, per_step_launches, _ = capture(step)
+            for _ in range(2):
+                graph.replay()
+        except RuntimeError as exc:   # e.g. a collective this NCCL / torch cannot capture: time it eagerly
+            graph, graph_error = None, f"{type(exc).__name__}: {exc}"[:300]
+            print(f"bench.py: CUDA graph capture failed, timing eager steps ({graph_error})", file=sys.stderr)
+            torch.cuda.synchronize()
+            step()
         barrier()
     launches0 = _native.launch_count()
     with clock_sampler(local_rank) as clocks:
@@ -887,7 +894,8 @@ def coda_arm(args, rank, world, local_rank):
                     "d2h_bytes_per_step": d2h, "cuda_graph": e2e_graphs is not None},
             "gpu_launches": launches,
             "host_enqueue_ms_per_step": host_ms,
-            "cuda_graph": bool(args.graph),
+            "cuda_graph": graph is not None,
+            "graph_error": graph_error,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "parity": parity,
