@@ -852,8 +852,10 @@ int gemm_impl(const coda_problem_t* pr, const coda_tensor_t* a, const coda_tenso
             const int es = P.out_f32 ? 4 : 2;
             const int wv = w;                  // values per 32-column chunk after the program
             const int rb = wv * es;
+            // 128-byte rows are stored as two 64-byte-wide halves (coda_fast.cuh staged_store)
+            const int bw = rb >= 128 ? wv / 2 : wv;
             rc = make_map(&mm, main_out->ptr, (uint64_t)main_out->cols, (uint64_t)M, (uint64_t)main_out->ld * es,
-                          (uint32_t)wv, rb >= 128 ? 16u : 32u, odt, store_swizzle(rb));
+                          (uint32_t)bw, 32u, odt, store_swizzle(bw * es));
             if (rc) return rc;
         }
         if (aux_slot >= 0) {
