@@ -608,17 +608,12 @@ def coda_arm(args, rank, world, local_rank):
 
     def capture(fn):
         """Capture one call of `fn` (a whole step: its launches, the hook's collectives on
-        the side stream and the join) as a CUDA graph; replaying it costs the host ~10 us
-        instead of the step's Python enqueue (1.3 ms, 3-7 ms with the per-gradient
-        collective calls), which a strong-scaled rank (~2.4 ms of device work at P = 8)
-        cannot hide."""
-        g = torch.cuda.CUDAGraph()
-        cap_stream = torch.cuda.Stream(device)
-        _native.prepare_stream_workspace(device, cap_stream)   # keep the split-K tail inside the graph
-        c0 = _native.launch_count()
-        with torch.cuda.graph(g, stream=cap_stream):
-            out = fn()
-        return g, _native.launch_count() - c0, out
+        the side stream and the join) as a CUDA graph (cd.StepGraph); replaying it costs the
+        host ~10 us instead of the step's Python enqueue (1.3 ms, 3-7 ms with the
+        per-gradient collective calls), which a strong-scaled rank (~2.4 ms of device work
+        at P = 8) cannot hide."""
+        sg = cd.StepGraph(fn, device, warmup=0)
+        return sg.graph, sg.launches, sg.outputs
 
     graph = None
     graph_error = None
