@@ -685,13 +685,24 @@ def layer_backward(grad_qkv: DenseMatrix, tape: LayerTape, weights: LayerWeights
     # weight gradients itself; bf16 storage only
     peer_gemm = getattr(wgrad_hook, "gemm", None) if prec is PrecisionMode.SIMBF16 else None
 
+    # a hook that rounds after its own reduction (parallel.WgradReduceScatter) takes the
+    # unrounded f32 weight gradients through reduce_unrounded() and hands back bf16 sums
+    # through reduced(); otherwise the hook leaves the f32 sum in place and it is rounded here
+    reduce_unrounded = getattr(wgrad_hook, "reduce_unrounded", None) if f32 else None
+
+    def hand_over(name, t):
+        if reduce_unrounded is not None:
+            reduce_unrounded(name, t)
+        else:
+            wgrad_hook(name, t)
+
     def wgrad(name, a, b):
         if peer_gemm is not None:
             return peer_gemm(name, a, b, precision=prec)
         res = _launch(traffic.K_GEMM, a, b, [], {}, trans_a=True, tile_shape=config.tile_shape,
                       reduction_tile_n=config.reduction_tile_n, precision=prec, ledger=ledger, out_f32=f32)
         if wgrad_hook is not None:
-            wgrad_hook(name, res.main.tensor)
+            hand_over(name, res.main.tensor)
         return res.main
 
     fold = config.fold_gamma
@@ -704,7 +715,7 @@ def layer_backward(grad_qkv: DenseMatrix, tape: LayerTape, weights: LayerWeights
         g_gain = finalize_rowdot(res.aux["gain_dot"], 1, ledger=ledger)
         g_gain.tensor   # no later launch consumes the gain gradient: finalize it now, inside the step
         if wgrad_hook is not None:
-            wgrad_hook(name, res.main.tensor)
+            hand_over(name, res.main.tensor)
             wgrad_hook(gname, g_gain.tensor)
         return res.main, g_gain
 
@@ -758,9 +769,7 @@ def layer_backward(grad_qkv: DenseMatrix, tape: LayerTape, weights: LayerWeights
         if wait is not None:
             wait()
     if f32:
-        # a hook that rounds after its own reduction (parallel.WgradReduceScatter) hands back
-        # the bf16 sums; otherwise the reduced f32 sums are rounded here, once
-        reduced = getattr(wgrad_hook, "reduced", None)
+        reduced = getattr(wgrad_hook, "reduced", None) if reduce_unrounded is not None else None
 
         def storage(name, g):
             t = reduced(name) if reduced is not None else None

@@ -123,11 +123,13 @@ class WgradReduceScatter(WgradAllReduce):
     all-gathered: (P-1)/P x (4 + 2) bytes per element, 25 % fewer on the wire, with
     the same single rounding of the same f32 sum.
 
-    The reduced bf16 gradient is handed back through `reduced(name)` (layer_backward
-    takes it instead of rounding the local f32 partial); tensors this path does not
-    apply to — gain vectors, bf16 gradients, element counts not divisible by the
-    world size — are all-reduced in place as in WgradAllReduce.  On CPU tensors (gloo
-    tests) the reduce-scatter / all-gather pair runs synchronously in place.
+    Protocol with layer_backward: an unrounded f32 weight gradient of the SIMBF16 path
+    is handed over with `reduce_unrounded(name, t)` and its bf16 sum taken back with
+    `reduced(name)` after `wait()`.  Everything else — gain vectors, gradients already
+    in storage precision (SIM32), shapes whose element count the world size does not
+    divide — goes through `hook(name, t)`, which leaves the f32 sum in place (NCCL
+    all-reduce on CUDA; on CPU tensors, the gloo tests, a synchronous reduce-scatter +
+    all-gather pair).
     """
 
     def __init__(self, dist, device=None, reserve_sms: int = 0):
@@ -141,33 +143,42 @@ class WgradReduceScatter(WgradAllReduce):
                 and tensor.numel() > 0)
 
     def __call__(self, name: str, tensor) -> None:
+        """Sum over ranks in place."""
         import torch
 
-        if not self._splits(tensor) or (self.side is not None and tensor.dtype != torch.float32):
+        if self.side is not None or not self._splits(tensor):
             return super().__call__(name, tensor)
         self.names.append(name)
         flat = tensor.view(-1)
-        n = flat.numel() // self.world
-        if self.side is None:
-            shard = torch.empty(n, dtype=tensor.dtype)
-            self.dist.reduce_scatter_tensor(shard, flat)
-            self.dist.all_gather_into_tensor(flat, shard)
-            return
+        shard = torch.empty(flat.numel() // self.world, dtype=tensor.dtype)
+        self.dist.reduce_scatter_tensor(shard, flat)
+        self.dist.all_gather_into_tensor(flat, shard)
+
+    def reduce_unrounded(self, name: str, tensor) -> None:
+        """Sum the unrounded f32 gradient over ranks and round it to bf16 once; the result
+        is `reduced(name)` after wait() (or, when the slice path does not apply, the sum
+        is left in place and `reduced(name)` is None)."""
+        import torch
+
+        if self.side is None or tensor.dtype != torch.float32 or not self._splits(tensor):
+            return self(name, tensor)
+        import ctypes
+
         from . import _native as nat
 
+        self.names.append(name)
         self._cap()
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(tensor.device))
         rows, cols = tensor.shape
+        n = tensor.numel() // self.world
         # the slice as a matrix when whole rows split evenly (vectorised rounding kernel)
         shape = (rows // self.world, cols) if rows % self.world == 0 else (1, n)
         with torch.cuda.stream(self.side):
             self.side.wait_event(ev)
             shard = torch.empty(shape, dtype=torch.float32, device=tensor.device)
-            self.dist.reduce_scatter_tensor(shard.view(-1), flat)
+            self.dist.reduce_scatter_tensor(shard.view(-1), tensor.view(-1))
             half = torch.empty(shape, dtype=torch.bfloat16, device=tensor.device)
-            import ctypes
-
             nat.call("coda_convert_f32_bf16", ctypes.byref(nat.tensor_desc(shard)),
                      ctypes.byref(nat.tensor_desc(half, nat.BF16)), self.side.cuda_stream)
             out = torch.empty((rows, cols), dtype=torch.bfloat16, device=tensor.device)
@@ -178,7 +189,7 @@ class WgradReduceScatter(WgradAllReduce):
         self._out[name] = out
 
     def reduced(self, name: str):
-        """The bf16 all-gathered sum of `name` (None if it went through the in-place path)."""
+        """The bf16 sum handed over by reduce_unrounded(name), once (None if it was summed in place)."""
         return self._out.pop(name, None)
 
 

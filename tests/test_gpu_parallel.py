@@ -26,13 +26,13 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _inputs():
+def _inputs(prec="SIMBF16"):
     sys.path.insert(0, str(ROOT))
     from oracle import coda_oracle as O
 
     m, d, ffn = 256, 128, 512
     rng = np.random.default_rng(21)
-    mode = O.SIMBF16
+    mode = getattr(O, prec)
     w = O.random_layer(rng, d, ffn, mode, scale=0.1)
     x, z = (O.q(rng.standard_normal((m, d)), mode) for _ in range(2))
     gq = O.q(rng.standard_normal((m, 3 * d)), mode)
@@ -40,11 +40,11 @@ def _inputs():
     return m, d, ffn, w, x, z, gq, gr
 
 
-def _run(rank, world, sl, hook=None, fold=False):
+def _run(rank, world, sl, hook=None, fold=False, prec="SIMBF16"):
     import paper_2605_19269_b200 as cd
 
-    m, d, ffn, w, x, z, gq, gr = _inputs()
-    P = cd.PrecisionMode.SIMBF16
+    m, d, ffn, w, x, z, gq, gr = _inputs(prec)
+    P = getattr(cd.PrecisionMode, prec)
     M = lambda a: cd.DenseMatrix.from_array(a, P)  # noqa: E731
     weights = cd.LayerWeights(w_out=M(w["w_out"]), gamma_ffn=cd.Vector.from_array(w["gamma_ffn"], P),
                               w_gate_up=M(w["w_gate_up"]), w_down=M(w["w_down"]),
@@ -63,7 +63,7 @@ def _run(rank, world, sl, hook=None, fold=False):
                                               "w_qkv")}
 
 
-def _worker(rank, world, port, out_dir, reserve=0, fold=False, kind="allreduce"):
+def _worker(rank, world, port, out_dir, reserve=0, fold=False, kind="allreduce", prec="SIMBF16"):
     sys.path.insert(0, str(ROOT))
     import torch
     import torch.distributed as dist
@@ -78,12 +78,12 @@ def _worker(rank, world, port, out_dir, reserve=0, fold=False, kind="allreduce")
     dev = torch.device("cuda", 0)
     hook = (parallel.WgradReduceScatter(dist, dev, reserve_sms=reserve) if kind == "rsag"
             else parallel.WgradAllReduce(dist, dev, reserve_sms=reserve))
-    grads = _run(rank, world, slice(sh.start, sh.stop), hook, fold=fold)
+    grads = _run(rank, world, slice(sh.start, sh.stop), hook, fold=fold, prec=prec)
     from paper_2605_19269_b200 import _native
 
     assert _native.sm_limit() == 0                   # the cap ends with wait()
     assert set(hook.names) == set(parallel.REDUCED)
-    if kind == "rsag":
+    if kind == "rsag" and prec == "SIMBF16":
         # the same f32 sums rounded once: bit-identical to the all-reduce path (P = 2 sums commute)
         ar = _run(rank, world, slice(sh.start, sh.stop), parallel.WgradAllReduce(dist, dev), fold=fold)
         grads.update({"ar_" + k: v for k, v in ar.items()})
@@ -121,3 +121,23 @@ def test_sharded_fused_backward_matches_full_batch(cuda_ready, tmp_path, reserve
         for name in parallel.REDUCED:
             for s in shards:
                 assert np.array_equal(s[name], s["ar_" + name]), name
+
+
+def test_reduce_scatter_hook_sim32(cuda_ready, tmp_path):
+    """SIM32 (f32 storage): the weight gradients reach WgradReduceScatter in storage
+    precision, so they are summed in place (never rounded to bf16)."""
+    import torch.multiprocessing as mp
+
+    from oracle import coda_oracle as O
+    from paper_2605_19269_b200 import parallel
+
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), 0, False, "rsag", "SIM32"), nprocs=world,
+                       join=True, start_method="spawn")
+    m = _inputs("SIM32")[0]
+    full = _run(0, 1, slice(0, m), prec="SIM32")
+    shards = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
+    for name in parallel.REDUCED:
+        for s in shards:
+            err = O.rel_error(s[name], full[name])
+            assert err < 1e-5, (name, err)       # f32 sums of two halves vs one full sum

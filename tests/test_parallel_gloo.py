@@ -140,3 +140,46 @@ def test_hook_caps_sms_only_while_reductions_are_in_flight():
         assert _native.sm_limit() == 0
     finally:
         _native.num_sms = orig_num_sms
+
+
+def test_reduce_scatter_hook_protocol():
+    """WgradReduceScatter: `hook(name, t)` always leaves the sum in place (gains, SIM32
+    storage-precision gradients); `reduce_unrounded` is the only entry that may hand the
+    result back through `reduced()` instead, and without a CUDA side stream it also sums in
+    place (reduced() is None).  layer_backward uses reduce_unrounded only for the unrounded
+    f32 partials of the SIMBF16 path."""
+    import inspect
+
+    import torch
+
+    sys.path.insert(0, str(ROOT))
+    from paper_2605_19269_b200 import kernels, parallel
+
+    class OneRank:
+        def get_world_size(self):
+            return 1
+
+        def get_rank(self):
+            return 0
+
+        def reduce_scatter_tensor(self, out, inp):
+            out.copy_(inp * 2)           # stand-in "sum" of two identical ranks
+
+        def all_gather_into_tensor(self, out, inp):
+            out.copy_(inp)
+
+        def all_reduce(self, t):
+            t.mul_(2)
+
+    hook = parallel.WgradReduceScatter(OneRank())
+    t = torch.ones(4, 6)
+    hook("w_out", t)
+    assert torch.equal(t, torch.full((4, 6), 2.0)) and hook.reduced("w_out") is None
+    v = torch.ones(5)
+    hook("gamma_ffn", v)                 # vectors: all-reduce in place
+    assert torch.equal(v, torch.full((5,), 2.0))
+    u = torch.ones(4, 6)
+    hook.reduce_unrounded("w_qkv", u)    # no side stream: in place
+    assert torch.equal(u, torch.full((4, 6), 2.0)) and hook.reduced("w_qkv") is None
+    src = inspect.getsource(kernels.layer_backward)
+    assert 'getattr(wgrad_hook, "reduce_unrounded", None) if f32 else None' in src
