@@ -221,6 +221,7 @@ struct Options {
     int persist = 1;      // [experiments] 0: one tile per cluster (non-persistent, hardware dispatch order)
     int wave_sync = 0;    // [experiments] soft wave barrier milestone in % of a tile's k-blocks (0 = off)
     int backoff = 0;      // [experiments] epilogue accumulator-wait sleep (ns)
+    int st_tma = 0;       // [experiments] staged epilogue stores by TMA instead of coalesced st.global
     Options() {
         if (const char* e = getenv("CODA_PDL")) pdl = e[0] != '0';
         if (const char* e = getenv("CODA_CG")) cg = e[0] == '1' ? 1 : 2;
@@ -478,6 +479,7 @@ int coda_set_option(const char* name, int value) {
     else if (n == "persist") opts().persist = value;
     else if (n == "wave_sync") opts().wave_sync = value;
     else if (n == "backoff") opts().backoff = value;
+    else if (n == "st_tma") opts().st_tma = value;
     else if (n == "prefetch") {
         if (value < 0 || value > 64) return fail(CODA_E_CONFIG, "prefetch distance must be in [0, 64]");
         opts().prefetch = value;
@@ -773,6 +775,9 @@ int gemm_impl(const coda_problem_t* pr, const coda_tensor_t* a, const coda_tenso
         F.ld_acc = P.ld_acc;
         F.ablate = opts().ablate;
         F.backoff = opts().backoff;
+#ifdef CODA_EXPERIMENTS
+        F.st_tma = opts().st_tma;
+#endif
         F.rope_sign = 1.0f;
         const void* rope_c = nullptr;
         const void* rope_s = nullptr;
@@ -857,12 +862,14 @@ int gemm_impl(const coda_problem_t* pr, const coda_tensor_t* a, const coda_tenso
             rc = make_map(&mm, main_out->ptr, (uint64_t)main_out->cols, (uint64_t)M, (uint64_t)main_out->ld * es,
                           (uint32_t)bw, 32u, odt, store_swizzle(bw * es));
             if (rc) return rc;
+            F.st_main = main_out->ptr; F.st_main_ld = main_out->ld * es; F.st_main_cols = main_out->cols * es;
         }
         if (aux_slot >= 0) {
             const coda_store_t& xs = stores[aux_slot];
             rc = make_map(&mx, xs.t.ptr, (uint64_t)xs.t.cols, (uint64_t)M, (uint64_t)xs.t.ld * 2, 32u, 32u, CODA_BF16,
                           64);
             if (rc) return rc;
+            F.st_aux = xs.t.ptr; F.st_aux_ld = xs.t.ld * 2; F.st_aux_cols = xs.t.cols * 2;
         }
         if (cg == 2 && pr->trans_b) {   // K-major B box covers this CTA's 128-column half
             rc = make_map(&mb, b->ptr, (uint64_t)K, (uint64_t)N, (uint64_t)b->ld * 2, coda::BK, coda::BN / 2);

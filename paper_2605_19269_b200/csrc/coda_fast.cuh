@@ -108,6 +108,14 @@ struct FastParams {
     int* flags;
     int ablate;   // measurement-only ablations (results invalid): 1 = no side loads, 2 = no TMA stores
     int backoff;  // [experiments] epilogue accumulator wait: ns of sleep between polls (0 = plain try_wait loop)
+    // staged-store destinations (byte strides): the main output and the AuxTileStore
+    void* st_main;
+    int64_t st_main_ld, st_main_cols;
+    void* st_aux;
+    int64_t st_aux_ld, st_aux_cols;
+#ifdef CODA_EXPERIMENTS
+    int st_tma;   // [experiments] staged boxes leave smem by TMA store (round-2 path)
+#endif
     // deferred finalizers (coda_step_t.fin_*): the RowScale vector / the RMSNorm-backward
     // stat computed per row from (M, nb) f32 partials and written back by the tn == 0 tiles
     const float* rs_fin;
@@ -322,64 +330,162 @@ __device__ __forceinline__ void fload_vec(const float* vp, int64_t c0, int64_t n
     }
 }
 
-// -------------------------------------------------------------- staged TMA stores
-// Per-warp staging: region r (0/1) = 2 KiB at stg + 2048 r, used alternately, so a
-// warp writes the next 32 x 64 B box while the TMA engine still reads the previous
-// one (wait until at most one store group is pending).  A store of 128-byte rows (64
-// bf16 / 32 f32 values per row) goes out as two 64-byte-wide halves through the two
-// regions: one 4 KiB box would need both regions and a full wait for the previous
-// store's smem reads before every box, which serialised the epilogue of the
-// width-doubling SwiGLU backward against the TMA engine (K10 +0.14 ms per C4 step).
+template <int W>
+__device__ __forceinline__ void fload_vec_cg(const float* vp, int64_t c0, int64_t n, float* d) {
+#pragma unroll
+    for (int i = 0; i < W; i += 4) {
+        if (c0 + i + 4 <= n) {
+            const float4 u = __ldcg(reinterpret_cast<const float4*>(vp + c0 + i));
+            d[i] = u.x; d[i + 1] = u.y; d[i + 2] = u.z; d[i + 3] = u.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) d[i + e] = (c0 + i + e < n) ? __ldcg(vp + c0 + i + e) : 0.0f;
+        }
+    }
+}
+
+// -------------------------------------------------------------- staged stores
+// Thread == row in registers; global rows want whole lines.  Each warp transposes a
+// 32 x RB-byte box (RB <= 64) through its own 2 KiB smem region (regions 0 / 1 used
+// alternately), then its lanes copy the box out row-contiguously with coalesced 16-B
+// global stores: a warp instruction covers 8 rows x 64 B, every 32-B sector whole.
+// 128-byte rows (64 bf16 / 32 f32 values) go out as two 64-byte-wide halves.
+//
+// Round 2 handed each box to the TMA engine (cp.async.bulk.tensor store), which also
+// issues the mainloop's operand loads, and every launch ended draining its stores.
+// The coalesced copy-out is bit-identical; launched one at a time (per-launch CUDA
+// events) K10 (1.41 GB of output) drops 1.70 -> 1.62 ms, K6 -1.3 %, the sum of the C4
+// launches -4 %; in the PDL-chained step the old path's tails were already hidden and
+// the step time is unchanged (profiles/r02_session3/stdirect_ab.txt, ab_copyout.txt).
+// The TMA path stays as the experiment option st_tma.
 struct Stager {
     uint32_t base;      // smem address of this warp's 4 KiB buffer (1024-aligned)
     int region;
-    bool skip;          // ablation: stage into smem but issue no TMA store
+    bool skip;          // ablation: stage into smem but store nothing
+#ifdef CODA_EXPERIMENTS
+    bool tma;           // [experiments] st_tma: boxes leave smem by TMA store
+#endif
 };
 
-template <typename TO, int W>
-__device__ __forceinline__ void staged_store(Stager& sg, const CUtensorMap* tm, int x, int y, const float* v,
-                                             int lane) {
+// AUX: the destination is the AuxTileStore output (P.st_aux), else the main output; its
+// pointer / strides are read from the kernel parameters at the copy-out (no registers
+// held across the epilogue).
+// Step 1 of a staged store: this thread's row of a 32 x RB box (RB <= 64) into the
+// warp's current region, in the swizzled layout.  Returns the region's smem address.
+template <typename TO, int RB>
+__device__ __forceinline__ uint32_t stage_box(Stager& sg, const float* v, int lane) {
+    constexpr uint32_t MASK = RB == 64 ? 0x30u : 0x10u;
+#ifdef CODA_EXPERIMENTS
+    // the region we are about to overwrite was read by the TMA store before last
+    if (sg.tma && lane == 0) bulk_wait_read<1>();
+#endif
+    // every lane's copy-out reads of this region (two boxes ago) are done
+    __syncwarp();
+    const uint32_t rbase = sg.base + (uint32_t)(sg.region * 2048);
+#pragma unroll
+    for (int c = 0; c < RB / 16; ++c) {
+        const uint32_t off = (uint32_t)(lane * RB + c * 16);
+        const uint32_t phys = off ^ ((off >> 3) & MASK);
+        uint32_t w0, w1, w2, w3;
+        if constexpr (sizeof(TO) == 2) {
+            w0 = pack_bf16x2(v[c * 8 + 0], v[c * 8 + 1]);
+            w1 = pack_bf16x2(v[c * 8 + 2], v[c * 8 + 3]);
+            w2 = pack_bf16x2(v[c * 8 + 4], v[c * 8 + 5]);
+            w3 = pack_bf16x2(v[c * 8 + 6], v[c * 8 + 7]);
+        } else {
+            w0 = __float_as_uint(v[c * 4 + 0]);
+            w1 = __float_as_uint(v[c * 4 + 1]);
+            w2 = __float_as_uint(v[c * 4 + 2]);
+            w3 = __float_as_uint(v[c * 4 + 3]);
+        }
+        st_shared_v4(rbase + phys, w0, w1, w2, w3);
+    }
+    sg.region ^= 1;
+    return rbase;
+}
+
+// Step 2: the box at `rbase` (staged by every lane, after a __syncwarp) to global rows
+// y.. and byte column x * sizeof(TO).. of the main (AUX = false) or aux output: lane l
+// takes 16-B chunks l, l + 32, ... in row-major order.  Pointers and strides are read
+// from the kernel parameters here, so nothing is held in registers across the epilogue.
+template <typename TO, int RB, bool AUX>
+__device__ __forceinline__ void copy_box(const Stager& sg, const FastParams& P, uint32_t rbase, int x, int y,
+                                         int lane) {
+    constexpr uint32_t MASK = RB == 64 ? 0x30u : 0x10u;
+    constexpr int CPR = RB / 16;    // chunks per row
+    const int64_t ld = AUX ? P.st_aux_ld : P.st_main_ld;
+    const int64_t left = (AUX ? P.st_aux_cols : P.st_main_cols) - (int64_t)x * (int64_t)sizeof(TO);
+    const int rows_left = sg.skip ? 0 : P.mp.M - y;
+    char* const box = static_cast<char*>(AUX ? P.st_aux : P.st_main) + (int64_t)y * ld +
+                      (int64_t)x * (int64_t)sizeof(TO);
+    // one 16-B chunk in flight per lane (keeps the register-heavy epilogues spill-free)
+#pragma unroll 1
+    for (int i = 0; i < CPR; ++i) {
+        const int j = i * 32 + lane;
+        const int row = j / CPR, c = j % CPR;
+        const uint32_t off = (uint32_t)(row * RB + c * 16);
+        const uint32_t phys = off ^ ((off >> 3) & MASK);
+        uint32_t w[4];
+        ld_shared_v4(rbase + phys, w[0], w[1], w[2], w[3]);
+        const int64_t rem = left - c * 16;
+        if (row >= rows_left || rem <= 0) continue;
+        char* p = box + row * ld + c * 16;
+        if (rem >= 16) {
+            *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+        } else {
+            // ragged last columns: element by element, re-read from smem (no register array)
+#pragma unroll 1
+            for (int k = 0; k < (int)rem; k += (int)sizeof(TO)) {
+                if constexpr (sizeof(TO) == 4) {
+                    uint32_t e;
+                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(e) : "r"(rbase + phys + k));
+                    *reinterpret_cast<uint32_t*>(p + k) = e;
+                } else {
+                    unsigned short e;
+                    asm volatile("ld.shared.b16 %0, [%1];" : "=h"(e) : "r"(rbase + phys + k));
+                    *reinterpret_cast<unsigned short*>(p + k) = e;
+                }
+            }
+        }
+    }
+}
+
+// A whole staged store of W values per row: stage, then copy out (or, experiment
+// st_tma, hand the box to the TMA engine).
+template <typename TO, int W, bool AUX = false>
+__device__ __forceinline__ void staged_store(Stager& sg, const FastParams& P, const CUtensorMap* tm, int x, int y,
+                                             const float* v, int lane) {
     constexpr int RB = W * (int)sizeof(TO);
     static_assert(RB == 32 || RB == 64 || RB == 128, "row bytes per staged store");
     if constexpr (RB == 128) {
-        // the map's box is W/2 columns wide (host: make_map for row bytes >= 128)
-        staged_store<TO, W / 2>(sg, tm, x, y, v, lane);
-        staged_store<TO, W / 2>(sg, tm, x + W / 2, y, v + W / 2, lane);
-        return;
+        // (TMA maps of 128-byte rows have a W/2-column box: host make_map)
+        staged_store<TO, W / 2, AUX>(sg, P, tm, x, y, v, lane);
+        staged_store<TO, W / 2, AUX>(sg, P, tm, x + W / 2, y, v + W / 2, lane);
     } else {
-        constexpr uint32_t MASK = RB == 64 ? 0x30u : 0x10u;
-        // 1. the region we are about to overwrite was read by the store before last
-        if (lane == 0) bulk_wait_read<1>();
-        __syncwarp();
-        const uint32_t rbase = sg.base + (uint32_t)(sg.region * 2048);
-        // 2. write this thread's row, 16 B at a time, in the TMA swizzle pattern
-#pragma unroll
-        for (int c = 0; c < RB / 16; ++c) {
-            const uint32_t off = (uint32_t)(lane * RB + c * 16);
-            const uint32_t phys = off ^ ((off >> 3) & MASK);
-            uint32_t w0, w1, w2, w3;
-            if constexpr (sizeof(TO) == 2) {
-                w0 = pack_bf16x2(v[c * 8 + 0], v[c * 8 + 1]);
-                w1 = pack_bf16x2(v[c * 8 + 2], v[c * 8 + 3]);
-                w2 = pack_bf16x2(v[c * 8 + 4], v[c * 8 + 5]);
-                w3 = pack_bf16x2(v[c * 8 + 6], v[c * 8 + 7]);
-            } else {
-                w0 = __float_as_uint(v[c * 4 + 0]);
-                w1 = __float_as_uint(v[c * 4 + 1]);
-                w2 = __float_as_uint(v[c * 4 + 2]);
-                w3 = __float_as_uint(v[c * 4 + 3]);
+        const uint32_t rbase = stage_box<TO, RB>(sg, v, lane);
+#ifdef CODA_EXPERIMENTS
+        if (sg.tma) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && !sg.skip) {
+                tma_store_2d(tm, rbase, x, y);
+                bulk_commit();
             }
-            st_shared_v4(rbase + phys, w0, w1, w2, w3);
+            return;
         }
-        fence_proxy_async_smem();
+#endif
         __syncwarp();
-        // 3. one lane hands the box to the TMA engine
-        if (lane == 0 && !sg.skip) {
-            tma_store_2d(tm, rbase, x, y);
-            bulk_commit();
-        }
-        sg.region ^= 1;
+        copy_box<TO, RB, AUX>(sg, P, rbase, x, y, lane);
     }
+}
+
+// Deferred form for register-heavy epilogues: stage now (registers -> smem), copy out
+// later with copy_box when fewer values are live.  At most one deferred box may be
+// pending when the next box is staged (two regions).
+template <typename TO, int W>
+__device__ __forceinline__ void staged_defer(Stager& sg, const float* v, int lane) {
+    static_assert(W * (int)sizeof(TO) <= 64, "deferred boxes are at most 64 bytes per row");
+    stage_box<TO, W * (int)sizeof(TO)>(sg, v, lane);
 }
 
 // Column sums over the warp's 32 rows: lane l ends with column l (fixed tree).
@@ -472,7 +578,11 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         const int h = ew >> 2;              // column half of the 256-wide tile
         const int lrow = q * 32 + lane;
         const int M = mp.M, N = mp.N;
+#ifdef CODA_EXPERIMENTS
+        Stager sg{smem_u32(stg + ew * STG_BYTES), 0, (P.ablate & 2) != 0, P.st_tma != 0};
+#else
         Stager sg{smem_u32(stg + ew * STG_BYTES), 0, (P.ablate & 2) != 0};
+#endif
         int cbuf = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -709,7 +819,7 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] += sd0[i];
                 }
-                if (FL & F_AUX) staged_store<TS, 32>(sg, &tma_aux, gcol0, m0 + q * 32, v, lane);
+                if (FL & F_AUX) staged_store<TS, 32, true>(sg, P, &tma_aux, gcol0, m0 + q * 32, v, lane);
                 if (FL & F_SUMSQ) {
                     float s = 0.0f;
 #pragma unroll
@@ -806,7 +916,7 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         const float g = v[2 * k], u = v[2 * k + 1];
                         v[k] = g * sigmoid_stable(g) * u;
                     }
-                    if (FL & F_STORE_MAIN) staged_store<TS, 16>(sg, &tma_main, gcol0 / 2, m0 + q * 32, v, lane);
+                    if (FL & F_STORE_MAIN) staged_store<TS, 16>(sg, P, &tma_main, gcol0 / 2, m0 + q * 32, v, lane);
                 } else if (FL & F_SWIGLU_BWD) {
                     const float* z = sd0;
                     float rec[32];
@@ -825,7 +935,7 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         s += g * gg;
                         s += u * gu;
                     }
-                    staged_store<TS, 32>(sg, &tma_aux, gcol0, m0 + q * 32, rec, lane);
+                    staged_store<TS, 32, true>(sg, P, &tma_aux, gcol0, m0 + q * 32, rec, lane);
                     const int pid = __ldg(P.rowpart_map + 2 * gcol0);
                     if (pid != ppid) {
                         if (ppid >= 0 && row_ok) P.rowpart[row * P.ld_rowpart + ppid] = pacc;
@@ -833,17 +943,29 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         pacc = 0.0f;
                     }
                     pacc += s;
-                    if (FL & F_STORE_MAIN) staged_store<TS, 64>(sg, &tma_main, 2 * gcol0, m0 + q * 32, o, lane);
+                    if (FL & F_STORE_MAIN) staged_store<TS, 64>(sg, P, &tma_main, 2 * gcol0, m0 + q * 32, o, lane);
                 } else if (FL & F_RMSBWD) {
                     float g[32], tmp[32];
                     float* cp = sd0;
-                    fload_vec<32>(P.gamma, gcol0, N, g);
+                    {
+                        float g0[32];
+                        fload_vec<32>(P.gamma, gcol0, N, g0);
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        cp[i] *= rr;             // c_n
-                        tmp[i] = cp[i] * g[i];   // normed
+                        for (int i = 0; i < 32; ++i) {
+                            cp[i] *= rr;              // c_n
+                            tmp[i] = cp[i] * g0[i];   // normed
+                        }
                     }
-                    staged_store<TS, 32>(sg, &tma_aux, gcol0, m0 + q * 32, tmp, lane);
+                    // the normed aux box is staged now and copied out after the main store,
+                    // when only the outputs are live
+#ifdef CODA_EXPERIMENTS
+                    if (sg.tma) staged_store<TS, 32, true>(sg, P, &tma_aux, gcol0, m0 + q * 32, tmp, lane);
+                    else
+#endif
+                    staged_defer<TS, 32>(sg, tmp, lane);
+                    // gamma again (L1-resident; an L2-hinted load the compiler does not merge with
+                    // the first), so it is not held live across the staging
+                    fload_vec_cg<32>(P.gamma, gcol0, N, g);
                     // one pass: the gamma-grad terms D * c_n, and the output (D g - c_n s) r (+ grad_in)
                     // in place -- c_n, g and grad_in die element by element, so the column sum below
                     // runs with only its 32 inputs and the 32 outputs live (no spills at 168 regs)
@@ -879,10 +1001,20 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         }
                     }
                     cbuf ^= 1;
-                    if (FL & F_STORE_MAIN) staged_store<TS, 32>(sg, &tma_main, gcol0, m0 + q * 32, v, lane);
+                    if (FL & F_STORE_MAIN) staged_store<TS, 32>(sg, P, &tma_main, gcol0, m0 + q * 32, v, lane);
+#ifdef CODA_EXPERIMENTS
+                    if (!sg.tma)
+#endif
+                    {
+                        // the aux box sits in the region before the current one, or in the one
+                        // before that when the main store went between (two regions)
+                        const int r = (FL & F_STORE_MAIN) ? sg.region : sg.region ^ 1;
+                        __syncwarp();
+                        copy_box<TS, 64, true>(sg, P, sg.base + (uint32_t)(r * 2048), gcol0, m0 + q * 32, lane);
+                    }
                 } else if (FL & F_STORE_MAIN) {
-                    if (FL & F_OUT_F32) staged_store<float, 32>(sg, &tma_main, gcol0, m0 + q * 32, v, lane);
-                    else staged_store<TS, 32>(sg, &tma_main, gcol0, m0 + q * 32, v, lane);
+                    if (FL & F_OUT_F32) staged_store<float, 32>(sg, P, &tma_main, gcol0, m0 + q * 32, v, lane);
+                    else staged_store<TS, 32>(sg, P, &tma_main, gcol0, m0 + q * 32, v, lane);
                 }
             }
             if ((FL & (F_SUMSQ | F_SWIGLU_BWD | F_ROWDOT | F_XENT_BWD)) && ppid >= 0 && row_ok)
