@@ -305,3 +305,30 @@ def test_concurrent_streams_with_tail_split(cuda_ready):
         _native.set_option("split_min_k", 8192)
     for r, o in zip(ref, outs):
         assert np.array_equal(r, o.main.data)
+
+
+@pytest.mark.parametrize("n", [33, 258, 262, 1000])
+@pytest.mark.parametrize("out_f32", [False, True])
+def test_ragged_columns_copy_out(cuda_ready, n, out_f32):
+    """The epilogue's coalesced copy-out of a staged box whose last 16-B chunk is partial
+    (N not a multiple of 8 bf16 / 4 f32 values): every column, the ragged last ones
+    included, matches the product (f32) or its bf16 rounding."""
+    import torch
+
+    cd = _mods()
+    P = cd.PrecisionMode.SIMBF16
+    rng = np.random.default_rng(n)
+    m, k = 300, 256
+    a = cd.DenseMatrix.from_array(rng.standard_normal((m, k)) / 16, P)
+    b = cd.DenseMatrix.from_array(rng.standard_normal((k, n)) / 16, P)
+    prob = cd.GemmProblem(m=m, n=n, k=k, precision=P)
+    t = cd.run_gemm(prob, a, b, out_f32=out_f32).main.tensor
+    torch.cuda.synchronize()
+    got = t.float().cpu().numpy().astype(np.float64)
+    exact = O.gemm(a.data, b.data, O.SIMBF16)
+    want = exact if out_f32 else O.q(exact, O.SIMBF16)
+    scale = np.max(np.abs(want))
+    tol = 1e-5 if out_f32 else 8e-3            # f32 accumulation order / one bf16 ulp
+    assert np.max(np.abs(got - want)) <= tol * scale
+    tail = slice(max(0, n - 9), n)             # the partial chunk and the one before it
+    assert np.max(np.abs(got[:, tail] - want[:, tail])) <= tol * scale
