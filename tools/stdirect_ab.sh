@@ -11,11 +11,11 @@ cfg=cd.PipelineConfig(hidden=d, ffn=2*inter, precision=cd.PrecisionMode.SIMBF16)
 w,a,c,s=bench.make_workload(cd,d,inter,m,0,dev)
 outs=[]
 for v in (0,1):
-    _native.set_option('st_direct',v)
+    _native.set_option("st_tma",1-v)
     f,b=bench.run_step(cd,cfg,w,a,c,s); torch.cuda.synchronize()
     outs.append({k:getattr(b,k).tensor.float().cpu().numpy() for k in ('x','z','w_out','w_gate_up','w_down','w_qkv','gamma_ffn','gamma_qkv')} | {'qkv':f.qkv.tensor.float().cpu().numpy()})
 print({k: bool(np.array_equal(outs[0][k],outs[1][k])) for k in outs[0]})
 PY
 cat gpurun_out/stdirect_check.txt
-python tools/ablate.py --variant st_direct=0 --variant st_direct=1 --variant st_direct=0 --variant st_direct=1 --rounds 6 > gpurun_out/stdirect_ab.txt 2>&1
+python tools/ablate.py --variant st_tma=1 --variant st_tma=0 --variant st_tma=1 --variant st_tma=0 --rounds 6 > gpurun_out/stdirect_ab.txt 2>&1
 tail -18 gpurun_out/stdirect_ab.txt
