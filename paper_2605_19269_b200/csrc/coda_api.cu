@@ -213,7 +213,11 @@ struct Options {
     int generic = 0;      // force the generic epilogue interpreter
     int raster = 8;       // raster group (pair m-tiles)
     int split = 1;        // split the partial last wave along K
-    int split_min_k = 8192;   // ... only for launches with at least this K (measured threshold)
+    // ... only for launches with at least this K, in pieces of at least split_piece_kb
+    // 64-wide k-blocks (profiles/r02_session3/split_ab: 4096 / 32 vs the round-2 8192 / 4:
+    // 4096^3 -1.5 %, 2048x28672x4096 -1.3 %, K10's shape -0.8 %, whole steps within noise)
+    int split_min_k = 4096;
+    int split_piece_kb = 32;
     int prefetch = 0;     // [experiments] L2 prefetch distance (k-blocks beyond the smem ring)
     int ablate = 0;       // [experiments] epilogue ablations (results invalid)
     int ring = 0;         // [experiments] operand ring stages in use (0 = the compiled depth)
@@ -465,7 +469,10 @@ int coda_set_option(const char* name, int value) {
         opts().cg = value;
     } else if (n == "generic") opts().generic = value != 0;
     else if (n == "split") opts().split = value != 0;
-    else if (n == "split_min_k") {
+    else if (n == "split_piece_kb") {
+        if (value < 1) return fail(CODA_E_CONFIG, "split_piece_kb must be >= 1");
+        opts().split_piece_kb = value;
+    } else if (n == "split_min_k") {
         if (value < 0) return fail(CODA_E_CONFIG, "split_min_k must be >= 0");
         opts().split_min_k = value;
     } else if (n == "raster") {
@@ -736,7 +743,7 @@ int gemm_impl(const coda_problem_t* pr, const coda_tensor_t* a, const coda_tenso
         if (!peer && opts().split && r > 0 && K >= opts().split_min_k && pr->workspace &&
             pr->workspace_bytes > (64 << 10)) {
             int sp = units / r;
-            if (sp > P.nk / 4) sp = P.nk / 4;
+            if (sp > P.nk / opts().split_piece_kb) sp = P.nk / opts().split_piece_kb;
             if (sp > 16) sp = 16;
             const int64_t tile_bytes = (int64_t)cg * coda::BM * coda::BN * 4;
             // every piece dumps its partial tile; one arrival counter per (tail tile, rank, warp)
