@@ -117,7 +117,8 @@ typedef struct {
  *   TARGET_GATHER  arg0 = operand (labels, int64), arg1 = store (gather, f32)
  *   ROPE           arg0 = cos operand, arg1 = sin operand, arg2 = backward flag,
  *                  arg3/arg4 = 1 + slot of compact (m, h/2) bf16 cos/sin tables or 0,
- *                  arg5 = h (q-span width; columns >= 2h are the identity)
+ *                  arg5 = h: column c < 2h rotates by angle (c mod h)/2, c >= 2h is the
+ *                  identity; 2h <= n (packed qkv, q-span width h) or h == n (a plain table)
  *   SWIGLU         —
  *   SWIGLU_BWD     arg0 = preact operand (factor 2), arg1 = recompute store,
  *                  arg2 = row-sum pieces store (factor 2), arg6 = row stream

@@ -639,12 +639,15 @@ int gemm_impl(const coda_problem_t* pr, const coda_tensor_t* a, const coda_tenso
             ok = opnd_ok(cs.arg[0]) && opnd_ok(cs.arg[1]) && w >= 2;
             if (ok && cs.arg[3] > 0) {   // compact tables: arg3/arg4 = 1 + operand slot, arg5 = q-span width h
                 const int h = cs.arg[5];
-                ok = opnd_ok(cs.arg[3] - 1) && opnd_ok(cs.arg[4] - 1) && h > 0 && h % 32 == 0 && 2 * (int64_t)h <= N;
+                // packed qkv (2h <= N: q and k share the h/2 angles, the rest is identity) or
+                // a plain table over the whole width (h == N: column c takes angle c / 2)
+                ok = opnd_ok(cs.arg[3] - 1) && opnd_ok(cs.arg[4] - 1) && h > 0 && h % 32 == 0 &&
+                     (2 * (int64_t)h <= N || (int64_t)h == N);
                 for (int j = 3; ok && j <= 4; ++j) {
                     const coda_tensor_t& t = operands[cs.arg[j] - 1];
                     ok = t.dtype == CODA_BF16 && t.rows == M && t.cols == h / 2;
                 }
-                if (!ok) return fail(CODA_E_BINDING, "step %d: compact RoPE tables must be bf16 (m, h/2), h %% 32 == 0", s);
+                if (!ok) return fail(CODA_E_BINDING, "step %d: compact RoPE tables must be bf16 (m, h/2), h %% 32 == 0, 2h <= n or h == n", s);
             }
             break;
         case CODA_OP_SWIGLU:

@@ -349,7 +349,9 @@ def run_gemm(
             if op != nat.OP_ROPE or len(descs) + 2 > nat.MAX_OPERANDS:
                 continue
             spec = rope_compact_of(bindings[onames[args[0]]], bindings[onames[args[1]]])
-            if spec is None or 2 * spec.hidden > p.n or spec.cos.shape[0] != p.m:
+            # the compact rule covers n columns when n >= 2 hidden (packed qkv) or n == hidden
+            # (a plain table over the whole width)
+            if spec is None or (2 * spec.hidden > p.n and spec.hidden != p.n) or spec.cos.shape[0] != p.m:
                 continue
             nops = len(descs)
             descs += [nat.tensor_desc(spec.cos), nat.tensor_desc(spec.sin)]

@@ -172,13 +172,22 @@ def rope_tables(m: int, width: int, *, base: float = 10000.0, start: int = 0,
         raise DimensionError(f"table rows must be positive, got {m}")
     ang = _angles(m, width, base, start)
     dev = default_device()
-    out = []
+    out, halves = [], []
     for fn in (np.cos, np.sin):
         half = torch.from_numpy(quantize(fn(ang), precision)).to(dev, dtype=precision.torch_dtype)
         full = alloc_matrix(m, width, precision.torch_dtype, dev)
         full[:, 0::2] = half
         full[:, 1::2] = half
         out.append(DenseMatrix._wrap(full, precision))
+        halves.append(half.contiguous())
+    if precision is PrecisionMode.SIMBF16 and width % 32 == 0:
+        # compact form (one angle per pair, half the bytes) for a rotation over exactly
+        # `width` columns: the RopeCompact rule with hidden = width maps column c < width
+        # to angle c // 2 (the fused forward epilogue; rope_backward_stat keeps the full
+        # tables for it)
+        spec = RopeCompact(cos=halves[0], sin=halves[1], hidden=width)
+        out[0]._rope = (spec, "cos")
+        out[1]._rope = (spec, "sin")
     return out[0], out[1]
 
 
@@ -216,7 +225,8 @@ class RopeCompact:
     """Compact packed-qkv RoPE tables: (m, hidden/2) bf16 cos/sin, one value per pair.
 
     Columns [0, 2*hidden) of the full table hold cos[:, (col % hidden) // 2] (q and k
-    spans share angles, kernels.py:184-206); columns >= 2*hidden are cos 1 / sin 0."""
+    spans share angles, kernels.py:184-206); columns >= 2*hidden are cos 1 / sin 0.
+    A plain `rope_tables(m, width)` pair is the case hidden = width = the table width."""
 
     cos: object
     sin: object

@@ -263,3 +263,31 @@ def test_compact_rope_roles_respected(cuda_ready):
         gz, _ = cd.rope_backward_stat(gq, gq, c, s, precision=P)
         ogz, _ = O.rope_backward_stat(gq.data, gq.data, c.data, s.data, O.SIMBF16)
         assert O.rel_error(gz.data, ogz) <= 1e-3
+
+
+@pytest.mark.parametrize("m,n", [(300, 512), (256, 96), (128, 4096)])
+@pytest.mark.parametrize("backward", [False, True])
+def test_plain_rope_tables_compact_bit_identical(cuda_ready, m, n, backward):
+    """rope_tables(m, width) attaches a compact (m, width/2) form (hidden = width); the
+    fused GEMM + PairwiseRope (K1, forward and backward rotation) loads it instead of
+    the full tables with bit-identical results, and rope_backward_stat, which keeps the
+    full tables for this layout, still runs."""
+    cd = _cd()
+    P = cd.PrecisionMode.SIMBF16
+    rng = np.random.default_rng(m + n)
+    a = cd.DenseMatrix.from_array(rng.standard_normal((m, 192)) / 8, P)
+    b = cd.DenseMatrix.from_array(rng.standard_normal((192, n)) / 8, P)
+    cos_c, sin_c = cd.rope_tables(m, n, start=3, precision=P)
+    spec = cd.kernels.rope_compact_of(cos_c, sin_c)
+    assert spec is not None and spec.hidden == n and spec.cos.shape == (m, n // 2)
+    cos_f, sin_f = cd.DenseMatrix.from_tensor(cos_c.tensor, P), cd.DenseMatrix.from_tensor(sin_c.tensor, P)
+    got = cd.gemm_rope(a, b, cos_c, sin_c, backward=backward, precision=P).main.data
+    want = cd.gemm_rope(a, b, cos_f, sin_f, backward=backward, precision=P).main.data
+    assert np.array_equal(got, want)
+    ref = O.k_rope(a.data, b.data, cos_f.data, sin_f.data, O.SIMBF16, backward=backward)["main"]
+    assert O.rel_error(got, ref) <= 2e-2
+    if not backward:
+        g = cd.DenseMatrix.from_array(rng.standard_normal((m, n)), P)
+        gz1, rd1 = cd.rope_backward_stat(g, cd.DenseMatrix.from_array(got, P), cos_c, sin_c, precision=P)
+        gz2, rd2 = cd.rope_backward_stat(g, cd.DenseMatrix.from_array(got, P), cos_f, sin_f, precision=P)
+        assert np.array_equal(gz1.data, gz2.data) and np.array_equal(rd1.data, rd2.data)
