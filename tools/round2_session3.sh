@@ -10,6 +10,7 @@ for t in 2048 4096 8192; do
   timeout -s KILL 300 python bench.py --tokens $t --no-cpu --no-parity --force-dist --graph \
     > $D/proxy_c4_${t}_dist_graph.json 2>/dev/null
 done
+python tools/primitive_sweep.py > $D/c2_primitive_sweep.jsonl 2>/dev/null
 timeout -s KILL 900 compute-sanitizer --tool memcheck python -m pytest tests/test_gpu_layer.py -q -x \
   -p no:cacheprovider > $D/memcheck.txt 2>&1; echo rc=$? >> $D/memcheck.txt
 tail -3 $D/memcheck.txt
