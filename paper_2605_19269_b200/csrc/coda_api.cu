@@ -225,7 +225,7 @@ struct Options {
     int persist = 1;      // [experiments] 0: one tile per cluster (non-persistent, hardware dispatch order)
     int wave_sync = 0;    // [experiments] soft wave barrier milestone in % of a tile's k-blocks (0 = off)
     int backoff = 0;      // [experiments] epilogue accumulator-wait sleep (ns)
-    int st_tma = 0;       // [experiments] staged epilogue stores by TMA instead of coalesced st.global
+    int st_tma = -1;      // staged epilogue stores: -1 per-launch choice, 0 lanes' copy-out, 1 TMA
     Options() {
         if (const char* e = getenv("CODA_PDL")) pdl = e[0] != '0';
         if (const char* e = getenv("CODA_CG")) cg = e[0] == '1' ? 1 : 2;
@@ -475,6 +475,9 @@ int coda_set_option(const char* name, int value) {
     } else if (n == "split_min_k") {
         if (value < 0) return fail(CODA_E_CONFIG, "split_min_k must be >= 0");
         opts().split_min_k = value;
+    } else if (n == "st_tma") {
+        if (value < -1 || value > 1) return fail(CODA_E_CONFIG, "st_tma must be -1, 0 or 1");
+        opts().st_tma = value;
     } else if (n == "raster") {
         if (value < 1) return fail(CODA_E_CONFIG, "raster group must be >= 1");
         opts().raster = value;
@@ -486,7 +489,6 @@ int coda_set_option(const char* name, int value) {
     else if (n == "persist") opts().persist = value;
     else if (n == "wave_sync") opts().wave_sync = value;
     else if (n == "backoff") opts().backoff = value;
-    else if (n == "st_tma") opts().st_tma = value;
     else if (n == "prefetch") {
         if (value < 0 || value > 64) return fail(CODA_E_CONFIG, "prefetch distance must be in [0, 64]");
         opts().prefetch = value;
@@ -785,9 +787,9 @@ int gemm_impl(const coda_problem_t* pr, const coda_tensor_t* a, const coda_tenso
         F.ld_acc = P.ld_acc;
         F.ablate = opts().ablate;
         F.backoff = opts().backoff;
-#ifdef CODA_EXPERIMENTS
-        F.st_tma = opts().st_tma;
-#endif
+        // epilogue store path: the lanes' coalesced copy-out, except the SwiGLU backward
+        // (three boxes per chunk) on a short mainloop, where the TMA engine is cheaper
+        F.st_tma = opts().st_tma >= 0 ? opts().st_tma : ((fl & coda::F_SWIGLU_BWD) && K < 4096 ? 1 : 0);
         F.rope_sign = 1.0f;
         const void* rope_c = nullptr;
         const void* rope_s = nullptr;

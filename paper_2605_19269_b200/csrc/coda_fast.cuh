@@ -113,9 +113,7 @@ struct FastParams {
     int64_t st_main_ld, st_main_cols;
     void* st_aux;
     int64_t st_aux_ld, st_aux_cols;
-#ifdef CODA_EXPERIMENTS
-    int st_tma;   // [experiments] staged boxes leave smem by TMA store (round-2 path)
-#endif
+    int st_tma;   // staged boxes leave smem by TMA store instead of the lanes' copy-out (host choice)
     // deferred finalizers (coda_step_t.fin_*): the RowScale vector / the RMSNorm-backward
     // stat computed per row from (M, nb) f32 partials and written back by the tn == 0 tiles
     const float* rs_fin;
@@ -357,14 +355,15 @@ __device__ __forceinline__ void fload_vec_cg(const float* vp, int64_t c0, int64_
 // events) K10 (1.41 GB of output) drops 1.70 -> 1.62 ms, K6 -1.3 %, the sum of the C4
 // launches -4 %; in the PDL-chained step the old path's tails were already hidden and
 // the step time is unchanged (profiles/r02_session3/stdirect_ab.txt, ab_copyout.txt).
-// The TMA path stays as the experiment option st_tma.
+// The TMA path stays for the one launch where the lanes' copy-out costs more than it
+// saves: the width-doubling SwiGLU backward (three boxes per chunk) on a short mainloop
+// (K < 4096: C3's K10 0.274 ms with TMA stores vs 0.296 ms, profiles/r02_session3/
+// ablate_sttma_c3.txt); the host sets FastParams::st_tma (option "st_tma" forces it).
 struct Stager {
     uint32_t base;      // smem address of this warp's 4 KiB buffer (1024-aligned)
     int region;
     bool skip;          // ablation: stage into smem but store nothing
-#ifdef CODA_EXPERIMENTS
-    bool tma;           // [experiments] st_tma: boxes leave smem by TMA store
-#endif
+    bool tma;           // boxes leave smem by TMA store (FastParams::st_tma)
 };
 
 // AUX: the destination is the AuxTileStore output (P.st_aux), else the main output; its
@@ -375,10 +374,8 @@ struct Stager {
 template <typename TO, int RB>
 __device__ __forceinline__ uint32_t stage_box(Stager& sg, const float* v, int lane) {
     constexpr uint32_t MASK = RB == 64 ? 0x30u : 0x10u;
-#ifdef CODA_EXPERIMENTS
-    // the region we are about to overwrite was read by the TMA store before last
+    // TMA path: the region we are about to overwrite was read by the store before last
     if (sg.tma && lane == 0) bulk_wait_read<1>();
-#endif
     // every lane's copy-out reads of this region (two boxes ago) are done
     __syncwarp();
     const uint32_t rbase = sg.base + (uint32_t)(sg.region * 2048);
@@ -463,7 +460,6 @@ __device__ __forceinline__ void staged_store(Stager& sg, const FastParams& P, co
         staged_store<TO, W / 2, AUX>(sg, P, tm, x + W / 2, y, v + W / 2, lane);
     } else {
         const uint32_t rbase = stage_box<TO, RB>(sg, v, lane);
-#ifdef CODA_EXPERIMENTS
         if (sg.tma) {
             fence_proxy_async_smem();
             __syncwarp();
@@ -473,7 +469,6 @@ __device__ __forceinline__ void staged_store(Stager& sg, const FastParams& P, co
             }
             return;
         }
-#endif
         __syncwarp();
         copy_box<TO, RB, AUX>(sg, P, rbase, x, y, lane);
     }
@@ -578,11 +573,7 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         const int h = ew >> 2;              // column half of the 256-wide tile
         const int lrow = q * 32 + lane;
         const int M = mp.M, N = mp.N;
-#ifdef CODA_EXPERIMENTS
         Stager sg{smem_u32(stg + ew * STG_BYTES), 0, (P.ablate & 2) != 0, P.st_tma != 0};
-#else
-        Stager sg{smem_u32(stg + ew * STG_BYTES), 0, (P.ablate & 2) != 0};
-#endif
         int cbuf = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -958,11 +949,8 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     }
                     // the normed aux box is staged now and copied out after the main store,
                     // when only the outputs are live
-#ifdef CODA_EXPERIMENTS
                     if (sg.tma) staged_store<TS, 32, true>(sg, P, &tma_aux, gcol0, m0 + q * 32, tmp, lane);
-                    else
-#endif
-                    staged_defer<TS, 32>(sg, tmp, lane);
+                    else staged_defer<TS, 32>(sg, tmp, lane);
                     // gamma again (L1-resident; an L2-hinted load the compiler does not merge with
                     // the first), so it is not held live across the staging
                     fload_vec_cg<32>(P.gamma, gcol0, N, g);
@@ -1002,10 +990,7 @@ coda_gemm_fast(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     }
                     cbuf ^= 1;
                     if (FL & F_STORE_MAIN) staged_store<TS, 32>(sg, P, &tma_main, gcol0, m0 + q * 32, v, lane);
-#ifdef CODA_EXPERIMENTS
-                    if (!sg.tma)
-#endif
-                    {
+                    if (!sg.tma) {
                         // the aux box sits in the region before the current one, or in the one
                         // before that when the main store went between (two regions)
                         const int r = (FL & F_STORE_MAIN) ? sg.region : sg.region ^ 1;
