@@ -280,7 +280,9 @@ int coda_gemm_peer_reduce(const coda_problem_t* problem, const coda_tensor_t* a,
  * mainloop, "generic" 0/1 force the generic epilogue interpreter, "raster" >= 1
  * raster group, "split" 0/1 wave-tail split-K, "split_min_k" the smallest K that
  * is split (default 4096) and "split_piece_kb" the fewest 64-wide k-blocks per piece
- * (default 32) (splitting changes only the deterministic f32 accumulation order).
+ * (default 32) (splitting changes only the deterministic f32 accumulation order),
+ * "st_tma" -1 / 0 / 1 the epilogue store path (-1 per launch: coalesced lane stores,
+ * TMA stores for the SwiGLU backward with K < 4096; 0 / 1 force one; same bits).
  * Process-wide.  Measurement knobs ("ring", "prefetch", "ablate" — the last makes
  * results invalid) exist only in experiment builds (-DCODA_EXPERIMENTS) and return
  * CODA_E_CONFIG from the product library. */
