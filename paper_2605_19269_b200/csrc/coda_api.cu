@@ -964,7 +964,7 @@ int coda_reduce_row_partials(const float* p, int64_t tm, int64_t n, int64_t ld, 
     int rc;
     DeviceGuard dg;
     if ((rc = bind_device(p, dg))) return rc;
-    return launch_pdl(coda::coda_reduce_row_partials_kernel, dim3(grid1d(n, 256)), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_reduce_row_partials_kernel",
+    return launch_pdl(coda::coda_reduce_row_partials_kernel, dim3(grid1d(n, 64)), dim3(64), 0, (cudaStream_t)stream, 1, "coda::coda_reduce_row_partials_kernel",
         p, tm, n, ld, out);
 }
 
@@ -973,7 +973,7 @@ int coda_combine_lse(const float* p, int64_t m, int64_t nb, int64_t ld, float* l
     int rc;
     DeviceGuard dg;
     if ((rc = bind_device(p, dg))) return rc;
-    return launch_pdl(coda::coda_combine_lse_kernel, dim3(grid1d(m, 256)), dim3(256), 0, (cudaStream_t)stream, 1, "coda::coda_combine_lse_kernel",
+    return launch_pdl(coda::coda_combine_lse_kernel, dim3(grid1d(m, 64)), dim3(64), 0, (cudaStream_t)stream, 1, "coda::coda_combine_lse_kernel",
         p, m, nb, ld, lse);
 }
 

@@ -78,15 +78,24 @@ __global__ void coda_finalize_rowdot_wide_kernel(const float* __restrict__ p, in
     s[i] = __fdiv_rn(t, d);
 }
 
-// Column totals over tile rows (coalesced: one thread per column).
-__global__ void coda_reduce_row_partials_kernel(const float* __restrict__ p, int64_t tm, int64_t n, int64_t ld,
-                                           float* __restrict__ out) {
+// Column totals over tile rows (coalesced: one thread per column), summed in ascending
+// row order; 16 rows of loads are issued ahead of each run of sequential adds.
+__global__ void __launch_bounds__(64) coda_reduce_row_partials_kernel(const float* __restrict__ p, int64_t tm,
+                                                                      int64_t n, int64_t ld, float* __restrict__ out) {
     griddep_wait();
     griddep_launch_dependents();
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     float t = 0.0f;
-    for (int64_t b = 0; b < tm; ++b) t = __fadd_rn(t, p[b * ld + j]);
+    int64_t b = 0;
+    for (; b + 16 <= tm; b += 16) {
+        float x[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) x[k] = __ldg(p + (b + k) * ld + j);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) t = __fadd_rn(t, x[k]);
+    }
+    for (; b < tm; ++b) t = __fadd_rn(t, p[b * ld + j]);
     out[j] = t;
 }
 
@@ -98,14 +107,44 @@ __device__ __forceinline__ void lse_merge(float& m, float& s, float mb, float sb
     m = mn;
 }
 
-__global__ void coda_combine_lse_kernel(const float* __restrict__ p, int64_t m, int64_t nb, int64_t ld,
-                                   float* __restrict__ lse) {
+// One thread per row, blocks merged strictly in ascending order (reductions.py:101-131).
+// The merge chain is sequential, so the loads run ahead of it: 8 (max, sum) pairs per
+// chunk as four 16-B loads, the next chunk in flight while the current one is merged
+// (one row at a time and one pair per iteration, the round-1 loop waited on every load:
+// 74 us for the LM head's 16384 x 256 pairs, 33.5 MB).
+__global__ void __launch_bounds__(64) coda_combine_lse_kernel(const float* __restrict__ p, int64_t m, int64_t nb,
+                                                              int64_t ld, float* __restrict__ lse) {
     griddep_wait();
     griddep_launch_dependents();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
+    const float* row = p + i * ld;
     float mx = -INFINITY, s = 0.0f;
-    for (int64_t b = 0; b < nb; ++b) lse_merge(mx, s, p[i * ld + 2 * b], p[i * ld + 2 * b + 1]);
+    int64_t b = 0;
+    if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+        const float4* v = reinterpret_cast<const float4*>(row);
+        const int64_t nc = nb / 8;   // whole chunks of 8 pairs
+        float4 cur[4], nxt[4];
+        if (nc > 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cur[k] = __ldg(v + k);
+        }
+        for (int64_t c = 0; c < nc; ++c) {
+            if (c + 1 < nc) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) nxt[k] = __ldg(v + 4 * (c + 1) + k);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                lse_merge(mx, s, cur[k].x, cur[k].y);
+                lse_merge(mx, s, cur[k].z, cur[k].w);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cur[k] = nxt[k];
+        }
+        b = nc * 8;
+    }
+    for (; b < nb; ++b) lse_merge(mx, s, row[2 * b], row[2 * b + 1]);
     lse[i] = (mx == -INFINITY) ? NAN : mx + logf(s);
 }
 
