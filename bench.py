@@ -969,7 +969,7 @@ def main(argv=None):
     ap.add_argument("--ncu", action="store_true", help="profiling pass only (no timing / JSON line)")
     ap.add_argument("--graph", action="store_true", default=None,
                     help="replay each step (device-timed, weak-scaling and e2e loops) as one captured CUDA graph "
-                         "(default: on when N > 1, where the host enqueue of a strong-scaled step would "
+                         "(default: on when N > 1 and for C1, where the host enqueue of a step would "
                          "otherwise exceed its device time)")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
     ap.add_argument("--force-dist", action="store_true",
@@ -990,8 +990,8 @@ def main(argv=None):
     if world != args.gpus:
         print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr, flush=True)
         return 2
-    if args.graph is None:
-        args.graph = world > 1
+    if args.graph is None:   # host-enqueue-bound steps: the strong-scaled ranks and the tiny C1 block
+        args.graph = world > 1 or args.config == "c1"
     if args.launcher_check:
         launcher_check(args, rank, world)
     elif args.impl == "reference":
