@@ -185,7 +185,7 @@ def test_library_is_sm100a_tcgen05():
     out = subprocess.run(["cuobjdump", "-sass", str(nat.LIB_PATH)], capture_output=True, text=True).stdout
     assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", str(nat.LIB_PATH)], capture_output=True,
                                        text=True).stdout
-    for mnemonic in ("UTCHMMA", "UTMALDG", "LDTM"):   # stores: coalesced st.global copy-out
+    for mnemonic in ("UTCHMMA", "UTMALDG", "UTMASTG", "LDTM"):
         assert mnemonic in out, mnemonic
 
 
