@@ -353,8 +353,8 @@ __device__ __forceinline__ void fload_vec_cg(const float* vp, int64_t c0, int64_
 // issues the mainloop's operand loads, and every launch ended draining its stores.
 // The coalesced copy-out is bit-identical; launched one at a time (per-launch CUDA
 // events) K10 (1.41 GB of output) drops 1.70 -> 1.62 ms, K6 -1.3 %, the sum of the C4
-// launches -4 %; in the PDL-chained step the old path's tails were already hidden and
-// the step time is unchanged (profiles/r02_session3/stdirect_ab.txt, ab_copyout.txt).
+// launches -4 %; in the PDL-chained step most of that was already hidden and the step
+// gains 0.7-1.2 % (profiles/r02_session3/stdirect_ab.txt, ab_store_path_c4_interleaved.jsonl).
 // The TMA path stays for the one launch where the lanes' copy-out costs more than it
 // saves: the width-doubling SwiGLU backward (three boxes per chunk) on a short mainloop
 // (K < 4096: C3's K10 0.274 ms with TMA stores vs 0.296 ms, profiles/r02_session3/
