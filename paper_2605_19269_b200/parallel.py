@@ -76,10 +76,18 @@ class WgradAllReduce:
             import torch
 
             self.side = torch.cuda.Stream(device)
+        # names reduced in the current (or, after wait(), the last) step, in order
         self.names: list[str] = []
+        self._joined = False
+
+    def _note(self, name: str) -> None:
+        if self._joined:           # a new step: keep only this step's names (bounded)
+            self.names.clear()
+            self._joined = False
+        self.names.append(name)
 
     def __call__(self, name: str, tensor) -> None:
-        self.names.append(name)
+        self._note(name)
         if self.side is None:
             self.dist.all_reduce(tensor)
             return
@@ -103,6 +111,7 @@ class WgradAllReduce:
             self._capped.__enter__()
 
     def wait(self) -> None:
+        self._joined = True
         if self.side is not None:
             import torch
 
@@ -148,7 +157,7 @@ class WgradReduceScatter(WgradAllReduce):
 
         if self.side is not None or not self._splits(tensor):
             return super().__call__(name, tensor)
-        self.names.append(name)
+        self._note(name)
         flat = tensor.view(-1)
         shard = torch.empty(flat.numel() // self.world, dtype=tensor.dtype)
         self.dist.reduce_scatter_tensor(shard, flat)
@@ -166,7 +175,7 @@ class WgradReduceScatter(WgradAllReduce):
 
         from . import _native as nat
 
-        self.names.append(name)
+        self._note(name)
         self._cap()
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(tensor.device))
@@ -272,7 +281,7 @@ class PeerWgradReduce(WgradAllReduce):
         nat.call("coda_gemm_peer_reduce", ctypes.byref(prob), ctypes.byref(nat.tensor_desc(a.tensor)),
                  ctypes.byref(nat.tensor_desc(b.tensor)), ctypes.byref(reg["desc"]), stream,
                  tag=f"gemm_peer_reduce {m}x{n}x{k} TN", flops=2.0 * m * n * k)
-        self.names.append(name)
+        self._note(name)
         self._pending = True
         return DenseMatrix._wrap(reg["out"], precision)
 

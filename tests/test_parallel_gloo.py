@@ -183,3 +183,23 @@ def test_reduce_scatter_hook_protocol():
     assert torch.equal(u, torch.full((4, 6), 2.0)) and hook.reduced("w_qkv") is None
     src = inspect.getsource(kernels.layer_backward)
     assert 'getattr(wgrad_hook, "reduce_unrounded", None) if f32 else None' in src
+
+
+def test_hook_names_are_per_step():
+    """A long run must not grow the hook's name list: after wait() the next reduction
+    starts a new step's list."""
+    import torch
+
+    sys.path.insert(0, str(ROOT))
+    from paper_2605_19269_b200 import parallel
+
+    class FakeDist:
+        def all_reduce(self, t):
+            pass
+
+    hook = parallel.WgradAllReduce(FakeDist())
+    for step in range(3):
+        for name in parallel.REDUCED:
+            hook(name, torch.zeros(2))
+        hook.wait()
+        assert hook.names == list(parallel.REDUCED), step
