@@ -155,8 +155,9 @@ class ClockSampler:
                     out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                          timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([x.strip() for x in out.split(",")])
+                    fields = [x.strip() for x in out.split(",")] if out else []
+                    if len(fields) == 6:          # an error message is not a sample
+                        self.samples.append(fields)
                 except Exception:
                     pass
                 self._stop.wait(0.2)
@@ -173,8 +174,8 @@ class ClockSampler:
     def summary(self) -> dict:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and
                           s[2 + i].lower() in ("active", "1")})
@@ -516,10 +517,16 @@ def coda_arm(args, rank, world, local_rank):
     import paper_2605_19269_b200 as cd
     from paper_2605_19269_b200 import _native
 
-    device = torch.device("cuda", local_rank)
+    device = torch.device("cuda", 0 if args.share_gpu else local_rank)
     torch.cuda.set_device(device)
     dist = None
-    if world > 1 or args.force_dist:
+    if world > 1 and args.share_gpu:
+        # test mode: every rank on cuda:0 over gloo (NCCL needs one GPU per rank); the
+        # collectives stage through the host, so nothing here is a measurement
+        import torch.distributed as dist  # noqa: F811
+
+        dist.init_process_group("gloo")
+    elif world > 1 or args.force_dist:
         import torch.distributed as dist  # noqa: F811
 
         comm = args.comm_sms if args.comm_sms is not None else (DEFAULT_COMM_SMS if world > 1 else 0)
@@ -629,7 +636,7 @@ def coda_arm(args, rank, world, local_rank):
             step()
         barrier()
     launches0 = _native.launch_count()
-    with clock_sampler(local_rank) as clocks:
+    with clock_sampler(device.index) as clocks:
         barrier()
         h0 = time.perf_counter()
         e0.record(stream)
@@ -903,6 +910,7 @@ def coda_arm(args, rank, world, local_rank):
             "comm_sms": comm_sms if dist is not None else 0,
             "wgrad_allreduce_dtype": args.wgrad_dtype if dist is not None else None,
             "wgrad_reduce": (type(hook).__name__ if hook is not None else None),
+            "share_gpu": bool(args.share_gpu),
             "fold_gamma": bool(args.fold_gamma),
             "launch_breakdown_ms": {k: round(v["avg_ms"], 4) for k, v in (prof or {}).items()},
         }
@@ -924,7 +932,7 @@ def spawn(args, argv) -> int:
     torch.distributed.run (one process per GPU, 127.0.0.1 rendezvous) and return its exit
     code.  Fails loudly when fewer than N CUDA devices are visible (unless --launcher-check,
     which runs the launch / rendezvous / all-reduce / max-over-ranks machinery on CPU)."""
-    if not args.launcher_check:
+    if not args.launcher_check and not args.share_gpu:
         import torch
 
         have = torch.cuda.device_count()
@@ -974,6 +982,9 @@ def main(argv=None):
     ap.add_argument("--no-graph", dest="graph", action="store_false")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the NCCL wgrad all-reduce path even at world size 1 (collective overlap check)")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="test mode: N ranks share cuda:0 over gloo (the multi-rank bench path on a one-GPU "
+                         "box; no CUDA graphs, all-reduce hook; not a measurement)")
     ap.add_argument("--launcher-check", action="store_true",
                     help="CPU/gloo check of the multi-rank launch: rendezvous, the per-step weight-gradient "
                          "all-reduce of this config's shapes, max-over-ranks timing and the rank-0 JSON line "
@@ -991,7 +1002,12 @@ def main(argv=None):
         print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr, flush=True)
         return 2
     if args.graph is None:   # host-enqueue-bound steps: the strong-scaled ranks and the tiny C1 block
-        args.graph = world > 1 or args.config == "c1"
+        args.graph = (world > 1 or args.config == "c1") and not args.share_gpu
+    if args.share_gpu:
+        if args.graph:
+            print("bench.py: --share-gpu runs gloo collectives, which CUDA graphs cannot capture", file=sys.stderr)
+            return 2
+        args.wgrad_reduce = "allreduce"
     if args.launcher_check:
         launcher_check(args, rank, world)
     elif args.impl == "reference":

@@ -60,3 +60,17 @@ def test_bench_line_graph_with_collectives(cuda_ready):
     assert out["host_enqueue_ms_per_step"] < 0.5
     assert out["gpu_launches"] > 3 * 15            # the block's kernels plus the slice roundings
     assert out["value"] > 0 and out["e2e"]["value"] > 0
+
+
+def test_bench_two_ranks_share_one_gpu(cuda_ready):
+    """The multi-rank bench path on a one-GPU box: --gpus 2 spawns two ranks (torchrun,
+    127.0.0.1 rendezvous), both on cuda:0 over gloo, token-sharded C4 with the weight-
+    gradient hook, max-over-ranks timing, the weak-scaling extra and the e2e loop; rank 0
+    prints one line with n_gpus 2 (a functional check, not a measurement)."""
+    out = _bench("--gpus", "2", "--share-gpu", "--tokens", "2048", "--steps", "3", "--warmup", "3", "--no-cpu",
+                 "--no-parity", "--ab-rounds", "0")
+    assert out["n_gpus"] == 2 and out["share_gpu"] is True and out["scaling"] == "strong"
+    assert out["config"]["tokens_per_gpu"] == 1024 and out["config"]["global_tokens"] == 2048
+    assert out["wgrad_reduce"] == "WgradAllReduce" and out["cuda_graph"] is False
+    assert out["value"] > 0 and out["e2e"]["value"] > 0
+    assert out["weak_scaling"]["global_tokens"] == 4096 and out["weak_scaling"]["value"] > 0
