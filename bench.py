@@ -685,7 +685,8 @@ def coda_arm(args, rank, world, local_rank):
     # ---- the other reading of the config text: weak scaling (the config's tokens on EVERY rank),
     # reported beside the strong-scaled headline for N > 1
     weak = None
-    if world > 1 and args.scaling == "strong":
+    # (also under --force-dist at world size 1, so the one-GPU tests exercise this path)
+    if (world > 1 or args.force_dist) and args.scaling == "strong":
         ww, wa, wc, wsn = make_workload(cd, d, inter, tokens, rank * tokens, device, blocks=nblocks, fp32=fp32,
                                         kv=kv)
 

@@ -60,6 +60,7 @@ def test_bench_line_graph_with_collectives(cuda_ready):
     assert out["host_enqueue_ms_per_step"] < 0.5
     assert out["gpu_launches"] > 3 * 15            # the block's kernels plus the slice roundings
     assert out["value"] > 0 and out["e2e"]["value"] > 0
+    assert out["weak_scaling"]["cuda_graph"] is True and out["weak_scaling"]["value"] > 0
 
 
 def test_bench_two_ranks_share_one_gpu(cuda_ready):
