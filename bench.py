@@ -331,6 +331,36 @@ class NullReduce:
         self.names.append(name)
 
 
+def _fixture_weights(cd, w, dev):
+    return cd.LayerWeights(w_out=upload_bf16(cd, w["w_out"], dev), gamma_ffn=upload_vec(cd, w["gamma_ffn"], dev),
+                           w_gate_up=upload_bf16(cd, w["w_gate_up"], dev), w_down=upload_bf16(cd, w["w_down"], dev),
+                           gamma_qkv=upload_vec(cd, w["gamma_qkv"], dev), w_qkv=upload_bf16(cd, w["w_qkv"], dev))
+
+
+def _fixture_compare(z, got: dict, dev) -> dict:
+    """Each output against the fixture: exact (small outputs) or sketch + norm + sampled rows."""
+    import numpy as np
+    import torch
+
+    from oracle import fullsize as FS
+
+    out = {}
+    for k in got:
+        t = got[k].tensor
+        if f"{k}__full" in z.files:
+            out[k] = FS.compare(k, t.double().cpu().numpy(), {"full": z[f"{k}__full"]})
+            continue
+        fp = {"sketch": z[f"{k}__sketch"].astype(np.float64), "rows": z[f"{k}__rows"].astype(np.float64),
+              "row_idx": z[f"{k}__row_idx"]}
+        S = torch.from_numpy(FS.sketch_matrix(k, t.shape[0], fp["sketch"].shape[0])).to(dev, torch.float64)
+        gs = (S @ t.double()).cpu().numpy()
+        gr = t[torch.from_numpy(fp["row_idx"]).to(dev)].double().cpu().numpy()
+        out[k] = FS.compare(k, None, fp, got_sketch=gs, got_rows=gr)
+        gnorm = float(torch.linalg.vector_norm(t.double()))
+        out[k]["norm_ratio"] = gnorm / float(z[f"{k}__norm"])
+    return out
+
+
 def fullsize_parity(name: str, variant: str = "plain") -> dict:
     """Full-size parity of config `name` (c3 / c4, or the c5 4-block stack) on cuda:0 against the
     committed oracle fixture tests/golden/fullsize_<name>.npz (made by
@@ -348,19 +378,12 @@ def fullsize_parity(name: str, variant: str = "plain") -> dict:
     z = np.load(ROOT / "tests" / "golden" / f"fullsize_{name}.npz")
     dev = torch.device("cuda", 0)
     P = cd.PrecisionMode.SIMBF16
-
-    def weights(w):
-        return cd.LayerWeights(w_out=upload_bf16(cd, w["w_out"], dev), gamma_ffn=upload_vec(cd, w["gamma_ffn"], dev),
-                               w_gate_up=upload_bf16(cd, w["w_gate_up"], dev),
-                               w_down=upload_bf16(cd, w["w_down"], dev),
-                               gamma_qkv=upload_vec(cd, w["gamma_qkv"], dev), w_qkv=upload_bf16(cd, w["w_qkv"], dev))
-
     if name in FS.BLOCKS:
         ws_np, acts_np = FS.make_stack_inputs(name, seed=int(z["meta_seed"]))
-        ws = [weights(w) for w in ws_np]
+        ws = [_fixture_weights(cd, w, dev) for w in ws_np]
     else:
         acts_np = FS.make_inputs(name, seed=int(z["meta_seed"]))
-        ws = weights(FS.weights_of(acts_np))
+        ws = _fixture_weights(cd, FS.weights_of(acts_np), dev)
     acts = {k: upload_bf16(cd, acts_np[k], dev) for k in ("x", "z", "grad_qkv", "grad_residual")}
     del acts_np
     m, d = acts["x"].shape
@@ -384,21 +407,40 @@ def fullsize_parity(name: str, variant: str = "plain") -> dict:
         got = {"qkv": fwd.qkv, "residual": fwd.residual}
         got.update({k: getattr(bwd, k) for k in O.GRAD_KEYS})
     torch.cuda.synchronize()
-    out = {}
-    for k in got:
-        t = got[k].tensor
-        if f"{k}__full" in z.files:
-            out[k] = FS.compare(k, t.double().cpu().numpy(), {"full": z[f"{k}__full"]})
-            continue
-        fp = {"sketch": z[f"{k}__sketch"].astype(np.float64), "rows": z[f"{k}__rows"].astype(np.float64),
-              "row_idx": z[f"{k}__row_idx"]}
-        S = torch.from_numpy(FS.sketch_matrix(k, t.shape[0], fp["sketch"].shape[0])).to(dev, torch.float64)
-        gs = (S @ t.double()).cpu().numpy()
-        gr = t[torch.from_numpy(fp["row_idx"]).to(dev)].double().cpu().numpy()
-        out[k] = FS.compare(k, None, fp, got_sketch=gs, got_rows=gr)
-        gnorm = float(torch.linalg.vector_norm(t.double()))
-        out[k]["norm_ratio"] = gnorm / float(z[f"{k}__norm"])
-    return out
+    return _fixture_compare(z, got, dev)
+
+
+def fullsize_parity_dp(name: str, hook, rank: int, world: int, device) -> dict:
+    """Data-parallel full-size parity (c3 / c4): every rank runs its strong-scaling token shard
+    of the fixture's inputs (RoPE tables at the shard's positions) through layer_forward /
+    layer_backward with the bench's weight-gradient hook; after the cross-rank reduction
+    the weight and gain gradients must equal the whole batch's, so they are compared with
+    the single-GPU fixture.  Collective: every rank calls it."""
+    import numpy as np
+    import torch
+
+    import paper_2605_19269_b200 as cd
+    from oracle import fullsize as FS
+    from paper_2605_19269_b200 import parallel
+
+    z = np.load(ROOT / "tests" / "golden" / f"fullsize_{name}.npz")
+    P = cd.PrecisionMode.SIMBF16
+    acts_np = FS.make_inputs(name, seed=int(z["meta_seed"]))
+    ws = _fixture_weights(cd, FS.weights_of(acts_np), device)
+    sh = parallel.shard(acts_np["x"].shape[0], rank, world, "strong")
+    acts = {k: upload_bf16(cd, np.ascontiguousarray(acts_np[k][sh.start:sh.stop]), device)
+            for k in ("x", "z", "grad_qkv", "grad_residual")}
+    del acts_np
+    d = acts["x"].shape[1]
+    cfg = cd.PipelineConfig(hidden=d, ffn=ws.w_gate_up.cols, precision=P)
+    cos, sin = cd.qkv_rope_tables(sh.rows, d, start=sh.start, precision=P)
+    fwd = cd.layer_forward(acts["x"], acts["z"], ws, cos, sin, config=cfg)
+    bwd = cd.layer_backward(acts["grad_qkv"], fwd.tape, ws, grad_residual=acts["grad_residual"], config=cfg,
+                            wgrad_hook=hook)
+    if hook is not None and hasattr(hook, "wait"):
+        hook.wait()
+    torch.cuda.synchronize()
+    return _fixture_compare(z, {k: getattr(bwd, k) for k in parallel.REDUCED}, device)
 
 
 def fullsize_summary(res: dict, tol: float = 2e-2) -> dict:
@@ -880,6 +922,17 @@ def coda_arm(args, rank, world, local_rank):
             (ROOT / "tests" / "golden" / f"fullsize_{args.config}.npz").exists():
         # the measured configuration itself, every output, against the pinned oracle (not timed)
         fullsize = fullsize_summary(fullsize_parity(args.config, "fold" if args.fold_gamma else "plain"))
+    elif world > 1 and dist is not None and hook is not None and not args.no_parity and args.tokens is None and \
+            args.scaling == "strong" and not fp32 and not args.fold_gamma and args.config in ("c3", "c4") and \
+            (ROOT / "tests" / "golden" / f"fullsize_{args.config}.npz").exists():
+        # every rank runs its shard of the fixture's batch; the reduced weight and gain gradients
+        # must equal the single-GPU oracle's (not timed; a collective, so all ranks take part)
+        res = fullsize_parity_dp(args.config, hook, rank, world, device)
+        if rank == 0:
+            fullsize = fullsize_summary(res)
+            fullsize["vs"] = (f"token-chunked fused-order CPU oracle of the whole block: the {len(res)} weight and "
+                              f"gain gradients after the {world}-rank {type(hook).__name__} reduction of "
+                              "token-sharded backward passes (sketch + sampled rows)")
 
     if rank == 0:
         line = {

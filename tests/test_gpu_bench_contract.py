@@ -75,3 +75,13 @@ def test_bench_two_ranks_share_one_gpu(cuda_ready):
     assert out["wgrad_reduce"] == "WgradAllReduce" and out["cuda_graph"] is False
     assert out["value"] > 0 and out["e2e"]["value"] > 0
     assert out["weak_scaling"]["global_tokens"] == 4096 and out["weak_scaling"]["value"] > 0
+
+
+def test_bench_two_ranks_full_size_dp_parity(cuda_ready):
+    """Two token-sharded ranks on one GPU (gloo) run the full C4 fixture batch, 8192 tokens
+    each; after the weight-gradient reduction the six reduced gradients match the
+    single-GPU full-size oracle fixture (bf16 bar 2e-2)."""
+    out = _bench("--gpus", "2", "--share-gpu", "--steps", "3", "--warmup", "3", "--no-cpu", "--ab-rounds", "0")
+    pf = out["parity_fullsize"]
+    assert pf is not None and pf["outputs"] == 6 and pf["pass"] is True, pf
+    assert pf["rel_err_max"] <= 2e-2
