@@ -234,6 +234,7 @@ struct Options {
         if (const char* e = getenv("CODA_SPLIT")) split = e[0] != '0';
 #ifdef CODA_EXPERIMENTS
         if (const char* e = getenv("CODA_PREFETCH")) prefetch = atoi(e);
+        if (const char* e = getenv("CODA_WAVE_SYNC")) wave_sync = atoi(e);
 #endif
     }
 };
