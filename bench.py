@@ -918,13 +918,10 @@ def coda_arm(args, rank, world, local_rank):
                          f"best of {reps} ({secs:.2f} s each)"}
 
     fullsize = None
-    if rank == 0 and world == 1 and not args.no_parity and args.tokens is None and \
-            (ROOT / "tests" / "golden" / f"fullsize_{args.config}.npz").exists():
-        # the measured configuration itself, every output, against the pinned oracle (not timed)
-        fullsize = fullsize_summary(fullsize_parity(args.config, "fold" if args.fold_gamma else "plain"))
-    elif world > 1 and dist is not None and hook is not None and not args.no_parity and args.tokens is None and \
+    have_fixture = (ROOT / "tests" / "golden" / f"fullsize_{args.config}.npz").exists()
+    if dist is not None and hook is not None and not args.no_parity and args.tokens is None and \
             args.scaling == "strong" and not fp32 and not args.fold_gamma and args.config in ("c3", "c4") and \
-            (ROOT / "tests" / "golden" / f"fullsize_{args.config}.npz").exists():
+            have_fixture:
         # every rank runs its shard of the fixture's batch; the reduced weight and gain gradients
         # must equal the single-GPU oracle's (not timed; a collective, so all ranks take part)
         res = fullsize_parity_dp(args.config, hook, rank, world, device)
@@ -933,6 +930,9 @@ def coda_arm(args, rank, world, local_rank):
             fullsize["vs"] = (f"token-chunked fused-order CPU oracle of the whole block: the {len(res)} weight and "
                               f"gain gradients after the {world}-rank {type(hook).__name__} reduction of "
                               "token-sharded backward passes (sketch + sampled rows)")
+    elif rank == 0 and world == 1 and not args.no_parity and args.tokens is None and have_fixture:
+        # the measured configuration itself, every output, against the pinned oracle (not timed)
+        fullsize = fullsize_summary(fullsize_parity(args.config, "fold" if args.fold_gamma else "plain"))
 
     if rank == 0:
         line = {

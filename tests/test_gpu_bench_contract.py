@@ -85,3 +85,13 @@ def test_bench_two_ranks_full_size_dp_parity(cuda_ready):
     pf = out["parity_fullsize"]
     assert pf is not None and pf["outputs"] == 6 and pf["pass"] is True, pf
     assert pf["rel_err_max"] <= 2e-2
+
+
+def test_bench_force_dist_full_size_parity(cuda_ready):
+    """A one-rank NCCL group with the default N > 1 hook (f32 reduce-scatter, bf16 rounding,
+    bf16 all-gather): the reduced full-size C4 weight and gain gradients match the oracle
+    fixture exactly as well as the plain single-GPU path does."""
+    out = _bench("--force-dist", "--steps", "3", "--warmup", "3", "--no-cpu", "--ab-rounds", "0")
+    pf = out["parity_fullsize"]
+    assert out["wgrad_reduce"] == "WgradReduceScatter"
+    assert pf["outputs"] == 6 and pf["pass"] is True and pf["rel_err_max"] <= 3.5e-3, pf
