@@ -75,3 +75,35 @@ def test_lm_head_backward_finite_differences(cuda_ready):
             scale = max(abs(fd), float(np.linalg.norm(g)) / np.sqrt(g.size))
             worst = max(worst, abs(fd - float(np.sum(g * u))) / scale)
     assert worst <= 1e-4, worst
+
+
+def test_lm_head_forward_full_size_sampled_rows(cuda_ready):
+    """The LM head at the benchmarked size (16384 tokens, d 4096, vocabulary 32768: K8 runs
+    16384 x 32768 x 4096 with the logits never stored): every statistic is per row, so 256
+    sampled rows of the GPU's per-token losses and log-sum-exps are checked against the
+    fused-order oracle run on exactly those rows over the whole vocabulary."""
+    import torch
+
+    import paper_2605_19269_b200 as cd
+
+    P = cd.PrecisionMode.SIMBF16
+    m, k, d, v = 16384, 4096, 4096, 32768
+    rng = np.random.default_rng(17)
+    qz = lambda x: O.q(x, O.SIMBF16)  # noqa: E731
+    a = qz(rng.standard_normal((m, k), dtype=np.float32))
+    b = qz(rng.standard_normal((k, d), dtype=np.float32) * 0.02)
+    z = qz(rng.standard_normal((m, d), dtype=np.float32))
+    gamma = qz(1 + 0.1 * rng.standard_normal(d))
+    wv = qz(rng.standard_normal((d, v), dtype=np.float32) * 0.02)
+    labels = rng.integers(0, v, m)
+    M = lambda x: cd.DenseMatrix.from_array(x, P)  # noqa: E731
+    cfg = cd.PipelineConfig(hidden=d, precision=P)
+    fwd = cd.lm_head_forward(M(a), M(b), M(z), cd.Vector.from_array(gamma, P), M(wv), labels, config=cfg)
+    torch.cuda.synchronize()
+    rows = np.sort(rng.choice(m, 256, replace=False))
+    of = O.lm_head_forward(a[rows], b, z[rows], gamma, wv, labels[rows], O.SIMBF16)
+    got_loss = fwd.losses.tensor.double().cpu().numpy()[rows]
+    got_lse = fwd.lse.tensor.double().cpu().numpy()[rows]
+    assert O.rel_error(got_lse, of["lse"]) <= 1e-5, O.rel_error(got_lse, of["lse"])
+    assert O.rel_error(got_loss, of["losses"]) <= 2e-2, O.rel_error(got_loss, of["losses"])
+    assert np.isfinite(fwd.mean_loss) and abs(fwd.mean_loss - np.log(v)) < 2.0
