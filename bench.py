@@ -492,7 +492,7 @@ def reference_arm(args, rank, world):
     line = {
         "impl": "reference", "metric": "block fwd+bwd tokens/s", "value": value, "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (bf16 storage grid)",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32 (bf16 storage grid)",
         "data": "synthetic", "config": {"workload": label, "tokens_sampled_per_step": sample},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
                          "sample": f"{sample} tokens of the {args.config} block per step, numpy/OpenBLAS all cores"},
