@@ -388,8 +388,9 @@ def fullsize_parity(name: str, variant: str = "plain") -> dict:
     del acts_np
     m, d = acts["x"].shape
     f = (ws[0] if isinstance(ws, list) else ws).w_gate_up.cols
-    cfg = cd.PipelineConfig(hidden=d, ffn=f, precision=P, fold_gamma=(variant == "fold"))
-    cos, sin = cd.qkv_rope_tables(m, d, precision=P)
+    kv = FS.KV.get(name)
+    cfg = cd.PipelineConfig(hidden=d, ffn=f, precision=P, fold_gamma=(variant == "fold"), kv_width=kv)
+    cos, sin = cd.qkv_rope_tables(m, d, precision=P, kv_width=kv)
     hook = NullReduce() if variant == "f32_hook" else None
     got = {}
     if isinstance(ws, list):
@@ -432,8 +433,9 @@ def fullsize_parity_dp(name: str, hook, rank: int, world: int, device) -> dict:
             for k in ("x", "z", "grad_qkv", "grad_residual")}
     del acts_np
     d = acts["x"].shape[1]
-    cfg = cd.PipelineConfig(hidden=d, ffn=ws.w_gate_up.cols, precision=P)
-    cos, sin = cd.qkv_rope_tables(sh.rows, d, start=sh.start, precision=P)
+    kv = FS.KV.get(name)
+    cfg = cd.PipelineConfig(hidden=d, ffn=ws.w_gate_up.cols, precision=P, kv_width=kv)
+    cos, sin = cd.qkv_rope_tables(sh.rows, d, start=sh.start, precision=P, kv_width=kv)
     fwd = cd.layer_forward(acts["x"], acts["z"], ws, cos, sin, config=cfg)
     bwd = cd.layer_backward(acts["grad_qkv"], fwd.tape, ws, grad_residual=acts["grad_residual"], config=cfg,
                             wgrad_hook=hook)
@@ -920,7 +922,7 @@ def coda_arm(args, rank, world, local_rank):
     fullsize = None
     have_fixture = (ROOT / "tests" / "golden" / f"fullsize_{args.config}.npz").exists()
     if dist is not None and hook is not None and not args.no_parity and args.tokens is None and \
-            args.scaling == "strong" and not fp32 and not args.fold_gamma and args.config in ("c3", "c4") and \
+            args.scaling == "strong" and not fp32 and not args.fold_gamma and args.config in ("c3", "c4", "c4gqa") and \
             have_fixture:
         # every rank runs its shard of the fixture's batch; the reduced weight and gain gradients
         # must equal the single-GPU oracle's (not timed; a collective, so all ranks take part)

@@ -40,8 +40,10 @@ CONFIGS = {
     "c3": (8192, 2048, 8192),
     "c4": (16384, 4096, 14336),
     "c5": (8192, 4096, 14336),     # per block of the 4-block stack, 8192 tokens per GPU
+    "c4gqa": (16384, 4096, 14336),  # C4 with the GQA extension: k / v spans 1024 wide
 }
 BLOCKS = {"c5": 4}
+KV = {"c4gqa": 1024}               # k / v span width (default: hidden, the reference's packed 3d)
 
 # order of the generated tensors (stream index = position)
 TENSORS = ("w_out", "gamma_ffn", "w_gate_up", "w_down", "gamma_qkv", "w_qkv", "x", "z", "grad_qkv",
@@ -77,8 +79,9 @@ def make_inputs(name: str, seed: int = 0, mode: str = O.SIMBF16, scale: float = 
     quantized to the storage grid of `mode`.  Float32 arrays (every grid value is exact in f32)."""
     m, d, inter = CONFIGS[name]
     f = 2 * inter
+    qw = d + 2 * KV.get(name, d)     # packed q | k | v width
     shapes = {"w_out": (d, d), "gamma_ffn": (d,), "w_gate_up": (d, f), "w_down": (inter, d), "gamma_qkv": (d,),
-              "w_qkv": (d, 3 * d), "x": (m, d), "z": (m, d), "grad_qkv": (m, 3 * d), "grad_residual": (m, d)}
+              "w_qkv": (d, qw), "x": (m, d), "z": (m, d), "grad_qkv": (m, qw), "grad_residual": (m, d)}
     out = {}
     for i, key in enumerate(TENSORS):
         if weights_only and not (key.startswith("w_") or key.startswith("gamma")):
@@ -150,12 +153,14 @@ def run_layer_chunked(inp: dict, mode: str = O.SIMBF16, chunk: int = 1024, eps: 
         raise ValueError("chunk must be a multiple of the 128-row tile (gain-gradient partials)")
     w = weights_of(inp)
     m, d = inp["x"].shape
+    kv = (w["w_qkv"].shape[1] - d) // 2
+    kv_width = None if kv == d else kv      # GQA extension: the k / v span width
     acc = {k: None for k in WGRADS}
     gparts = {k: [] for k in GAINS}
     rows = {k: [] for k in ROW_LOCAL} if on_rows is None else None
     for r0 in range(0, m, chunk):
         r1 = min(m, r0 + chunk)
-        cos, sin = O.qkv_rope_tables(r1 - r0, d, mode, start=r0)
+        cos, sin = O.qkv_rope_tables(r1 - r0, d, mode, start=r0, kv_width=kv_width)
         f = O.layer_forward(inp["x"][r0:r1], inp["z"][r0:r1], w, cos, sin, mode, eps=eps)
         b = _backward_parts(inp["grad_qkv"][r0:r1], f, w, mode, inp["grad_residual"][r0:r1])
         for k in WGRADS:

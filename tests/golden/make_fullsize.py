@@ -9,7 +9,7 @@ norm and a few full sampled rows (gain gradients are stored whole).  The GPU tes
 (tests/test_gpu_fullsize_parity.py) regenerates the same bf16 inputs from the
 same seeds on the box, runs the CUDA path, and compares against these.
 
-    python tests/golden/make_fullsize.py [c3] [c4]
+    python tests/golden/make_fullsize.py [c3] [c4] [c5] [c4gqa]
 """
 
 from __future__ import annotations

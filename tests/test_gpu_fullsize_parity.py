@@ -62,8 +62,9 @@ def _check(res: dict, label: str):
             assert abs(r["norm_ratio"] - 1.0) <= TOL, (label, k, r)
 
 
-@pytest.mark.parametrize("name", ["c4", "c3"])
+@pytest.mark.parametrize("name", ["c4", "c3", "c4gqa"])
 def test_fullsize_block_vs_oracle(cuda_ready, name):
+    """c4gqa: the GQA extension (k / v spans of 1024) at C4 size, fixture fullsize_c4gqa.npz."""
     t0 = time.time()
     _check(run_fullsize(name), f"{name} full block vs chunked fused-order oracle ({time.time() - t0:.0f}s)")
 

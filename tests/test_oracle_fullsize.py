@@ -105,3 +105,24 @@ def test_stack_chunked_equals_chained_oracle():
         for k in FS.WGRADS:
             assert O.rel_error(res[f"{k}.{b}"], g[k]) < 2e-3, (k, b)
         gq, gr = np.concatenate([np.zeros((m, 2 * d)), g["x"]], axis=1), g["z"]
+
+
+def test_chunked_equals_unchunked_gqa():
+    """The GQA extension layout (k / v spans narrower than hidden) through the chunked driver."""
+    FS.CONFIGS["_g"], FS.KV["_g"] = (512, 128, 256), 32
+    try:
+        inp = FS.make_inputs("_g", seed=5, mode=O.SIMBF16, scale=0.2)
+    finally:
+        del FS.CONFIGS["_g"], FS.KV["_g"]
+    m, d = inp["x"].shape
+    assert inp["w_qkv"].shape == (d, d + 64) and inp["grad_qkv"].shape == (m, d + 64)
+    w = FS.weights_of(inp)
+    cos, sin = O.qkv_rope_tables(m, d, O.SIMBF16, kv_width=32)
+    f = O.layer_forward(inp["x"], inp["z"], w, cos, sin, O.SIMBF16)
+    b = O.layer_backward(inp["grad_qkv"], f, w, O.SIMBF16, grad_residual=inp["grad_residual"])
+    res = FS.run_layer_chunked(inp, O.SIMBF16, chunk=128)
+    assert np.array_equal(res["qkv"], f["qkv"])
+    for k in ("x", "z", "gamma_ffn", "gamma_qkv"):
+        assert np.array_equal(res[k], b[k]), k
+    for k in FS.WGRADS:
+        assert O.rel_error(res[k], b[k]) < 2e-3, k
